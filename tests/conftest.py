@@ -1,0 +1,22 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built CUDA library")
+    config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+@pytest.fixture(scope="session")
+def cuda_device():
+    """GPU tests fail loudly (never skip) when no CUDA device is visible."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("gpu-marked test selected but torch.cuda.is_available() is False")
+    return torch.device("cuda:0")
