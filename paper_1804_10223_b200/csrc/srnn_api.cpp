@@ -1,0 +1,564 @@
+// srnn_api.cpp -- the C ABI declared in include/srnn.h: plan creation and
+// capacity planning, weight loading through the packer
+// (a2), and the forward entry points that enqueue the input-projection GEMM
+// (a1) and the persistent recurrent kernel (a3-a9).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/srnn.h"
+#include "srnn_internal.h"
+#include "srnn_packer.h"
+
+using namespace srnn;
+
+struct srnn_plan {
+    srnn_config_t cfg{};
+    int G = 1;
+    int sm_count = 148;
+    int smem_optin = 232448;  // B200: 227 KB per block opt-in
+    int BT = 4, n_tiles_max = 1;
+    bool host_only = false;
+    bool loaded = false;
+    // layout decisions
+    Layout lay;
+    int np_inst = 0;
+    int regs = 0;
+    size_t smem_bytes = 0;
+    int64_t nnz = 0;
+    // device buffers
+    void* d_img = nullptr;          // uint2 (fp32) or uint32 (fp16) image
+    int32_t* d_unit0 = nullptr;
+    int32_t* d_wslots = nullptr;
+    float* d_wx = nullptr;
+    float* d_bias = nullptr;
+    float* d_bprime = nullptr;      // [T_max][B_max][G*H]
+    unsigned long long* d_xbuf = nullptr;
+    int32_t* d_status = nullptr;
+    size_t xbuf_words = 0;
+    uint32_t epoch = 1;
+    // host-call staging (srnn_forward_host)
+    cudaStream_t stream = nullptr;
+    float *d_x = nullptr, *d_h0 = nullptr, *d_c0 = nullptr, *d_y = nullptr, *d_hT = nullptr, *d_cT = nullptr;
+    unsigned long long timeout_ns = 2000000000ull;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int max_threads_for_np(int np) { return np <= 8 ? 1024 : np <= 16 ? 768 : np <= 32 ? 512 : np <= 48 ? 352 : 320; }
+
+int inst_for(int slots) {
+    for (int i = 0; i < kNumNP; ++i)
+        if (kNPList[i] >= slots) return kNPList[i];
+    return -1;
+}
+
+size_t smem_for(const srnn_plan* p, int units_max, int bt, int n_tiles) {
+    size_t s = static_cast<size_t>(p->cfg.hidden) * bt * 4;
+    s += static_cast<size_t>(p->G) * units_max * bt * 4;
+    if (p->G == 4) s += static_cast<size_t>(n_tiles) * units_max * bt * 4;
+    return s + 16;
+}
+
+void free_device(srnn_plan* p) {
+    cudaFree(p->d_img);
+    cudaFree(p->d_unit0);
+    cudaFree(p->d_wslots);
+    cudaFree(p->d_wx);
+    cudaFree(p->d_bias);
+    cudaFree(p->d_bprime);
+    cudaFree(p->d_xbuf);
+    cudaFree(p->d_status);
+    cudaFree(p->d_x);
+    cudaFree(p->d_h0);
+    cudaFree(p->d_c0);
+    cudaFree(p->d_y);
+    cudaFree(p->d_hT);
+    cudaFree(p->d_cT);
+    if (p->stream) cudaStreamDestroy(p->stream);
+    p->d_img = nullptr;
+}
+
+// Estimated cycles of one tile-step on the busiest CTA (planner cost model,
+// DESIGN.md Sec. 5): shared-memory wavefronts vs issue, plus the reduction
+// latency, plus the exchange round trip.
+double cost_model(const Layout& lay, int bt, int H, int n_tiles) {
+    const double wf = static_cast<double>(lay.wavefronts_max_cta);
+    const double issue = static_cast<double>(lay.issue_max_cta) * (1 + bt) / 4.0;
+    int lg = 0;
+    while ((1 << lg) < lay.lanes_per_row) ++lg;
+    const double reduce = lg * (30.0 + 2.0 * bt);
+    const double chain = lay.slots_used * 4.0;
+    const double ingress = static_cast<double>(H) * bt * 8.0 / 64.0;
+    const double sync = lay.num_ctas > 1 ? 900.0 + 2.0 * lay.num_ctas : 600.0;
+    return n_tiles * (std::max(std::max(wf, issue), chain) + reduce + ingress + sync);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* srnn_status_string(srnn_status_t s) {
+    switch (s) {
+        case SRNN_OK: return "SRNN_OK";
+        case SRNN_ERR_INVALID_VALUE: return "SRNN_ERR_INVALID_VALUE";
+        case SRNN_ERR_NOT_ON_CHIP: return "SRNN_ERR_NOT_ON_CHIP";
+        case SRNN_ERR_BAD_WEIGHTS: return "SRNN_ERR_BAD_WEIGHTS";
+        case SRNN_ERR_STATE: return "SRNN_ERR_STATE";
+        case SRNN_ERR_CUDA: return "SRNN_ERR_CUDA";
+        case SRNN_ERR_TIMEOUT: return "SRNN_ERR_TIMEOUT";
+        case SRNN_ERR_UNSUPPORTED: return "SRNN_ERR_UNSUPPORTED";
+    }
+    return "SRNN_ERR_UNKNOWN";
+}
+
+const char* srnn_version(void) { return "srnn 0.1 sm_100a"; }
+
+srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
+    if (cfg == nullptr || out == nullptr) return SRNN_ERR_INVALID_VALUE;
+    *out = nullptr;
+    const srnn_config_t& c = *cfg;
+    if (c.hidden < 1 || c.hidden > 65536 || c.input < 1 || c.batch < 1 || c.max_steps < 0) return SRNN_ERR_INVALID_VALUE;
+    if (!(c.density >= 0.0f && c.density <= 1.0f)) return SRNN_ERR_INVALID_VALUE;
+    if (c.cell != SRNN_CELL_RNN && c.cell != SRNN_CELL_LSTM) return SRNN_ERR_INVALID_VALUE;
+    if (c.act < SRNN_ACT_RELU || c.act > SRNN_ACT_IDENTITY) return SRNN_ERR_INVALID_VALUE;
+    if (c.prec != SRNN_PREC_FP32 && c.prec != SRNN_PREC_FP16W_FP32ACC) return SRNN_ERR_INVALID_VALUE;
+    if (c.lanes_per_row != 0 &&
+        (c.lanes_per_row < 1 || c.lanes_per_row > 32 || (c.lanes_per_row & (c.lanes_per_row - 1)) != 0))
+        return SRNN_ERR_INVALID_VALUE;
+    if (c.num_ctas < 0) return SRNN_ERR_INVALID_VALUE;
+
+    srnn_plan* p = new (std::nothrow) srnn_plan();
+    if (!p) return SRNN_ERR_INVALID_VALUE;
+    p->cfg = c;
+    p->G = c.cell == SRNN_CELL_LSTM ? 4 : 1;
+    p->host_only = (c.flags & SRNN_FLAG_HOST_ONLY) != 0;
+    if (const char* t = std::getenv("SRNN_TIMEOUT_MS")) p->timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
+    if (!p->host_only) {
+        DeviceGuard g(c.device);
+        if (!g.ok) {
+            delete p;
+            return SRNN_ERR_CUDA;
+        }
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, c.device) != cudaSuccess) {
+            delete p;
+            return SRNN_ERR_CUDA;
+        }
+        p->sm_count = prop.multiProcessorCount;
+        p->smem_optin = static_cast<int>(prop.sharedMemPerBlockOptin);
+        if (!prop.cooperativeLaunch) {
+            delete p;
+            return SRNN_ERR_UNSUPPORTED;
+        }
+    }
+    if (c.num_ctas > p->sm_count) {
+        delete p;
+        return SRNN_ERR_INVALID_VALUE;
+    }
+    // Batch tile: the paper's wide load interleaves 4 samples;
+    // narrower tiles when B_max < 4 or when h staging would not fit.
+    int bt = c.batch >= 4 ? 4 : (c.batch >= 2 ? 2 : 1);
+    const int umax_guess = (c.hidden + p->sm_count - 1) / p->sm_count;
+    while (bt > 1 && smem_for(p, umax_guess, bt, (c.batch + bt - 1) / bt) > static_cast<size_t>(p->smem_optin)) bt /= 2;
+    p->BT = bt;
+    p->n_tiles_max = (c.batch + bt - 1) / bt;
+    if (smem_for(p, umax_guess, bt, p->n_tiles_max) > static_cast<size_t>(p->smem_optin)) {
+        delete p;
+        return SRNN_ERR_NOT_ON_CHIP;  // h staging alone exceeds shared memory
+    }
+    // Register budget for the expected pairs: two registers per pair in the
+    // hoisted format, at most ~75% of each SM's 64K registers.
+    const double exp_pairs = static_cast<double>(c.density) * p->G * c.hidden * static_cast<double>(c.hidden);
+    const double reg_capacity_pairs = 0.75 * 65536.0 * p->sm_count / 2.0;
+    if (exp_pairs > reg_capacity_pairs) {
+        delete p;
+        return SRNN_ERR_NOT_ON_CHIP;
+    }
+    if (!p->host_only) {
+        DeviceGuard g(c.device);
+        const size_t tile_stride = (static_cast<size_t>(c.hidden) * bt + 1) & ~static_cast<size_t>(1);
+        p->xbuf_words = 2 * static_cast<size_t>(p->n_tiles_max) * tile_stride;
+        const size_t bp_elems = static_cast<size_t>(std::max(1, c.max_steps)) * c.batch * p->G * c.hidden;
+        if (cudaMalloc(&p->d_xbuf, p->xbuf_words * 8) != cudaSuccess ||
+            cudaMalloc(&p->d_status, sizeof(int32_t)) != cudaSuccess ||
+            cudaMalloc(&p->d_bprime, bp_elems * sizeof(float)) != cudaSuccess ||
+            cudaMemset(p->d_xbuf, 0, p->xbuf_words * 8) != cudaSuccess ||
+            cudaMemset(p->d_status, 0, sizeof(int32_t)) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            free_device(p);
+            delete p;
+            return SRNN_ERR_CUDA;
+        }
+    }
+    *out = p;
+    return SRNN_OK;
+}
+
+srnn_status_t srnn_plan_query(srnn_plan_t p, srnn_plan_info_t* out) {
+    if (!p || !out) return SRNN_ERR_INVALID_VALUE;
+    std::memset(out, 0, sizeof(*out));
+    out->sm_count = p->sm_count;
+    out->batch_tile = p->BT;
+    out->num_batch_tiles = p->n_tiles_max;
+    out->fits = 1;
+    if (p->loaded) {
+        const Layout& l = p->lay;
+        out->num_ctas = l.num_ctas;
+        out->threads_per_cta = l.threads;
+        out->lanes_per_row = l.lanes_per_row;
+        out->pairs_per_lane = p->np_inst;
+        out->slots_used = l.slots_used;
+        int umax = 0;
+        for (int c = 0; c < l.num_ctas; ++c) umax = std::max(umax, l.cta_unit0[c + 1] - l.cta_unit0[c]);
+        out->units_per_cta_max = umax;
+        out->regs_per_thread = p->regs;
+        out->packed_registers = 0;
+        out->nnz = p->nnz;
+        out->slots_total = l.slots_total;
+        out->smem_bytes_per_cta = static_cast<int64_t>(p->smem_bytes);
+        out->weight_image_bytes = static_cast<int64_t>(l.num_ctas) * p->np_inst * l.threads *
+                                  (p->cfg.prec == SRNN_PREC_FP32 ? 8 : 4);
+        out->wavefronts_per_step_max = l.wavefronts_max_cta;
+        out->wavefronts_per_step_ideal = l.wavefronts_ideal_cta;
+        out->conflict_wavefronts = l.conflicts_max_cta;
+    }
+    return SRNN_OK;
+}
+
+srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int32_t* col, const float* val,
+                                int64_t nnz, const float* wx, const float* bias) {
+    if (!p || !rowptr || (nnz > 0 && (!col || !val)) || !wx || nnz < 0) return SRNN_ERR_INVALID_VALUE;
+    const int H = p->cfg.hidden, G = p->G, R = G * H;
+    // ---- validate CSR (S:125 duplicates; rowptr monotone; col range) ----
+    if (rowptr[0] != 0 || rowptr[R] != nnz) return SRNN_ERR_BAD_WEIGHTS;
+    for (int r = 0; r < R; ++r) {
+        if (rowptr[r + 1] < rowptr[r]) return SRNN_ERR_BAD_WEIGHTS;
+        std::vector<int32_t> cs(col + rowptr[r], col + rowptr[r + 1]);
+        for (int32_t v : cs)
+            if (v < 0 || v >= H) return SRNN_ERR_BAD_WEIGHTS;
+        std::sort(cs.begin(), cs.end());
+        for (size_t i = 1; i < cs.size(); ++i)
+            if (cs[i] == cs[i - 1]) return SRNN_ERR_BAD_WEIGHTS;
+    }
+    const bool fp16 = p->cfg.prec == SRNN_PREC_FP16W_FP32ACC;
+    // fp16 mode: RNE-quantise the values once.
+    std::vector<float> qval(val, val + nnz);
+    if (fp16)
+        for (auto& v : qval) v = half_to_float(float_to_half_rne(v));
+    PackInput in;
+    in.H = H;
+    in.G = G;
+    in.rowptr = rowptr;
+    in.col = col;
+    in.val = qval.data();
+    in.BT = p->BT;
+    in.naive = (p->cfg.flags & SRNN_FLAG_NAIVE_LAYOUT) != 0;
+
+    // ---- search (num_ctas, lanes_per_row, slot budget) ----
+    std::vector<int> cands_c;
+    if (p->cfg.num_ctas > 0) {
+        cands_c.push_back(p->cfg.num_ctas);
+    } else {
+        const int cmax = std::min(p->sm_count, H);
+        cands_c.push_back(cmax);
+        for (int cc = cmax / 2; cc >= 1; cc /= 2) cands_c.push_back(cc);
+    }
+    std::vector<int> cands_l;
+    if (p->cfg.lanes_per_row > 0)
+        cands_l.push_back(p->cfg.lanes_per_row);
+    else
+        cands_l = {32, 16, 8, 4, 2, 1};
+    double best_cost = 1e300;
+    Layout best;
+    int best_inst = 0;
+    bool any = false;
+    for (int C : cands_c) {
+        const int umax = (H + C - 1) / C;
+        const size_t smem = smem_for(p, umax, p->BT, p->n_tiles_max);
+        if (smem > static_cast<size_t>(p->smem_optin)) continue;
+        for (int L : cands_l) {
+            const int rows_max = G * umax;
+            const int threads = ((rows_max * L + 31) / 32) * 32;
+            if (threads > 1024) continue;
+            const int np0 = std::max(1, min_np(in, L));
+            if (np0 > kNPList[kNumNP - 1]) continue;
+            const int np_hi = in.naive ? np0 : std::min(kNPList[kNumNP - 1], np0 + std::max(2, np0 / 4));
+            for (int np = np0; np <= np_hi; ++np) {
+                const int inst = inst_for(np);
+                if (inst < 0 || threads > max_threads_for_np(inst)) break;
+                Layout lay;
+                if (!pack_layout(in, C, L, np, &lay)) continue;
+                const int inst_used = inst_for(std::max(1, lay.slots_used));
+                if (inst_used < 0 || lay.threads > max_threads_for_np(inst_used)) continue;
+                const double cst = cost_model(lay, p->BT, H, p->n_tiles_max);
+                if (cst < best_cost) {
+                    best_cost = cst;
+                    best = std::move(lay);
+                    best_inst = inst_used;
+                    any = true;
+                }
+            }
+        }
+    }
+    if (!any) return SRNN_ERR_NOT_ON_CHIP;
+    // Re-pack at the chosen instance width so the image has np_inst slots.
+    Layout fin;
+    {
+        // pack with the same budget, then widen the image to np_inst slots (padding)
+        fin = best;
+        if (best.np_budget != best_inst) {
+            Layout w = best;
+            w.np_budget = best_inst;
+            const size_t n = static_cast<size_t>(w.num_ctas) * best_inst * w.threads;
+            w.col.assign(n, 0);
+            w.val.assign(n, 0.0f);
+            w.row.assign(n, -1);
+            const int nslot = std::min(best.np_budget, best_inst);
+            for (int c = 0; c < w.num_ctas; ++c)
+                for (int i = 0; i < nslot; ++i)
+                    for (int t = 0; t < w.threads; ++t) {
+                        w.col[w.idx(c, i, t)] = best.col[best.idx(c, i, t)];
+                        w.val[w.idx(c, i, t)] = best.val[best.idx(c, i, t)];
+                        w.row[w.idx(c, i, t)] = best.row[best.idx(c, i, t)];
+                    }
+            fin = std::move(w);
+        }
+    }
+    int umax = 0;
+    for (int c = 0; c < fin.num_ctas; ++c) umax = std::max(umax, fin.cta_unit0[c + 1] - fin.cta_unit0[c]);
+    p->smem_bytes = smem_for(p, umax, p->BT, p->n_tiles_max);
+    p->np_inst = best_inst;
+    p->lay = std::move(fin);
+    p->nnz = nnz;
+    p->regs = 2 * best_inst + 58;  // host-only estimate; replaced by the compiled count below
+
+    if (!p->host_only) {
+        DeviceGuard g(p->cfg.device);
+        const Layout& l = p->lay;
+        const size_t n = static_cast<size_t>(l.num_ctas) * p->np_inst * l.threads;
+        cudaFree(p->d_img);
+        cudaFree(p->d_unit0);
+        cudaFree(p->d_wslots);
+        cudaFree(p->d_wx);
+        cudaFree(p->d_bias);
+        p->d_img = nullptr;
+        p->d_unit0 = p->d_wslots = nullptr;
+        p->d_wx = p->d_bias = nullptr;
+        cudaError_t e = cudaSuccess;
+        if (fp16) {
+            std::vector<uint32_t> img(n);
+            for (size_t i = 0; i < n; ++i)
+                img[i] = (static_cast<uint32_t>(l.col[i]) << 16) | float_to_half_rne(l.val[i]);
+            e = cudaMalloc(&p->d_img, n * 4);
+            if (e == cudaSuccess) e = cudaMemcpy(p->d_img, img.data(), n * 4, cudaMemcpyHostToDevice);
+        } else {
+            std::vector<uint2> img(n);
+            for (size_t i = 0; i < n; ++i) {
+                uint32_t b;
+                std::memcpy(&b, &l.val[i], 4);
+                img[i] = make_uint2(static_cast<uint32_t>(l.col[i]), b);
+            }
+            e = cudaMalloc(&p->d_img, n * 8);
+            if (e == cudaSuccess) e = cudaMemcpy(p->d_img, img.data(), n * 8, cudaMemcpyHostToDevice);
+        }
+        const size_t wx_n = static_cast<size_t>(R) * p->cfg.input;
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_unit0, l.cta_unit0.size() * 4);
+        if (e == cudaSuccess) e = cudaMemcpy(p->d_unit0, l.cta_unit0.data(), l.cta_unit0.size() * 4, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_wslots, l.warp_slots.size() * 4);
+        if (e == cudaSuccess) e = cudaMemcpy(p->d_wslots, l.warp_slots.data(), l.warp_slots.size() * 4, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_wx, wx_n * 4);
+        if (e == cudaSuccess) e = cudaMemcpy(p->d_wx, wx, wx_n * 4, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_bias, static_cast<size_t>(R) * 4);
+        if (e == cudaSuccess) {
+            if (bias)
+                e = cudaMemcpy(p->d_bias, bias, static_cast<size_t>(R) * 4, cudaMemcpyHostToDevice);
+            else
+                e = cudaMemset(p->d_bias, 0, static_cast<size_t>(R) * 4);
+        }
+        if (e != cudaSuccess) return SRNN_ERR_CUDA;
+        // Compiled register count and co-residency check for the instance.
+        RecParams rp{};
+        rp.threads = l.threads;
+        int regs = 0, maxb = 0;
+        int le = launch_recurrent(p->np_inst, p->BT, G, 0, rp, l.num_ctas, p->smem_bytes, nullptr, true, &regs, &maxb);
+        if (le != 0) return SRNN_ERR_CUDA;
+        p->regs = regs;
+        if (maxb < 1) return SRNN_ERR_NOT_ON_CHIP;
+    }
+    p->loaded = true;
+    return SRNN_OK;
+}
+
+srnn_status_t srnn_input_projection(srnn_plan_t p, int32_t T, int32_t B, const float* x, float* bprime, void* stream) {
+    if (!p) return SRNN_ERR_INVALID_VALUE;
+    if (!p->loaded || p->host_only) return SRNN_ERR_STATE;
+    if (T < 0 || T > p->cfg.max_steps || B < 1 || B > p->cfg.batch || (T > 0 && (!x || !bprime)))
+        return SRNN_ERR_INVALID_VALUE;
+    if (T == 0) return SRNN_OK;
+    DeviceGuard g(p->cfg.device);
+    GemmParams gp;
+    gp.M = static_cast<int64_t>(T) * B;
+    gp.N = p->G * p->cfg.hidden;
+    gp.K = p->cfg.input;
+    gp.A = x;
+    gp.W = p->d_wx;
+    gp.bias = p->d_bias;
+    gp.C = bprime;
+    return launch_gemm_f32(gp, stream) == 0 ? SRNN_OK : SRNN_ERR_CUDA;
+}
+
+srnn_status_t srnn_recurrence(srnn_plan_t p, int32_t T, int32_t B, const float* bprime, const float* h0,
+                              const float* c0, float* y, float* hT, float* cT, void* stream) {
+    if (!p) return SRNN_ERR_INVALID_VALUE;
+    if (!p->loaded || p->host_only) return SRNN_ERR_STATE;
+    if (T < 0 || T > p->cfg.max_steps || B < 1 || B > p->cfg.batch || (T > 0 && !bprime)) return SRNN_ERR_INVALID_VALUE;
+    DeviceGuard g(p->cfg.device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t hb = static_cast<size_t>(B) * p->cfg.hidden * sizeof(float);
+    if (T == 0) {  // T = 0 returns h0 unchanged
+        cudaError_t e = cudaSuccess;
+        if (hT) e = h0 ? cudaMemcpyAsync(hT, h0, hb, cudaMemcpyDeviceToDevice, st) : cudaMemsetAsync(hT, 0, hb, st);
+        if (e == cudaSuccess && cT && p->G == 4)
+            e = c0 ? cudaMemcpyAsync(cT, c0, hb, cudaMemcpyDeviceToDevice, st) : cudaMemsetAsync(cT, 0, hb, st);
+        return e == cudaSuccess ? SRNN_OK : SRNN_ERR_CUDA;
+    }
+    if (static_cast<uint64_t>(p->epoch) + static_cast<uint64_t>(T) + 1 >= 0xffffffffull) {
+        if (cudaMemsetAsync(p->d_xbuf, 0, p->xbuf_words * 8, st) != cudaSuccess) return SRNN_ERR_CUDA;
+        p->epoch = 1;
+    }
+    RecParams rp{};
+    rp.H = p->cfg.hidden;
+    rp.G = p->G;
+    rp.B = B;
+    rp.T = T;
+    rp.n_tiles = (B + p->BT - 1) / p->BT;
+    rp.act = p->cfg.act;
+    rp.threads = p->lay.threads;
+    rp.lanes_per_row = p->lay.lanes_per_row;
+    rp.np_inst = p->np_inst;
+    int umax = 0;
+    for (int c = 0; c < p->lay.num_ctas; ++c) umax = std::max(umax, p->lay.cta_unit0[c + 1] - p->lay.cta_unit0[c]);
+    rp.units_max = umax;
+    rp.epoch = p->epoch;
+    rp.flags = p->cfg.flags;
+    if (p->cfg.prec == SRNN_PREC_FP32)
+        rp.img_f32 = static_cast<const uint2*>(p->d_img);
+    else
+        rp.img_f16 = static_cast<const uint32_t*>(p->d_img);
+    rp.cta_unit0 = p->d_unit0;
+    rp.warp_slots = p->d_wslots;
+    rp.bprime = bprime;
+    rp.h0 = h0;
+    rp.c0 = p->G == 4 ? c0 : nullptr;
+    rp.y = y;
+    rp.hT = hT;
+    rp.cT = p->G == 4 ? cT : nullptr;
+    rp.xbuf = p->d_xbuf;
+    rp.status = p->d_status;
+    rp.timeout_ns = p->timeout_ns;
+    int e = launch_recurrent(p->np_inst, p->BT, p->G, 0, rp, p->lay.num_ctas, p->smem_bytes, stream, false, nullptr,
+                             nullptr);
+    if (e != 0) return SRNN_ERR_CUDA;
+    p->epoch += static_cast<uint32_t>(T) + 1;
+    return SRNN_OK;
+}
+
+srnn_status_t srnn_forward(srnn_plan_t p, int32_t T, int32_t B, const float* x, const float* h0, const float* c0,
+                           float* y, float* hT, float* cT, void* stream) {
+    if (!p) return SRNN_ERR_INVALID_VALUE;
+    if (!p->loaded || p->host_only) return SRNN_ERR_STATE;
+    if (T < 0 || T > p->cfg.max_steps || B < 1 || B > p->cfg.batch || (T > 0 && !x)) return SRNN_ERR_INVALID_VALUE;
+    if (T > 0) {
+        srnn_status_t s = srnn_input_projection(p, T, B, x, p->d_bprime, stream);
+        if (s != SRNN_OK) return s;
+    }
+    return srnn_recurrence(p, T, B, p->d_bprime, h0, c0, y, hT, cT, stream);
+}
+
+srnn_status_t srnn_forward_host(srnn_plan_t p, int32_t T, int32_t B, const float* x_host, const float* h0_host,
+                                const float* c0_host, float* y_host, float* hT_host, float* cT_host) {
+    if (!p) return SRNN_ERR_INVALID_VALUE;
+    if (!p->loaded || p->host_only) return SRNN_ERR_STATE;
+    if (T < 0 || T > p->cfg.max_steps || B < 1 || B > p->cfg.batch || (T > 0 && !x_host)) return SRNN_ERR_INVALID_VALUE;
+    DeviceGuard g(p->cfg.device);
+    const int H = p->cfg.hidden, I = p->cfg.input;
+    const size_t xs = static_cast<size_t>(std::max(1, p->cfg.max_steps)) * p->cfg.batch * I * 4;
+    const size_t ys = static_cast<size_t>(std::max(1, p->cfg.max_steps)) * p->cfg.batch * H * 4;
+    const size_t hs = static_cast<size_t>(p->cfg.batch) * H * 4;
+    if (!p->d_x) {
+        if (cudaMalloc(&p->d_x, xs) != cudaSuccess || cudaMalloc(&p->d_y, ys) != cudaSuccess ||
+            cudaMalloc(&p->d_h0, hs) != cudaSuccess || cudaMalloc(&p->d_c0, hs) != cudaSuccess ||
+            cudaMalloc(&p->d_hT, hs) != cudaSuccess || cudaMalloc(&p->d_cT, hs) != cudaSuccess)
+            return SRNN_ERR_CUDA;
+    }
+    cudaStream_t st = p->stream;
+    const size_t xb = static_cast<size_t>(T) * B * I * 4, yb = static_cast<size_t>(T) * B * H * 4,
+                 hb = static_cast<size_t>(B) * H * 4;
+    cudaError_t e = cudaSuccess;
+    if (T > 0) e = cudaMemcpyAsync(p->d_x, x_host, xb, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && h0_host) e = cudaMemcpyAsync(p->d_h0, h0_host, hb, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && c0_host && p->G == 4) e = cudaMemcpyAsync(p->d_c0, c0_host, hb, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return SRNN_ERR_CUDA;
+    srnn_status_t s = srnn_forward(p, T, B, p->d_x, h0_host ? p->d_h0 : nullptr, c0_host ? p->d_c0 : nullptr,
+                                   y_host ? p->d_y : nullptr, p->d_hT, p->G == 4 ? p->d_cT : nullptr, st);
+    if (s != SRNN_OK) return s;
+    if (y_host && T > 0) e = cudaMemcpyAsync(y_host, p->d_y, yb, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && hT_host) e = cudaMemcpyAsync(hT_host, p->d_hT, hb, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && cT_host && p->G == 4) e = cudaMemcpyAsync(cT_host, p->d_cT, hb, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return SRNN_ERR_CUDA;
+    return srnn_plan_status(p);
+}
+
+srnn_status_t srnn_plan_status(srnn_plan_t p) {
+    if (!p) return SRNN_ERR_INVALID_VALUE;
+    if (p->host_only) return SRNN_OK;
+    DeviceGuard g(p->cfg.device);
+    int32_t s = 0;
+    if (cudaMemcpy(&s, p->d_status, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return SRNN_ERR_CUDA;
+    if (s != 0 && cudaMemset(p->d_status, 0, 4) != cudaSuccess) return SRNN_ERR_CUDA;
+    return static_cast<srnn_status_t>(s);
+}
+
+srnn_status_t srnn_plan_export_layout(srnn_plan_t p, int32_t* col_out, float* val_out, int32_t* row_out,
+                                      int64_t capacity) {
+    if (!p) return SRNN_ERR_INVALID_VALUE;
+    if (!p->loaded) return SRNN_ERR_STATE;
+    const int64_t n = static_cast<int64_t>(p->lay.col.size());
+    if (capacity < n) return SRNN_ERR_INVALID_VALUE;
+    if (col_out) std::memcpy(col_out, p->lay.col.data(), n * 4);
+    if (val_out) std::memcpy(val_out, p->lay.val.data(), n * 4);
+    if (row_out) std::memcpy(row_out, p->lay.row.data(), n * 4);
+    return SRNN_OK;
+}
+
+srnn_status_t srnn_destroy(srnn_plan_t p) {
+    if (!p) return SRNN_OK;
+    if (!p->host_only) {
+        DeviceGuard g(p->cfg.device);
+        free_device(p);
+    }
+    delete p;
+    return SRNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+// srnn_internal.h -- shared between the host planner (srnn_api.cpp) and the
+// CUDA kernels of the product path.  Never included by oracle/.
+#pragma once
+#include <cstdint>
+
+#ifndef SRNN_MAX_THREADS
+#define SRNN_MAX_THREADS 1024
+#endif
+
+namespace srnn {
+
+// Kernel arguments of the persistent recurrent kernel (one struct, passed by
+// value through cudaLaunchCooperativeKernel).
+struct RecParams {
+    // problem
+    int32_t H;        // hidden units
+    int32_t G;        // gates per unit (1 RNN, 4 LSTM)
+    int32_t B;        // batch of this call (<= n_tiles*BT)
+    int32_t T;        // timesteps of this call (>= 1)
+    int32_t n_tiles;  // batch tiles of width BT processed per step
+    int32_t act;      // srnn_act_t (RNN only)
+    int32_t threads;  // threads per CTA
+    int32_t lanes_per_row;  // L
+    int32_t np_inst;  // slots per lane in the image (= template NP)
+    int32_t units_max;      // max units of any CTA (smem sizing)
+    uint32_t epoch;   // tag of h_0 for this call; h_s carries epoch + s
+    uint32_t flags;   // SRNN_FLAG_* subset relevant on device
+    // packed weights: [cta][slot][thread]
+    const uint2* img_f32;      // fp32 mode: {col, float bits}
+    const uint32_t* img_f16;   // fp16 mode: (col << 16) | half bits
+    const int32_t* cta_unit0;  // [num_ctas + 1] first unit of each CTA
+    const int32_t* warp_slots; // [num_ctas][warps] slots used by each warp (warp-uniform)
+    // data
+    const float* bprime;  // [T][B][G*H]
+    const float* h0;      // [B][H] or null
+    const float* c0;      // [B][H] or null
+    float* y;             // [T][B][H] or null
+    float* hT;            // [B][H] or null
+    float* cT;            // [B][H] or null
+    unsigned long long* xbuf;  // tagged exchange words [2][n_tiles][H][BT]
+    int32_t* status;      // device status word (srnn_status_t)
+    unsigned long long timeout_ns;
+};
+
+struct GemmParams {
+    int64_t M;   // rows of x (T*B)
+    int32_t N;   // G*H
+    int32_t K;   // I
+    const float* A;      // [M][K] fp32
+    const float* W;      // [N][K] fp32
+    const float* bias;   // [N] or null
+    float* C;            // [M][N]
+};
+
+// Launch helpers implemented in the .cu files. Return cudaError_t as int.
+int launch_recurrent(int np, int bt, int g, int packed, const RecParams& p, int num_ctas,
+                     size_t smem_bytes, void* stream, bool query_only, int* regs_out,
+                     int* max_blocks_per_sm_out);
+int launch_gemm_f32(const GemmParams& p, void* stream);
+
+// Compiled register-slot instances (pairs per lane).
+constexpr int kNumNP = 8;
+constexpr int kNPList[kNumNP] = {4, 8, 12, 16, 24, 32, 48, 64};
+
+}  // namespace srnn

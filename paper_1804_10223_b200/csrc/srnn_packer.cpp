@@ -1,0 +1,298 @@
+// srnn_packer.cpp -- bank-aware packing of the pruned recurrent matrix into
+// the per-lane register slots of the persistent kernel.
+//
+// Paper basis:
+//   * <index, value> pairs, all pairs of a thread from one row.
+//   * rows padded with <index, 0> pairs so every lane runs the same slot count
+//     (PAPER.md:91); padding never changes the result.
+//   * bank-aware order: pairs of a row may be reordered freely ("reordering
+//     nonzeros' locations for each row does not affect the final result, but
+//     it can change the access sequence to shared memory");
+//     App. A Alg. 1 greedily places each pair in the
+//     "Color" column of its bank.
+//
+// Re-targeted to sm_100a: the kernel stages h as [H][BT] fp32, so one pair is
+// one LDS of 4*BT bytes (LDS.128 for BT = 4, the paper's ld.shared.v4 wide
+// load).  Shared memory serves 128 B per wavefront, so a warp
+// instruction is split into phases of P = 32/BT lanes; within a phase two
+// lanes conflict iff they read different columns j, j' with j = j' (mod P),
+// and lanes reading the same column broadcast.  Alg. 1's "bank" becomes the
+// residue col mod P and its "Color(bank)" column becomes the lane of a phase
+// group.  Unlike Alg. 1 (one row per warp), a phase group may hold several
+// rows (lanes_per_row < P), so the greedy works slot by slot: each (slot,
+// phase group) is filled first with pairs of pairwise-distinct residues
+// (largest remaining bucket first, round-robin over the rows of the group),
+// then -- only when a row would otherwise miss its slot budget -- with forced
+// pairs that cost an extra wavefront.  Free lanes get padding pairs that read
+// a column already read in the same phase (a broadcast, no extra wavefront).
+#include "srnn_packer.h"
+
+#include <algorithm>
+#include <cstring>
+
+namespace srnn {
+
+uint16_t float_to_half_rne(float f) {
+    uint32_t x;
+    std::memcpy(&x, &f, 4);
+    const uint32_t sign = (x >> 16) & 0x8000u;
+    const uint32_t ax = x & 0x7fffffffu;
+    if (ax >= 0x7f800000u) {  // inf or nan
+        return static_cast<uint16_t>(sign | 0x7c00u | (ax > 0x7f800000u ? 0x200u | ((ax >> 13) & 0x3ffu) : 0u));
+    }
+    if (ax >= 0x477ff000u) return static_cast<uint16_t>(sign | 0x7c00u);  // rounds to >= 65520 -> inf
+    if (ax < 0x38800000u) {                                                 // result subnormal or zero
+        if (ax < 0x33000000u) return static_cast<uint16_t>(sign);           // < 2^-25: rounds to 0
+        const uint32_t e = ax >> 23;
+        const uint32_t m = (ax & 0x7fffffu) | 0x800000u;
+        const uint32_t shift = 126 - e;  // 14 + (112 - e) ... value = m * 2^(e-150); half sub unit 2^-24
+        // number of half-subnormal units: m * 2^(e - 150 + 24) = m >> (126 - e)
+        uint32_t q = m >> shift;
+        const uint32_t rem = m & ((1u << shift) - 1u);
+        const uint32_t half = 1u << (shift - 1);
+        if (rem > half || (rem == half && (q & 1u))) ++q;
+        return static_cast<uint16_t>(sign | q);
+    }
+    // normal
+    uint32_t r = ax - 0x38000000u;  // rebias exponent 127 -> 15 (in float bit layout)
+    uint32_t q = r >> 13;
+    const uint32_t rem = r & 0x1fffu;
+    if (rem > 0x1000u || (rem == 0x1000u && (q & 1u))) ++q;
+    return static_cast<uint16_t>(sign | q);
+}
+
+float half_to_float(uint16_t h) {
+    const uint32_t sign = (static_cast<uint32_t>(h) & 0x8000u) << 16;
+    uint32_t e = (h >> 10) & 0x1fu;
+    uint32_t m = h & 0x3ffu;
+    uint32_t x;
+    if (e == 0) {
+        if (m == 0) {
+            x = sign;
+        } else {  // subnormal
+            e = 1;
+            while ((m & 0x400u) == 0) {
+                m <<= 1;
+                --e;
+            }
+            m &= 0x3ffu;
+            x = sign | ((e + 112) << 23) | (m << 13);
+        }
+    } else if (e == 31) {
+        x = sign | 0x7f800000u | (m << 13);
+    } else {
+        x = sign | ((e + 112) << 23) | (m << 13);
+    }
+    float f;
+    std::memcpy(&f, &x, 4);
+    return f;
+}
+
+namespace {
+
+inline int32_t global_row(int k, int U, int u0, int H) { return (k / U) * H + u0 + (k % U); }
+
+struct RowState {
+    int32_t grow = -1;                       // global row
+    std::vector<std::vector<int64_t>> bucket;  // per residue: CSR positions, ascending column
+    std::vector<size_t> head;                // consumed prefix per bucket
+    int64_t remaining = 0;
+    int lane0 = 0;                           // first lane of the row in the warp
+};
+
+}  // namespace
+
+int min_np(const PackInput& in, int L) {
+    int64_t mx = 0;
+    for (int r = 0; r < in.G * in.H; ++r) mx = std::max<int64_t>(mx, in.rowptr[r + 1] - in.rowptr[r]);
+    return static_cast<int>((mx + L - 1) / L);
+}
+
+bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
+    const int H = in.H, G = in.G;
+    const int P = 32 / in.BT;
+    const int ng = 32 / P;  // phase groups per warp instruction
+    const int rpw = 32 / L;
+    Layout& lay = *out;
+    lay = Layout();
+    lay.num_ctas = C;
+    lay.lanes_per_row = L;
+    lay.np_budget = NP;
+    lay.cta_unit0.resize(C + 1);
+    int umax = 0;
+    for (int c = 0; c <= C; ++c) lay.cta_unit0[c] = static_cast<int32_t>((static_cast<int64_t>(c) * H) / C);
+    for (int c = 0; c < C; ++c) umax = std::max(umax, lay.cta_unit0[c + 1] - lay.cta_unit0[c]);
+    const int rows_max = G * umax;
+    lay.warps = std::max(1, (rows_max + rpw - 1) / rpw);
+    lay.threads = lay.warps * 32;
+    const size_t n_img = static_cast<size_t>(C) * NP * lay.threads;
+    lay.col.assign(n_img, 0);
+    lay.val.assign(n_img, 0.0f);
+    lay.row.assign(n_img, -1);
+    lay.warp_slots.assign(static_cast<size_t>(C) * lay.warps, 0);
+
+    std::vector<RowState> rows(rpw);
+    std::vector<int32_t> gcol(P);       // column used per residue in current (slot, group); -1 none
+    std::vector<std::vector<int32_t>> distinct(P);
+    for (int c = 0; c < C; ++c) {
+        const int u0 = lay.cta_unit0[c];
+        const int U = lay.cta_unit0[c + 1] - u0;
+        const int n_rows = G * U;
+        int64_t wf_cta = 0, issue_cta = 0, pairs_cta = 0, conf_cta = 0;
+        for (int w = 0; w < lay.warps; ++w) {
+            const int k0 = w * rpw;
+            const int nr = std::max(0, std::min(rpw, n_rows - k0));
+            for (int q = 0; q < rpw; ++q) {
+                RowState& rs = rows[q];
+                rs.grow = -1;
+                rs.remaining = 0;
+                rs.lane0 = q * L;
+                rs.bucket.assign(P, {});
+                rs.head.assign(P, 0);
+                if (q >= nr) continue;
+                rs.grow = global_row(k0 + q, U, u0, H);
+                const int64_t b = in.rowptr[rs.grow], e = in.rowptr[rs.grow + 1];
+                rs.remaining = e - b;
+                pairs_cta += e - b;
+                if (e - b > static_cast<int64_t>(L) * NP) return false;
+                for (int64_t p = b; p < e; ++p) rs.bucket[in.col[p] % P].push_back(p);
+            }
+            // slot-major fill
+            int used_slots = 0;
+            int64_t wf_warp = 0;
+            std::vector<int64_t> wf_slot(NP, 0), conf_slot(NP, 0);
+            for (int i = 0; i < NP; ++i) {
+                bool any_real = false;
+                for (int g = 0; g < ng; ++g) {
+                    const int gl0 = g * P, gl1 = gl0 + P;
+                    std::fill(gcol.begin(), gcol.end(), -1);
+                    for (int r = 0; r < P; ++r) distinct[r].clear();
+                    // lanes of this group, per row
+                    auto place = [&](int q, int lane, int64_t pos) {
+                        const size_t at = lay.idx(c, i, w * 32 + lane);
+                        lay.col[at] = in.col[pos];
+                        lay.val[at] = in.val[pos];
+                        lay.row[at] = rows[q].grow;
+                        const int r = in.col[pos] % P;
+                        if (std::find(distinct[r].begin(), distinct[r].end(), in.col[pos]) == distinct[r].end())
+                            distinct[r].push_back(in.col[pos]);
+                        if (gcol[r] < 0) gcol[r] = in.col[pos];
+                        rows[q].remaining--;
+                        any_real = true;
+                    };
+                    std::vector<char> lane_used(P, 0);
+                    if (in.naive) {
+                        for (int lane = gl0; lane < gl1; ++lane) {
+                            const int q = lane / L;
+                            if (q >= nr) continue;
+                            const int64_t k = static_cast<int64_t>(i) * L + (lane - rows[q].lane0);
+                            const int64_t b = in.rowptr[rows[q].grow], e = in.rowptr[rows[q].grow + 1];
+                            if (b + k < e) {
+                                place(q, lane, b + k);
+                                lane_used[lane - gl0] = 1;
+                            }
+                        }
+                    } else {
+                        // pass 1: conflict-free, round-robin over the rows in the group
+                        bool progress = true;
+                        while (progress) {
+                            progress = false;
+                            for (int q = gl0 / L; q < nr && q * L < gl1; ++q) {
+                                RowState& rs = rows[q];
+                                if (rs.remaining == 0) continue;
+                                int lane = -1;
+                                for (int l = std::max(gl0, rs.lane0); l < std::min(gl1, rs.lane0 + L); ++l)
+                                    if (!lane_used[l - gl0]) {
+                                        lane = l;
+                                        break;
+                                    }
+                                if (lane < 0) continue;
+                                int best = -1;
+                                size_t best_n = 0;
+                                for (int r = 0; r < P; ++r) {
+                                    const size_t n = rs.bucket[r].size() - rs.head[r];
+                                    if (n == 0) continue;
+                                    const bool free_res = gcol[r] < 0 || gcol[r] == in.col[rs.bucket[r][rs.head[r]]];
+                                    if (free_res && n > best_n) {
+                                        best = r;
+                                        best_n = n;
+                                    }
+                                }
+                                if (best < 0) continue;
+                                place(q, lane, rs.bucket[best][rs.head[best]++]);
+                                lane_used[lane - gl0] = 1;
+                                progress = true;
+                            }
+                        }
+                        // pass 2: forced placements for rows behind their slot budget
+                        for (int q = gl0 / L; q < nr && q * L < gl1; ++q) {
+                            RowState& rs = rows[q];
+                            const int lanes_later_groups =
+                                std::max(0, rs.lane0 + L - std::max(gl1, rs.lane0));  // lanes of q in groups > g
+                            int64_t quota = rs.remaining - (static_cast<int64_t>(NP - i - 1) * L + lanes_later_groups);
+                            for (int l = std::max(gl0, rs.lane0); l < std::min(gl1, rs.lane0 + L) && quota > 0; ++l) {
+                                if (lane_used[l - gl0]) continue;
+                                int best = -1;
+                                size_t best_d = 0, best_n = 0;
+                                for (int r = 0; r < P; ++r) {
+                                    const size_t n = rs.bucket[r].size() - rs.head[r];
+                                    if (n == 0) continue;
+                                    const size_t d = distinct[r].size();
+                                    if (best < 0 || d < best_d || (d == best_d && n > best_n)) {
+                                        best = r;
+                                        best_d = d;
+                                        best_n = n;
+                                    }
+                                }
+                                if (best < 0) break;
+                                place(q, l, rs.bucket[best][rs.head[best]++]);
+                                lane_used[l - gl0] = 1;
+                                --quota;
+                            }
+                        }
+                    }
+                    // padding: broadcast a column already read in this phase
+                    int32_t pad = 0;
+                    for (int r = 0; r < P; ++r)
+                        if (gcol[r] >= 0) {
+                            pad = gcol[r];
+                            break;
+                        }
+                    int64_t wf = 1;
+                    for (int r = 0; r < P; ++r) wf = std::max<int64_t>(wf, static_cast<int64_t>(distinct[r].size()));
+                    wf_slot[i] += wf;
+                    conf_slot[i] += wf - 1;
+                    for (int lane = gl0; lane < gl1; ++lane) {
+                        if (lane_used[lane - gl0]) continue;
+                        const size_t at = lay.idx(c, i, w * 32 + lane);
+                        lay.col[at] = pad;
+                        lay.val[at] = 0.0f;
+                        const int q = lane / L;
+                        lay.row[at] = q < nr ? rows[q].grow : -1;
+                    }
+                }
+                if (any_real) used_slots = i + 1;
+            }
+            for (int q = 0; q < nr; ++q)
+                if (rows[q].remaining != 0) return false;
+            for (int i = 0; i < used_slots; ++i) {
+                wf_warp += wf_slot[i];
+                conf_cta += conf_slot[i];
+            }
+            lay.warp_slots[static_cast<size_t>(c) * lay.warps + w] = used_slots;
+            lay.slots_used = std::max(lay.slots_used, used_slots);
+            wf_cta += wf_warp;
+            issue_cta += used_slots;
+            lay.slots_total += static_cast<int64_t>(used_slots) * 32;
+        }
+        if (wf_cta > lay.wavefronts_max_cta) {
+            lay.wavefronts_max_cta = wf_cta;
+            lay.conflicts_max_cta = conf_cta;
+        }
+        lay.wavefronts_ideal_cta = std::max<int64_t>(lay.wavefronts_ideal_cta, (pairs_cta + P - 1) / P);
+        lay.issue_max_cta = std::max(lay.issue_max_cta, issue_cta);
+    }
+    return true;
+}
+
+}  // namespace srnn

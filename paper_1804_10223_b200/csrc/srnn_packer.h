@@ -1,0 +1,50 @@
+// srnn_packer.h -- host-side planner + packer of the sparse weight image
+// (SURVEY.md Sec. 8 a2, a10).  Pure C++, no CUDA; unit-tested on the CPU
+// through srnn_plan_export_layout.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+namespace srnn {
+
+struct PackInput {
+    int32_t H = 0, G = 1;
+    const int32_t* rowptr = nullptr;  // [G*H+1]
+    const int32_t* col = nullptr;     // [nnz]
+    const float* val = nullptr;       // [nnz] (already fp16-rounded in fp16 mode)
+    int32_t BT = 4;                   // batch tile -> shared-memory phase size P = 32/BT lanes
+    bool naive = false;               // CSR-order lane-strided layout (PAPER.md:91 baseline)
+};
+
+struct Layout {
+    int32_t num_ctas = 0, lanes_per_row = 0, threads = 0, warps = 0;
+    int32_t np_budget = 0;   // slot budget the greedy packed against
+    int32_t slots_used = 0;  // max over warps of used slots
+    std::vector<int32_t> cta_unit0;   // [num_ctas+1]
+    std::vector<int32_t> warp_slots;  // [num_ctas*warps]
+    // per (cta, slot < np_budget, thread): column, value, owning global row (-1 idle)
+    std::vector<int32_t> col;
+    std::vector<float> val;
+    std::vector<int32_t> row;
+    int64_t wavefronts_max_cta = 0;    // predicted smem wavefronts per tile-step, busiest CTA
+    int64_t wavefronts_ideal_cta = 0;  // ceil(pairs/32 lanes)*(32/P)-style ideal for that CTA
+    int64_t conflicts_max_cta = 0;     // sum over (slot, phase) of (wavefronts - 1) in that CTA
+    int64_t issue_max_cta = 0;         // warp-slot instructions of the busiest CTA
+    int64_t slots_total = 0;
+    size_t idx(int c, int i, int t) const {
+        return (static_cast<size_t>(c) * np_budget + i) * threads + t;
+    }
+};
+
+// Pack for a fixed CTA count, lanes per row and slot budget.  Returns false if
+// some row does not fit in lanes_per_row * np_budget slots.
+bool pack_layout(const PackInput& in, int num_ctas, int lanes_per_row, int np_budget, Layout* out);
+
+// Smallest budget a row needs: max_r ceil(len_r / L).
+int min_np(const PackInput& in, int lanes_per_row);
+
+// IEEE binary16 round-to-nearest-even of a float (as numpy astype(float16)).
+uint16_t float_to_half_rne(float f);
+float half_to_float(uint16_t h);
+
+}  // namespace srnn

@@ -1,0 +1,170 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol declared in
+include/srnn.h, validates its inputs, and its host-side packer produces a
+layout that reconstructs U_r exactly (PAPER.md:91 padding and PAPER.md:100
+reordering "do not change" the result).  No device call is made here
+(SRNN_FLAG_HOST_ONLY plans)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1804_10223_b200 import FLAG_HOST_ONLY, FLAG_NAIVE_LAYOUT, SparseRNN, SrnnError, inputs, load_library
+from paper_1804_10223_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_1804_10223_b200 import build
+    build.build()
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "srnn.h")).read()
+    return sorted(set(re.findall(r"\b(srnn_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = load_library()
+    syms = header_symbols()
+    assert len(syms) >= 10
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.EXPORTED)
+    assert lib.srnn_version().decode().startswith("srnn")
+    assert lib.srnn_status_string(-6).decode() == "SRNN_ERR_TIMEOUT"
+
+
+def host_plan(prob, prec="fp32", **kw):
+    m = SparseRNN(prob["H"], prob["I"], prob["B"], prob["T"], prob["density"], prob["cell"], prob.get("act", "relu"),
+                  prec, flags=FLAG_HOST_ONLY | kw.pop("flags", 0), **kw)
+    m.load_weights(prob["rowptr"], prob["col"], prob["val"], prob["wx"], prob["bias"])
+    return m
+
+
+def reconstruct(m, prob):
+    col, val, row = m.export_layout()
+    G, H = prob["G"], prob["H"]
+    dense = np.zeros((G * H, H), np.float64)
+    cnt = np.zeros((G * H, H), np.int64)
+    real = (row >= 0) & (val != 0)
+    np.add.at(dense, (row[real], col[real]), val[real].astype(np.float64))
+    np.add.at(cnt, (row[real], col[real]), 1)
+    return dense, cnt, (col, val, row)
+
+
+def csr_dense(prob, vals=None):
+    G, H = prob["G"], prob["H"]
+    rp, cl = prob["rowptr"], prob["col"]
+    v = prob["val"] if vals is None else vals
+    d = np.zeros((G * H, H), np.float64)
+    rows = np.repeat(np.arange(G * H), np.diff(rp))
+    d[rows, cl] = v
+    return d
+
+
+@pytest.mark.parametrize("H,B,d,cell,pattern", [
+    (256, 1, 0.10, "rnn", "unstructured"),     # C1 shape
+    (1152, 4, 0.10, "rnn", "unstructured"),    # Table 1 shape
+    (300, 3, 0.05, "rnn", "unstructured"),     # ragged
+    (128, 2, 0.125, "lstm", "row_balanced"),   # NMT-like LSTM
+    (97, 1, 0.3, "lstm", "unstructured"),
+])
+@pytest.mark.parametrize("naive", [False, True])
+def test_packer_reconstructs_matrix_exactly(H, B, d, cell, pattern, naive):
+    prob = inputs.make_problem(H, H, B, 4, d, cell=cell, pattern=pattern)
+    m = host_plan(prob, "fp32", flags=FLAG_NAIVE_LAYOUT if naive else 0)
+    dense, cnt, (col, val, row) = reconstruct(m, prob)
+    assert np.array_equal(dense, csr_dense(prob))
+    assert cnt.max() <= 1 and cnt.sum() == prob["nnz"]
+    inf = m.info()
+    assert inf["nnz"] == prob["nnz"]
+    assert 0 < inf["slots_used"] <= inf["pairs_per_lane"]
+    # lanes of one row are L consecutive lanes carrying the same row id
+    L = inf["lanes_per_row"]
+    r = row.reshape(inf["num_ctas"], inf["pairs_per_lane"], -1, L)
+    assert (r == r[..., :1]).all()
+    # padding slots read a valid column (any in-range index, R6)
+    assert col.min() >= 0 and col.max() < H
+
+
+def test_fp16_quantisation_is_numpy_rne():
+    prob = inputs.make_problem(512, 512, 4, 4, 0.1)
+    rng = np.random.default_rng(0)
+    vals = (rng.standard_normal(prob["nnz"]) * np.exp(rng.uniform(-20, 12, prob["nnz"]))).astype(np.float32)
+    vals[:4] = [6.1035156e-05, 5.9604645e-08, 2.9802322e-08, 65519.0]  # normal/subnormal/tie/overflow edges
+    prob["val"] = vals
+    m = host_plan(prob, "fp16")
+    dense, cnt, _ = reconstruct(m, prob)
+    with np.errstate(over="ignore"):
+        q = vals.astype(np.float16).astype(np.float64)
+    ref = csr_dense(prob, q)
+    assert np.array_equal(dense, ref)
+
+
+def test_bank_aware_layout_cuts_predicted_conflicts():
+    """wide loads + bank-aware layout cut conflicts by > 80%."""
+    prob = inputs.make_problem(1152, 1152, 4, 4, 0.10)
+    naive = host_plan(prob, "fp32", flags=FLAG_NAIVE_LAYOUT, lanes_per_row=32, num_ctas=148).info()
+    aware = host_plan(prob, "fp32", lanes_per_row=32, num_ctas=148).info()
+    extra_naive = naive["conflict_wavefronts"]
+    extra_aware = aware["conflict_wavefronts"]
+    assert extra_naive > 0
+    assert extra_aware <= 0.2 * extra_naive, (naive, aware)
+
+
+@pytest.mark.parametrize("mutate,code", [
+    ("dup", -3), ("range", -3), ("monotone", -3), ("nnz", -3),
+])
+def test_load_weights_rejects_bad_csr(mutate, code):
+    prob = inputs.make_problem(64, 64, 1, 2, 0.2)
+    rp, cl, vl = prob["rowptr"].copy(), prob["col"].copy(), prob["val"].copy()
+    nnz = len(cl)
+    if mutate == "dup":
+        r = int(np.argmax(np.diff(rp) >= 2))
+        cl[rp[r] + 1] = cl[rp[r]]
+    elif mutate == "range":
+        cl[3] = 64
+    elif mutate == "monotone":
+        rp[5], rp[6] = rp[6], rp[5] - 1
+    m = SparseRNN(64, 64, 1, 2, 0.2, flags=FLAG_HOST_ONLY, prec="fp32")
+    lib = load_library()
+    from paper_1804_10223_b200._lib import _ptr
+    rp = np.ascontiguousarray(rp, np.int32)
+    cl = np.ascontiguousarray(cl, np.int32)
+    vl = np.ascontiguousarray(vl, np.float32)
+    wx = np.ascontiguousarray(prob["wx"], np.float32)
+    n = nnz + (1 if mutate == "nnz" else 0)
+    got = lib.srnn_load_weights(m.handle, _ptr(rp), _ptr(cl), _ptr(vl), n, _ptr(wx), None)
+    assert got == code
+
+
+def test_plan_create_rejects_bad_config_and_state_errors():
+    with pytest.raises(SrnnError):
+        SparseRNN(0, 4, 1, 1, 0.1, flags=FLAG_HOST_ONLY)
+    with pytest.raises(SrnnError):
+        SparseRNN(16, 4, 1, 1, 1.5, flags=FLAG_HOST_ONLY)
+    with pytest.raises(SrnnError):
+        SparseRNN(16, 4, 1, 1, 0.1, flags=FLAG_HOST_ONLY, lanes_per_row=3)
+    m = SparseRNN(16, 4, 1, 1, 0.1, flags=FLAG_HOST_ONLY)
+    with pytest.raises(SrnnError) as e:
+        m.export_layout()
+    lib = load_library()
+    assert lib.srnn_forward(m.handle, 1, 1, None, None, None, None, None, None, None) == -4  # host-only -> STATE
+
+
+def test_not_on_chip_is_reported():
+    # 65536 hidden at 50% density: ~2.1e9 pairs cannot be register-resident
+    with pytest.raises(SrnnError) as e:
+        SparseRNN(65536, 16, 1, 1, 0.5, flags=FLAG_HOST_ONLY)
+    assert e.value.code == -2
+
+
+def test_density_zero_and_one_layouts():
+    for d in (0.0, 1.0):
+        prob = inputs.make_problem(64, 8, 2, 3, d)
+        m = host_plan(prob, "fp32")
+        dense, cnt, _ = reconstruct(m, prob)
+        assert np.array_equal(dense, csr_dense(prob))
