@@ -297,7 +297,7 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
         if (smem > static_cast<size_t>(p->smem_optin)) continue;
         for (int L : cands_l) {
             const int rows_max = G * umax;
-            const int threads = ((rows_max * L + 31) / 32) * 32;
+            const int threads = std::max(((rows_max * L + 31) / 32) * 32, ((umax * p->BT + 31) / 32) * 32);
             if (threads > 1024) continue;
             const int np0 = std::max(1, min_np(in, L));
             if (np0 > kNPList[kNumNP - 1]) continue;

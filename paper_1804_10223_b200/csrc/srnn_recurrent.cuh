@@ -233,7 +233,10 @@ __global__ void __launch_bounds__(MaxThreads<NP>::value, 1) srnn_persistent_kern
     const int krow = warp * (32 / L) + lane / L;  // local row of this lane
     const bool row_leader = (lane % L) == 0 && krow < G * U;
 
-    if (tid == 0) *s_abort = 0;
+    if (tid == 0) {
+        *s_abort = 0;
+        if (U * BT > p.threads) atomicCAS(p.status, 0, -7 /* SRNN_ERR_UNSUPPORTED: planner bug */);
+    }
     // ---- publish h_0 (tag = epoch) and initialise c ----
     if (epi) {
         for (int k = 0; k < p.n_tiles; ++k) {
