@@ -80,7 +80,9 @@ typedef enum { SRNN_PREC_FP32 = 0, SRNN_PREC_FP16W_FP32ACC = 1 } srnn_prec_t;
 #define SRNN_FLAG_HOST_ONLY      (1u << 2) /* plan + pack on the host only; no device calls at all */
 #define SRNN_FLAG_SIMT_GEMM      (1u << 3) /* fp16 mode: use the fp32 SIMT input GEMM (ablation)    */
 #define SRNN_FLAG_DEBUG_JITTER   (1u << 4) /* inject per-CTA __nanosleep delays (sync-protocol test)*/
-#define SRNN_FLAG_FP16_EXCHANGE  (1u << 5) /* fp16 mode: exchange/stage h as fp16 (fewer bytes)     */
+#define SRNN_FLAG_FP32_STAGING   (1u << 5) /* fp16 mode: stage/exchange h in fp32 and keep fp32
+                                              register pairs (ablation; default fp16 staging and
+                                              one register per pair)        */
 
 typedef struct {
     int32_t hidden;     /* H >= 1, <= 65536 (u16 column index)                          */

@@ -26,7 +26,7 @@ FLAG_NAIVE_LAYOUT = 1 << 1
 FLAG_HOST_ONLY = 1 << 2
 FLAG_SIMT_GEMM = 1 << 3
 FLAG_DEBUG_JITTER = 1 << 4
-FLAG_FP16_EXCHANGE = 1 << 5
+FLAG_FP32_STAGING = 1 << 5
 
 EXPORTED = ["srnn_plan_create", "srnn_plan_query", "srnn_load_weights", "srnn_forward", "srnn_input_projection",
             "srnn_recurrence", "srnn_forward_host", "srnn_plan_status", "srnn_plan_export_layout",

@@ -23,6 +23,8 @@ struct srnn_plan {
     int sm_count = 148;
     int smem_optin = 232448;  // B200: 227 KB per block opt-in
     int BT = 4, n_tiles_max = 1;
+    bool f16 = false;  // fp16 register pairs + fp16 h staging/exchange (fp16 mode default)
+    int E = 16;        // bytes per staged h row
     bool host_only = false;
     bool loaded = false;
     // layout decisions
@@ -63,16 +65,16 @@ struct DeviceGuard {
     }
 };
 
-int max_threads_for_np(int np) { return np <= 8 ? 1024 : np <= 16 ? 768 : np <= 32 ? 512 : np <= 48 ? 352 : 320; }
-
-int inst_for(int slots) {
+int inst_for(int slots, bool f16) {
     for (int i = 0; i < kNumNP; ++i)
-        if (kNPList[i] >= slots) return kNPList[i];
+        if (kNPList[i] >= slots && kNPList[i] <= max_np(f16)) return kNPList[i];
     return -1;
 }
 
+int elem_bytes(bool f16, int bt) { return f16 ? 2 * bt : 4 * bt; }
+
 size_t smem_for(const srnn_plan* p, int units_max, int bt, int n_tiles) {
-    size_t s = static_cast<size_t>(p->cfg.hidden) * bt * 4;
+    size_t s = (static_cast<size_t>(p->cfg.hidden) * elem_bytes(p->f16, bt) + 15) & ~static_cast<size_t>(15);
     s += static_cast<size_t>(p->G) * units_max * bt * 4;
     if (p->G == 4) s += static_cast<size_t>(n_tiles) * units_max * bt * 4;
     return s + 16;
@@ -100,14 +102,15 @@ void free_device(srnn_plan* p) {
 // Estimated cycles of one tile-step on the busiest CTA (planner cost model,
 // DESIGN.md Sec. 5): shared-memory wavefronts vs issue, plus the reduction
 // latency, plus the exchange round trip.
-double cost_model(const Layout& lay, int bt, int H, int n_tiles) {
+double cost_model(const Layout& lay, int bt, int H, int n_tiles, bool f16) {
     const double wf = static_cast<double>(lay.wavefronts_max_cta);
-    const double issue = static_cast<double>(lay.issue_max_cta) * (1 + bt) / 4.0;
+    const double issue = static_cast<double>(lay.issue_max_cta) * (2 + bt) / 4.0;
     int lg = 0;
     while ((1 << lg) < lay.lanes_per_row) ++lg;
     const double reduce = lg * (30.0 + 2.0 * bt);
     const double chain = lay.slots_used * 4.0;
-    const double ingress = static_cast<double>(H) * bt * 8.0 / 64.0;
+    const double words_per_unit = f16 ? (bt == 4 ? 2.0 : 1.0) : bt;
+    const double ingress = static_cast<double>(H) * words_per_unit * 8.0 / 48.0;
     const double sync = lay.num_ctas > 1 ? 900.0 + 2.0 * lay.num_ctas : 600.0;
     return n_tiles * (std::max(std::max(wf, issue), chain) + reduce + ingress + sync);
 }
@@ -176,10 +179,18 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     }
     // Batch tile: the paper's wide load interleaves 4 samples;
     // narrower tiles when B_max < 4 or when h staging would not fit.
+    p->f16 = c.prec == SRNN_PREC_FP16W_FP32ACC && (c.flags & SRNN_FLAG_FP32_STAGING) == 0;
     int bt = c.batch >= 4 ? 4 : (c.batch >= 2 ? 2 : 1);
+    // fp16 register pairs carry the hs byte offset in 16 bits: H * E <= 65536
+    while (p->f16 && bt > 1 && static_cast<int64_t>(c.hidden) * elem_bytes(true, bt) > 65536) bt /= 2;
+    if (p->f16 && static_cast<int64_t>(c.hidden) * elem_bytes(true, bt) > 65536) {
+        delete p;
+        return SRNN_ERR_UNSUPPORTED;
+    }
     const int umax_guess = (c.hidden + p->sm_count - 1) / p->sm_count;
     while (bt > 1 && smem_for(p, umax_guess, bt, (c.batch + bt - 1) / bt) > static_cast<size_t>(p->smem_optin)) bt /= 2;
     p->BT = bt;
+    p->E = elem_bytes(p->f16, bt);
     p->n_tiles_max = (c.batch + bt - 1) / bt;
     if (smem_for(p, umax_guess, bt, p->n_tiles_max) > static_cast<size_t>(p->smem_optin)) {
         delete p;
@@ -188,14 +199,15 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     // Register budget for the expected pairs: two registers per pair in the
     // hoisted format, at most ~75% of each SM's 64K registers.
     const double exp_pairs = static_cast<double>(c.density) * p->G * c.hidden * static_cast<double>(c.hidden);
-    const double reg_capacity_pairs = 0.75 * 65536.0 * p->sm_count / 2.0;
+    const double reg_capacity_pairs = 0.75 * 65536.0 * p->sm_count / (p->f16 ? 1.0 : 2.0);
     if (exp_pairs > reg_capacity_pairs) {
         delete p;
         return SRNN_ERR_NOT_ON_CHIP;
     }
     if (!p->host_only) {
         DeviceGuard g(c.device);
-        const size_t tile_stride = (static_cast<size_t>(c.hidden) * bt + 1) & ~static_cast<size_t>(1);
+        const int wpr = p->f16 ? (bt == 4 ? 2 : 1) : bt;  // tagged words per unit
+        const size_t tile_stride = (static_cast<size_t>(c.hidden) * wpr + 1) & ~static_cast<size_t>(1);
         p->xbuf_words = 2 * static_cast<size_t>(p->n_tiles_max) * tile_stride;
         const size_t bp_elems = static_cast<size_t>(std::max(1, c.max_steps)) * c.batch * p->G * c.hidden;
         if (cudaMalloc(&p->d_xbuf, p->xbuf_words * 8) != cudaSuccess ||
@@ -231,12 +243,12 @@ srnn_status_t srnn_plan_query(srnn_plan_t p, srnn_plan_info_t* out) {
         for (int c = 0; c < l.num_ctas; ++c) umax = std::max(umax, l.cta_unit0[c + 1] - l.cta_unit0[c]);
         out->units_per_cta_max = umax;
         out->regs_per_thread = p->regs;
-        out->packed_registers = 0;
+        out->packed_registers = p->f16 ? 1 : 0;
         out->nnz = p->nnz;
         out->slots_total = l.slots_total;
         out->smem_bytes_per_cta = static_cast<int64_t>(p->smem_bytes);
         out->weight_image_bytes = static_cast<int64_t>(l.num_ctas) * p->np_inst * l.threads *
-                                  (p->cfg.prec == SRNN_PREC_FP32 ? 8 : 4);
+                                  (p->f16 ? 4 : 8);
         out->wavefronts_per_step_max = l.wavefronts_max_cta;
         out->wavefronts_per_step_ideal = l.wavefronts_ideal_cta;
         out->conflict_wavefronts = l.conflicts_max_cta;
@@ -271,6 +283,7 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
     in.col = col;
     in.val = qval.data();
     in.BT = p->BT;
+    in.E = p->E;
     in.naive = (p->cfg.flags & SRNN_FLAG_NAIVE_LAYOUT) != 0;
 
     // ---- search (num_ctas, lanes_per_row, slot budget) ----
@@ -300,16 +313,16 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
             const int threads = std::max(((rows_max * L + 31) / 32) * 32, ((umax * p->BT + 31) / 32) * 32);
             if (threads > 1024) continue;
             const int np0 = std::max(1, min_np(in, L));
-            if (np0 > kNPList[kNumNP - 1]) continue;
-            const int np_hi = in.naive ? np0 : std::min(kNPList[kNumNP - 1], np0 + std::max(2, np0 / 4));
+            if (np0 > max_np(p->f16)) continue;
+            const int np_hi = in.naive ? np0 : std::min(max_np(p->f16), np0 + std::max(2, np0 / 4));
             for (int np = np0; np <= np_hi; ++np) {
-                const int inst = inst_for(np);
-                if (inst < 0 || threads > max_threads_for_np(inst)) break;
+                const int inst = inst_for(np, p->f16);
+                if (inst < 0 || threads > max_threads_for(inst, p->f16)) break;
                 Layout lay;
                 if (!pack_layout(in, C, L, np, &lay)) continue;
-                const int inst_used = inst_for(std::max(1, lay.slots_used));
-                if (inst_used < 0 || lay.threads > max_threads_for_np(inst_used)) continue;
-                const double cst = cost_model(lay, p->BT, H, p->n_tiles_max);
+                const int inst_used = inst_for(std::max(1, lay.slots_used), p->f16);
+                if (inst_used < 0 || lay.threads > max_threads_for(inst_used, p->f16)) continue;
+                const double cst = cost_model(lay, p->BT, H, p->n_tiles_max, p->f16);
                 if (cst < best_cost) {
                     best_cost = cst;
                     best = std::move(lay);
@@ -349,7 +362,7 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
     p->np_inst = best_inst;
     p->lay = std::move(fin);
     p->nnz = nnz;
-    p->regs = 2 * best_inst + 58;  // host-only estimate; replaced by the compiled count below
+    p->regs = (p->f16 ? 1 : 2) * best_inst + 60;  // host-only estimate; replaced by the compiled count below
 
     if (!p->host_only) {
         DeviceGuard g(p->cfg.device);
@@ -364,10 +377,10 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
         p->d_unit0 = p->d_wslots = nullptr;
         p->d_wx = p->d_bias = nullptr;
         cudaError_t e = cudaSuccess;
-        if (fp16) {
+        if (p->f16) {
             std::vector<uint32_t> img(n);
             for (size_t i = 0; i < n; ++i)
-                img[i] = (static_cast<uint32_t>(l.col[i]) << 16) | float_to_half_rne(l.val[i]);
+                img[i] = (static_cast<uint32_t>(l.col[i] * p->E) << 16) | float_to_half_rne(l.val[i]);
             e = cudaMalloc(&p->d_img, n * 4);
             if (e == cudaSuccess) e = cudaMemcpy(p->d_img, img.data(), n * 4, cudaMemcpyHostToDevice);
         } else {
@@ -375,7 +388,7 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
             for (size_t i = 0; i < n; ++i) {
                 uint32_t b;
                 std::memcpy(&b, &l.val[i], 4);
-                img[i] = make_uint2(static_cast<uint32_t>(l.col[i]), b);
+                img[i] = make_uint2(static_cast<uint32_t>(l.col[i] * p->E), b);
             }
             e = cudaMalloc(&p->d_img, n * 8);
             if (e == cudaSuccess) e = cudaMemcpy(p->d_img, img.data(), n * 8, cudaMemcpyHostToDevice);
@@ -399,7 +412,8 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
         RecParams rp{};
         rp.threads = l.threads;
         int regs = 0, maxb = 0;
-        int le = launch_recurrent(p->np_inst, p->BT, G, 0, rp, l.num_ctas, p->smem_bytes, nullptr, true, &regs, &maxb);
+        int le = launch_recurrent(p->np_inst, p->BT, G, p->f16 ? 1 : 0, rp, l.num_ctas, p->smem_bytes, nullptr, true,
+                                  &regs, &maxb);
         if (le != 0) return SRNN_ERR_CUDA;
         p->regs = regs;
         if (maxb < 1) return SRNN_ERR_NOT_ON_CHIP;
@@ -460,10 +474,10 @@ srnn_status_t srnn_recurrence(srnn_plan_t p, int32_t T, int32_t B, const float* 
     rp.units_max = umax;
     rp.epoch = p->epoch;
     rp.flags = p->cfg.flags;
-    if (p->cfg.prec == SRNN_PREC_FP32)
-        rp.img_f32 = static_cast<const uint2*>(p->d_img);
-    else
+    if (p->f16)
         rp.img_f16 = static_cast<const uint32_t*>(p->d_img);
+    else
+        rp.img_f32 = static_cast<const uint2*>(p->d_img);
     rp.cta_unit0 = p->d_unit0;
     rp.warp_slots = p->d_wslots;
     rp.bprime = bprime;
@@ -475,8 +489,8 @@ srnn_status_t srnn_recurrence(srnn_plan_t p, int32_t T, int32_t B, const float* 
     rp.xbuf = p->d_xbuf;
     rp.status = p->d_status;
     rp.timeout_ns = p->timeout_ns;
-    int e = launch_recurrent(p->np_inst, p->BT, p->G, 0, rp, p->lay.num_ctas, p->smem_bytes, stream, false, nullptr,
-                             nullptr);
+    int e = launch_recurrent(p->np_inst, p->BT, p->G, p->f16 ? 1 : 0, rp, p->lay.num_ctas, p->smem_bytes, stream,
+                             false, nullptr, nullptr);
     if (e != 0) return SRNN_ERR_CUDA;
     p->epoch += static_cast<uint32_t>(T) + 1;
     return SRNN_OK;

@@ -26,8 +26,8 @@ struct RecParams {
     uint32_t epoch;   // tag of h_0 for this call; h_s carries epoch + s
     uint32_t flags;   // SRNN_FLAG_* subset relevant on device
     // packed weights: [cta][slot][thread]
-    const uint2* img_f32;      // fp32 mode: {col, float bits}
-    const uint32_t* img_f16;   // fp16 mode: (col << 16) | half bits
+    const uint2* img_f32;      // fp32 mode: {hs byte offset, float bits}
+    const uint32_t* img_f16;   // fp16 mode: (hs byte offset << 16) | half bits
     const int32_t* cta_unit0;  // [num_ctas + 1] first unit of each CTA
     const int32_t* warp_slots; // [num_ctas][warps] slots used by each warp (warp-uniform)
     // data
@@ -53,13 +53,20 @@ struct GemmParams {
 };
 
 // Launch helpers implemented in the .cu files. Return cudaError_t as int.
-int launch_recurrent(int np, int bt, int g, int packed, const RecParams& p, int num_ctas,
+int launch_recurrent(int np, int bt, int g, int f16, const RecParams& p, int num_ctas,
                      size_t smem_bytes, void* stream, bool query_only, int* regs_out,
                      int* max_blocks_per_sm_out);
 int launch_gemm_f32(const GemmParams& p, void* stream);
 
-// Compiled register-slot instances (pairs per lane).
-constexpr int kNumNP = 8;
-constexpr int kNPList[kNumNP] = {4, 8, 12, 16, 24, 32, 48, 64};
+// Compiled register-slot instances (pairs per lane); 96 exists only for the
+// fp16 mode (one register per pair).
+constexpr int kNumNP = 9;
+constexpr int kNPList[kNumNP] = {4, 8, 12, 16, 24, 32, 48, 64, 96};
+inline int max_np(bool f16) { return f16 ? 96 : 64; }
+// Must match MaxThreads<NP, F16> in srnn_recurrent.cuh.
+inline int max_threads_for(int np, bool f16) {
+    if (f16) return np <= 12 ? 640 : np <= 32 ? 512 : np <= 48 ? 384 : 256;
+    return np <= 4 ? 768 : np <= 12 ? 640 : np <= 32 ? 512 : np <= 48 ? 384 : 256;
+}
 
 }  // namespace srnn

@@ -110,8 +110,14 @@ int min_np(const PackInput& in, int L) {
 
 bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
     const int H = in.H, G = in.G;
-    const int P = 32 / in.BT;
+    // Lanes per shared-memory phase: a wavefront serves 128 B, so an LDS of E
+    // bytes per lane is split into phases of P = 128/E lanes (one phase of 32
+    // lanes for E <= 4).  Conflicts are decided by key(col) mod P; equal keys
+    // broadcast (E = 2: two fp16 columns share one 4-byte bank word).
+    const int E = in.E;
+    const int P = E >= 4 ? 128 / E : 32;
     const int ng = 32 / P;  // phase groups per warp instruction
+    auto key = [E](int32_t c) { return E >= 4 ? c : (c >> 1); };
     const int rpw = 32 / L;
     Layout& lay = *out;
     lay = Layout();
@@ -156,7 +162,7 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
                 rs.remaining = e - b;
                 pairs_cta += e - b;
                 if (e - b > static_cast<int64_t>(L) * NP) return false;
-                for (int64_t p = b; p < e; ++p) rs.bucket[in.col[p] % P].push_back(p);
+                for (int64_t p = b; p < e; ++p) rs.bucket[key(in.col[p]) % P].push_back(p);
             }
             // slot-major fill
             int used_slots = 0;
@@ -174,9 +180,9 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
                         lay.col[at] = in.col[pos];
                         lay.val[at] = in.val[pos];
                         lay.row[at] = rows[q].grow;
-                        const int r = in.col[pos] % P;
-                        if (std::find(distinct[r].begin(), distinct[r].end(), in.col[pos]) == distinct[r].end())
-                            distinct[r].push_back(in.col[pos]);
+                        const int r = key(in.col[pos]) % P;
+                        if (std::find(distinct[r].begin(), distinct[r].end(), key(in.col[pos])) == distinct[r].end())
+                            distinct[r].push_back(key(in.col[pos]));
                         if (gcol[r] < 0) gcol[r] = in.col[pos];
                         rows[q].remaining--;
                         any_real = true;
@@ -213,7 +219,8 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
                                 for (int r = 0; r < P; ++r) {
                                     const size_t n = rs.bucket[r].size() - rs.head[r];
                                     if (n == 0) continue;
-                                    const bool free_res = gcol[r] < 0 || gcol[r] == in.col[rs.bucket[r][rs.head[r]]];
+                                    const bool free_res =
+                                        gcol[r] < 0 || key(gcol[r]) == key(in.col[rs.bucket[r][rs.head[r]]]);
                                     if (free_res && n > best_n) {
                                         best = r;
                                         best_n = n;

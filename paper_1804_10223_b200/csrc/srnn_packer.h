@@ -12,7 +12,8 @@ struct PackInput {
     const int32_t* rowptr = nullptr;  // [G*H+1]
     const int32_t* col = nullptr;     // [nnz]
     const float* val = nullptr;       // [nnz] (already fp16-rounded in fp16 mode)
-    int32_t BT = 4;                   // batch tile -> shared-memory phase size P = 32/BT lanes
+    int32_t BT = 4;                   // batch tile (samples per staged h row)
+    int32_t E = 16;                   // bytes per staged h row (4*BT fp32, 2*BT fp16): one LDS per pair
     bool naive = false;               // CSR-order lane-strided layout (PAPER.md:91 baseline)
 };
 

@@ -78,7 +78,7 @@ __device__ __forceinline__ float activation(int act, float z) {
 }
 __device__ __forceinline__ float sigmoidf_acc(float z) { return 1.0f / (1.0f + expf(-z)); }
 
-// Spin-wait bookkeeping shared by all loaders of a CTA.
+// Spin-wait bookkeeping of one loader thread.
 struct Watchdog {
     unsigned long long t0;
     uint32_t spins;
@@ -86,7 +86,7 @@ struct Watchdog {
 
 // Returns true when the wait must be abandoned (timeout here or elsewhere).
 __device__ __forceinline__ bool watchdog_tick(Watchdog& wd, int32_t* status, unsigned long long timeout_ns) {
-    if ((++wd.spins & 255u) != 0u) return false;
+    if ((++wd.spins & 15u) != 0u) return false;
     unsigned long long now = globaltimer_ns();
     if (wd.t0 == 0) wd.t0 = now;
     if (*reinterpret_cast<volatile int32_t*>(status) != 0) return true;
@@ -97,102 +97,203 @@ __device__ __forceinline__ bool watchdog_tick(Watchdog& wd, int32_t* status, uns
     return false;
 }
 
-// Stage h_{s-1} (tile k) into shared memory: spin on tags (tag mode) or
-// check them once (grid-sync mode).  Returns false on abort.
-__device__ __forceinline__ bool load_tile(const unsigned long long* __restrict__ src, float* hs,
-                                          int n_words, uint32_t want, bool spin,
-                                          int32_t* status, unsigned long long timeout_ns) {
-    constexpr int K = 4;
-    const int n2 = n_words >> 1;
-    const ulonglong2* src2 = reinterpret_cast<const ulonglong2*>(src);
-    Watchdog wd{0ull, 0u};
-    bool ok = true;
-    const int nt = blockDim.x;
-    for (int base = threadIdx.x; base < n2; base += K * nt) {
-        ulonglong2 v[K];
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const int idx = base + j * nt;
-            if (idx < n2) v[j] = ld_relaxed_v2(src2 + idx);
-        }
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const int idx = base + j * nt;
-            ulonglong2 x = v[j];
-            if (idx < n2) {
-                bool ready = tag_of(x.x) == want && tag_of(x.y) == want;
-                if (!ready && !spin) {
-                    atomicCAS(status, 0, -4 /* protocol violation -> SRNN_ERR_STATE */);
-                    ready = true;
-                }
-                while (!ready && ok) {
-                    ok = !watchdog_tick(wd, status, timeout_ns);
-                    x = ld_relaxed_v2(src2 + idx);
-                    ready = tag_of(x.x) == want && tag_of(x.y) == want;
-                }
-                *reinterpret_cast<float2*>(hs + 2 * idx) = make_float2(val_of(x.x), val_of(x.y));
-            }
+// ---------------------------------------------------------------------------
+// Exchange / staging formats.
+//   F32: word = {fp32 h, u32 tag}, one word per (unit, sample); hs[H][BT] fp32.
+//   F16: word = {fp16 h(b), fp16 h(b+1), u32 tag}, ceil(BT/2) words per unit;
+//        hs[H][BT] fp16 ("a lower-precision data type for the
+//        activations would remove the shared memory bandwidth and storage
+//        burden").  A 16-byte chunk (two words) always maps onto a contiguous
+//        piece of hs, so the loader is a pure copy with a tag check.
+// ---------------------------------------------------------------------------
+template <bool F16, int BT>
+struct Fmt {
+    static constexpr int WPR = F16 ? (BT == 4 ? 2 : 1) : BT;   // words per unit
+    static constexpr int E = F16 ? 2 * BT : 4 * BT;            // hs bytes per unit
+    static constexpr int CHUNK_HS = (F16 && BT == 1) ? 4 : 8;  // hs bytes per 16-byte chunk
+
+    // store chunk `idx` (words w0, w1; w1 valid iff has1) into hs
+    __device__ __forceinline__ static void store(unsigned char* hs, int idx, unsigned long long w0,
+                                                 unsigned long long w1, bool has1) {
+        if (F16 && BT == 1) {
+            const uint32_t lo = static_cast<uint32_t>(w0) & 0xffffu;
+            if (has1)
+                *reinterpret_cast<uint32_t*>(hs + 4 * idx) = lo | (static_cast<uint32_t>(w1) << 16);
+            else
+                *reinterpret_cast<unsigned short*>(hs + 4 * idx) = static_cast<unsigned short>(lo);
+        } else {
+            if (has1)
+                *reinterpret_cast<uint2*>(hs + 8 * idx) = make_uint2(static_cast<uint32_t>(w0), static_cast<uint32_t>(w1));
+            else
+                *reinterpret_cast<uint32_t*>(hs + 8 * idx) = static_cast<uint32_t>(w0);
         }
     }
-    if ((n_words & 1) && threadIdx.x == 0) {
-        unsigned long long x = ld_relaxed_u64(src + n_words - 1);
-        bool ready = tag_of(x) == want;
-        if (!ready && !spin) {
-            atomicCAS(status, 0, -4);
-            ready = true;
+};
+
+// Stage h_{s-1} (one batch tile) into shared memory.  Every thread owns up
+// to K 16-byte chunks per group; all of them are in flight at once, and
+// chunks whose tags are stale are re-polled together (one round trip per
+// round, not per chunk).  Tag mode spins; grid-sync mode checks once.
+template <bool F16, int BT, int K>
+__device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, unsigned char* hs, int n_words,
+                                          uint32_t want, bool spin, int32_t* status,
+                                          unsigned long long timeout_ns) {
+    const int n_chunks = (n_words + 1) >> 1;
+    const int nt = blockDim.x;
+    Watchdog wd{0ull, 0u};
+    bool ok = true;
+    for (int base = threadIdx.x; base < n_chunks; base += K * nt) {
+        ulonglong2 v[K];
+        uint32_t pend = 0u;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const int idx = base + j * nt;
+            if (idx < n_chunks) {
+                v[j] = ld_relaxed_v2(src + idx);
+                pend |= 1u << j;
+            }
         }
-        while (!ready && ok) {
-            ok = !watchdog_tick(wd, status, timeout_ns);
-            x = ld_relaxed_u64(src + n_words - 1);
-            ready = tag_of(x) == want;
+        while (true) {
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                if (pend & (1u << j)) {
+                    const int idx = base + j * nt;
+                    const bool has1 = 2 * idx + 1 < n_words;
+                    if (tag_of(v[j].x) == want && (!has1 || tag_of(v[j].y) == want)) {
+                        Fmt<F16, BT>::store(hs, idx, v[j].x, v[j].y, has1);
+                        pend &= ~(1u << j);
+                    }
+                }
+            }
+            if (pend == 0u) break;
+            if (!spin) {
+                atomicCAS(status, 0, -4 /* protocol violation -> SRNN_ERR_STATE */);
+                break;
+            }
+            if (watchdog_tick(wd, status, timeout_ns)) {
+                ok = false;
+                break;
+            }
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+                if (pend & (1u << j)) v[j] = ld_relaxed_v2(src + base + j * nt);
         }
-        hs[n_words - 1] = val_of(x);
+        if (!ok) break;
     }
     return ok;
 }
 
-template <int BT>
-struct HVec;
-template <>
-struct HVec<1> {
-    __device__ __forceinline__ static void fma(float (&acc)[1], float w, const unsigned char* base, uint32_t off) {
-        const float h = *reinterpret_cast<const float*>(base + off);
-        acc[0] = fmaf(w, h, acc[0]);
+// ---------------------------------------------------------------------------
+// Register-resident weights and the operate stage.
+//   F32: two registers per pair, {hs byte offset, fp32 value}, FFMA.
+//   F16: one register per pair, (hs byte offset << 16) | fp16 value, and the
+//        sm_100 mixed-precision FMA d.f32 = a.f16 * b.f16 + c.f32 (FHFMA), so
+//        nothing is decoded per step ("two column indices can be
+//        compressed into a 32-bit register ... fp16 for the weights").
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float fma_f16f16f32(uint32_t a_lo_half, uint32_t b_half_bits, float c) {
+    float d;
+    asm("fma.rn.f32.f16 %0, %1, %2, %3;"
+        : "=f"(d)
+        : "h"(static_cast<unsigned short>(a_lo_half)), "h"(static_cast<unsigned short>(b_half_bits)), "f"(c));
+    return d;
+}
+
+template <int NP, int BT, bool F16>
+struct Weights;
+
+template <int NP, int BT>
+struct Weights<NP, BT, false> {
+    uint32_t off[NP];
+    float w[NP];
+    __device__ __forceinline__ void load(const RecParams& p, size_t img0, int n_w) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            off[i] = 0u;
+            w[i] = 0.0f;
+            if (i < n_w) {
+                const uint2 e = p.img_f32[img0 + static_cast<size_t>(i) * p.threads];
+                off[i] = e.x;
+                w[i] = __uint_as_float(e.y);
+            }
+        }
     }
-};
-template <>
-struct HVec<2> {
-    __device__ __forceinline__ static void fma(float (&acc)[2], float w, const unsigned char* base, uint32_t off) {
-        const float2 h = *reinterpret_cast<const float2*>(base + off);
-        acc[0] = fmaf(w, h.x, acc[0]);
-        acc[1] = fmaf(w, h.y, acc[1]);
-    }
-};
-template <>
-struct HVec<4> {
-    __device__ __forceinline__ static void fma(float (&acc)[4], float w, const unsigned char* base, uint32_t off) {
-        const float4 h = *reinterpret_cast<const float4*>(base + off);
-        acc[0] = fmaf(w, h.x, acc[0]);
-        acc[1] = fmaf(w, h.y, acc[1]);
-        acc[2] = fmaf(w, h.z, acc[2]);
-        acc[3] = fmaf(w, h.w, acc[3]);
+    __device__ __forceinline__ void operate(float (&acc)[BT], const unsigned char* hs, int n_w) const {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            if (i < n_w) {
+                if (BT == 4) {
+                    const float4 h = *reinterpret_cast<const float4*>(hs + off[i]);
+                    acc[0] = fmaf(w[i], h.x, acc[0]);
+                    acc[1 % BT] = fmaf(w[i], h.y, acc[1 % BT]);
+                    acc[2 % BT] = fmaf(w[i], h.z, acc[2 % BT]);
+                    acc[3 % BT] = fmaf(w[i], h.w, acc[3 % BT]);
+                } else if (BT == 2) {
+                    const float2 h = *reinterpret_cast<const float2*>(hs + off[i]);
+                    acc[0] = fmaf(w[i], h.x, acc[0]);
+                    acc[1 % BT] = fmaf(w[i], h.y, acc[1 % BT]);
+                } else {
+                    acc[0] = fmaf(w[i], *reinterpret_cast<const float*>(hs + off[i]), acc[0]);
+                }
+            }
+        }
     }
 };
 
-// Max threads per CTA of each register-slot instance (caps ptxas' register
-// budget at 65536 / MAXT while leaving room for the 2*NP hoisted registers).
-template <int NP>
+template <int NP, int BT>
+struct Weights<NP, BT, true> {
+    uint32_t pw[NP];
+    __device__ __forceinline__ void load(const RecParams& p, size_t img0, int n_w) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) pw[i] = i < n_w ? p.img_f16[img0 + static_cast<size_t>(i) * p.threads] : 0u;
+    }
+    __device__ __forceinline__ void operate(float (&acc)[BT], const unsigned char* hs, int n_w) const {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            if (i < n_w) {
+                const uint32_t o = pw[i] >> 16;
+                if (BT == 4) {
+                    const uint2 h = *reinterpret_cast<const uint2*>(hs + o);
+                    acc[0] = fma_f16f16f32(pw[i], h.x, acc[0]);
+                    acc[1 % BT] = fma_f16f16f32(pw[i], h.x >> 16, acc[1 % BT]);
+                    acc[2 % BT] = fma_f16f16f32(pw[i], h.y, acc[2 % BT]);
+                    acc[3 % BT] = fma_f16f16f32(pw[i], h.y >> 16, acc[3 % BT]);
+                } else if (BT == 2) {
+                    const uint32_t h = *reinterpret_cast<const uint32_t*>(hs + o);
+                    acc[0] = fma_f16f16f32(pw[i], h, acc[0]);
+                    acc[1 % BT] = fma_f16f16f32(pw[i], h >> 16, acc[1 % BT]);
+                } else {
+                    const uint32_t h = *reinterpret_cast<const unsigned short*>(hs + o);
+                    acc[0] = fma_f16f16f32(pw[i], h, acc[0]);
+                }
+            }
+        }
+    }
+};
+
+// Max threads per CTA of each instance.  The register file is split over
+// the 4 SM sub-partitions (16K registers each), so with W warps a thread may
+// hold at most 512 / ceil(W/4) registers: 256 threads -> 255, 384 -> 168,
+// 512 -> 128, 640 -> 96, 768 -> 80.  Each instance gets the largest thread
+// count whose budget still holds its register-resident pairs.
+template <int NP, bool F16>
 struct MaxThreads {
-    static constexpr int value = NP <= 8 ? 1024 : NP <= 16 ? 768 : NP <= 32 ? 512 : NP <= 48 ? 352 : 320;
+    static constexpr int value = F16 ? (NP <= 12 ? 640 : NP <= 32 ? 512 : NP <= 48 ? 384 : 256)
+                                     : (NP <= 4 ? 768 : NP <= 12 ? 640 : NP <= 32 ? 512 : NP <= 48 ? 384 : 256);
+};
+template <int NP, bool F16>
+struct LoadK {
+    static constexpr int value = F16 ? (NP <= 48 ? 8 : 4) : 4;
 };
 
-template <int NP, int BT, int G>
-__global__ void __launch_bounds__(MaxThreads<NP>::value, 1) srnn_persistent_kernel(const RecParams p) {
+template <int NP, int BT, int G, bool F16>
+__global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent_kernel(const RecParams p) {
+    using F = Fmt<F16, BT>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int H = p.H;
-    float* hs = reinterpret_cast<float*>(smem);        // [H][BT]   h_{s-1} tile (offset 0)
-    float* zs = hs + H * BT;                           // [G*Umax][BT] reduced rows
-    float* cs = zs + G * p.units_max * BT;             // LSTM cell state [n_tiles][Umax][BT]
+    unsigned char* hs = smem;                                                    // [H][BT] h_{s-1} (offset 0)
+    float* zs = reinterpret_cast<float*>(smem + ((static_cast<size_t>(H) * F::E + 15) & ~static_cast<size_t>(15)));
+    float* cs = zs + G * p.units_max * BT;                                       // LSTM c [n_tiles][Umax][BT]
     int* s_abort = reinterpret_cast<int*>(cs + (G == 4 ? p.n_tiles * p.units_max * BT : 0));
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -201,34 +302,17 @@ __global__ void __launch_bounds__(MaxThreads<NP>::value, 1) srnn_persistent_kern
     const int U = p.cta_unit0[cta + 1] - u0;
     const int L = p.lanes_per_row;
     const int n_w = p.warp_slots[cta * (p.threads >> 5) + warp];
-    const int tile_stride = (H * BT + 1) & ~1;
+    const int n_words = H * F::WPR;
+    const int tile_stride = (n_words + 1) & ~1;
 
     // ---- prologue: weights HBM -> registers (once per forward) ----
-    uint32_t off[NP];
-    float w[NP];
-    const size_t img0 = static_cast<size_t>(cta) * NP * p.threads + tid;
-#pragma unroll
-    for (int i = 0; i < NP; ++i) {
-        off[i] = 0u;
-        w[i] = 0.0f;
-        if (i < n_w) {
-            const size_t at = img0 + static_cast<size_t>(i) * p.threads;
-            if (p.img_f32 != nullptr) {
-                const uint2 e = p.img_f32[at];
-                off[i] = e.x * (BT * 4);
-                w[i] = __uint_as_float(e.y);
-            } else {
-                const uint32_t e = p.img_f16[at];
-                off[i] = (e >> 16) * (BT * 4);
-                w[i] = __half2float(__ushort_as_half(static_cast<unsigned short>(e & 0xffffu)));
-            }
-        }
-    }
+    Weights<NP, BT, F16> W;
+    W.load(p, static_cast<size_t>(cta) * NP * p.threads + tid, n_w);
 
-    // Epilogue role: thread e < U*BT owns (unit eu, sample eb) of every tile.
+    // Epilogue role: thread e < U*BT owns (unit e / BT, sample e % BT).
     const bool epi = tid < U * BT;
-    const int eb = epi ? tid / U : 0;
-    const int eu = epi ? tid - eb * U : 0;
+    const int eu = epi ? tid / BT : 0;
+    const int eb = epi ? tid - eu * BT : 0;
     const int unit = u0 + eu;
     const int krow = warp * (32 / L) + lane / L;  // local row of this lane
     const bool row_leader = (lane % L) == 0 && krow < G * U;
@@ -237,17 +321,34 @@ __global__ void __launch_bounds__(MaxThreads<NP>::value, 1) srnn_persistent_kern
         *s_abort = 0;
         if (U * BT > p.threads) atomicCAS(p.status, 0, -7 /* SRNN_ERR_UNSUPPORTED: planner bug */);
     }
-    // ---- publish h_0 (tag = epoch) and initialise c ----
-    if (epi) {
-        for (int k = 0; k < p.n_tiles; ++k) {
-            const int bg = k * BT + eb;
-            const float h = (p.h0 != nullptr && bg < p.B) ? p.h0[static_cast<size_t>(bg) * H + unit] : 0.0f;
-            st_relaxed_u64(p.xbuf + static_cast<size_t>(k) * tile_stride + unit * BT + eb, pack_tagged(h, p.epoch));
-            if (G == 4) {
-                cs[(k * p.units_max + eu) * BT + eb] =
-                    (p.c0 != nullptr && bg < p.B) ? p.c0[static_cast<size_t>(bg) * H + unit] : 0.0f;
+
+    // Publish h of (step s, tile k) as tagged words (all threads call: shuffles).
+    auto publish = [&](int s, int k, float h) {
+        unsigned long long* dst = p.xbuf + static_cast<size_t>((s & 1) * p.n_tiles + k) * tile_stride;
+        const uint32_t tag = p.epoch + static_cast<uint32_t>(s);
+        if (!F16) {
+            if (epi) st_relaxed_u64(dst + unit * BT + eb, pack_tagged(h, tag));
+        } else {
+            const uint32_t hb = __half_as_ushort(__float2half_rn(h));
+            const uint32_t nb = __shfl_down_sync(0xffffffffu, hb, 1);
+            if (epi && (BT == 1 || (eb & 1) == 0)) {
+                const uint32_t lo = BT == 1 ? hb : (hb | (nb << 16));
+                st_relaxed_u64(dst + unit * F::WPR + (eb >> 1), (static_cast<unsigned long long>(tag) << 32) | lo);
             }
         }
+    };
+
+    // ---- publish h_0 (tag = epoch) and initialise c ----
+    for (int k = 0; k < p.n_tiles; ++k) {
+        const int bg = k * BT + eb;
+        float h = 0.0f;
+        if (epi) {
+            h = (p.h0 != nullptr && bg < p.B) ? p.h0[static_cast<size_t>(bg) * H + unit] : 0.0f;
+            if (G == 4)
+                cs[(k * p.units_max + eu) * BT + eb] =
+                    (p.c0 != nullptr && bg < p.B) ? p.c0[static_cast<size_t>(bg) * H + unit] : 0.0f;
+        }
+        publish(0, k, h);
     }
     const bool grid_sync = (p.flags & kFlagGridSync) != 0u;
     if (grid_sync) cg::this_grid().sync();
@@ -264,24 +365,21 @@ __global__ void __launch_bounds__(MaxThreads<NP>::value, 1) srnn_persistent_kern
                 for (int q = 0; q < G; ++q)
                     bp[q] = bg < p.B ? __ldg(p.bprime + (static_cast<size_t>(s - 1) * p.B + bg) * GH + q * H + unit) : 0.0f;
             }
-            // ---- load: h_{s-1} tile k -> hs ----
-            const unsigned long long* src =
-                p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride;
-            if (!load_tile(src, hs, H * BT, p.epoch + static_cast<uint32_t>(s - 1), !grid_sync, p.status, p.timeout_ns))
+            // ---- load: h_{s-1} tile k -> hs (PAPER.md:63) ----
+            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
+                p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
+            if (!load_tile<F16, BT, LoadK<NP, F16>::value>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
+                                                            !grid_sync, p.status, p.timeout_ns))
                 *s_abort = 1;
             __syncthreads();
             if (*s_abort) goto done;
 
-            // ---- operate ----
+            // ---- operate + reduce ----
             {
                 float acc[BT];
 #pragma unroll
                 for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
-#pragma unroll
-                for (int i = 0; i < NP; ++i) {
-                    if (i < n_w) HVec<BT>::fma(acc, w[i], smem, off[i]);
-                }
-                // ---- reduce over the row's L lanes (fixed butterfly order) ----
+                W.operate(acc, hs, n_w);
                 for (int m = L >> 1; m >= 1; m >>= 1) {
 #pragma unroll
                     for (int b = 0; b < BT; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], m);
@@ -294,8 +392,8 @@ __global__ void __launch_bounds__(MaxThreads<NP>::value, 1) srnn_persistent_kern
             __syncthreads();
 
             // ---- epilogue: activation / gates, y, tagged publish of h_s ----
+            float h = 0.0f;
             if (epi) {
-                float h;
                 if (G == 1) {
                     h = activation(p.act, zs[eu * BT + eb] + bp[0]);
                 } else {
@@ -317,9 +415,8 @@ __global__ void __launch_bounds__(MaxThreads<NP>::value, 1) srnn_persistent_kern
                     const uint32_t r = (static_cast<uint32_t>(cta) * 2654435761u) ^ (static_cast<uint32_t>(s * 40503 + k));
                     __nanosleep((r >> 7) & 2047u);
                 }
-                st_relaxed_u64(p.xbuf + static_cast<size_t>((s & 1) * p.n_tiles + k) * tile_stride + unit * BT + eb,
-                               pack_tagged(h, p.epoch + static_cast<uint32_t>(s)));
             }
+            publish(s, k, h);
             if (grid_sync) cg::this_grid().sync();
         }
     }
@@ -327,10 +424,10 @@ done:
     return;
 }
 
-template <int NP, int BT, int G>
+template <int NP, int BT, int G, bool F16>
 static int launch_one(const RecParams& p, int num_ctas, size_t smem, void* stream, bool query_only,
                       int* regs_out, int* max_blocks_out) {
-    auto fn = srnn_persistent_kernel<NP, BT, G>;
+    auto fn = srnn_persistent_kernel<NP, BT, G, F16>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return static_cast<int>(e);
     if (regs_out != nullptr || max_blocks_out != nullptr) {
@@ -342,7 +439,7 @@ static int launch_one(const RecParams& p, int num_ctas, size_t smem, void* strea
             int nb = 0;
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, p.threads, smem);
             if (e != cudaSuccess) return static_cast<int>(e);
-            *max_blocks_out = p.threads > MaxThreads<NP>::value ? 0 : nb;
+            *max_blocks_out = p.threads > MaxThreads<NP, F16>::value ? 0 : nb;
         }
     }
     if (query_only) return 0;
@@ -352,12 +449,12 @@ static int launch_one(const RecParams& p, int num_ctas, size_t smem, void* strea
     return static_cast<int>(e);
 }
 
-template <int NP>
+template <int NP, bool F16>
 int launch_np(int bt, int g, const RecParams& p, int num_ctas, size_t smem, void* stream, bool query_only,
               int* regs_out, int* max_blocks_out) {
 #define SRNN_CASE(BT_, G_)                                                                                    \
     if (bt == BT_ && g == G_)                                                                                 \
-        return launch_one<NP, BT_, G_>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out);
+        return launch_one<NP, BT_, G_, F16>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out);
     SRNN_CASE(1, 1)
     SRNN_CASE(2, 1)
     SRNN_CASE(4, 1)

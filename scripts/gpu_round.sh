@@ -1,0 +1,13 @@
+#!/bin/bash
+# One GPU session: tests, bench, variants, ncu.  Output under gpurun_out/.
+cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -q -x ${TESTSEL:-} > gpurun_out/gpu_tests.log 2>&1; echo tests=$?
+rm -f gpurun_out/qt.log
+for args in "" "--L 32" "--L 16" "--flags 32" "--flags 1" "--prec fp32" "--prec fp32 --L 32"; do
+  timeout 120 python scripts/quick_time.py $args >> gpurun_out/qt.log 2>&1
+done
+if [ -n "$BENCH" ]; then timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$?; fi
+if [ -n "$NCU" ]; then
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:srnn_persistent -c 1 -o gpurun_out/prof_rec -f python scripts/quick_time.py --reps 1 $NCU_ARGS > gpurun_out/ncu_full.log 2>&1; echo ncu=$?
+fi

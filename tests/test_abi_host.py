@@ -158,8 +158,12 @@ def test_plan_create_rejects_bad_config_and_state_errors():
 def test_not_on_chip_is_reported():
     # 65536 hidden at 50% density: ~2.1e9 pairs cannot be register-resident
     with pytest.raises(SrnnError) as e:
-        SparseRNN(65536, 16, 1, 1, 0.5, flags=FLAG_HOST_ONLY)
+        SparseRNN(65536, 16, 1, 1, 0.5, flags=FLAG_HOST_ONLY, prec="fp32")
     assert e.value.code == -2
+    # fp16 register pairs hold the staged-h byte offset in 16 bits: H <= 32768
+    with pytest.raises(SrnnError) as e:
+        SparseRNN(40000, 16, 1, 1, 0.001, flags=FLAG_HOST_ONLY, prec="fp16")
+    assert e.value.code == -7
 
 
 def test_density_zero_and_one_layouts():

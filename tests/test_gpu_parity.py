@@ -8,7 +8,8 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_1804_10223_b200 import (FLAG_DEBUG_JITTER, FLAG_GRID_SYNC, FLAG_NAIVE_LAYOUT, from_problem, inputs)
+from paper_1804_10223_b200 import (FLAG_DEBUG_JITTER, FLAG_FP32_STAGING, FLAG_GRID_SYNC, FLAG_NAIVE_LAYOUT,
+                                   from_problem, inputs)
 
 pytestmark = pytest.mark.gpu
 
@@ -103,21 +104,29 @@ def test_jitter_is_bitwise_deterministic(cuda_device):
     assert np.array_equal(a["y"], b["y"]) and np.array_equal(a["y"], c["y"])
 
 
+@pytest.mark.parametrize("B", [1, 2, 4])
+def test_fp16_mode_fp32_staging_ablation(cuda_device, B):
+    prob = inputs.make_problem(900, 900, B, 20, 0.1, act="tanh", h0="random")
+    check(prob, "fp16", flags=FLAG_FP32_STAGING)
+
+
 def test_naive_layout_parity(cuda_device):
     prob = inputs.make_problem(1152, 1152, 4, 16, 0.1, act="relu")
     check(prob, "fp32", flags=FLAG_NAIVE_LAYOUT)
 
 
+@pytest.mark.parametrize("prec", ["fp32", "fp16"])
 @pytest.mark.parametrize("L", [1, 2, 4, 8, 16, 32])
-def test_every_lane_mapping(cuda_device, L):
+def test_every_lane_mapping(cuda_device, L, prec):
     prob = inputs.make_problem(512, 512, 4, 8, 0.05, act="tanh", h0="random")
-    check(prob, "fp32", lanes_per_row=L)
+    check(prob, prec, lanes_per_row=L)
 
 
-@pytest.mark.parametrize("C", [1, 3, 148])
-def test_cta_counts(cuda_device, C):
-    prob = inputs.make_problem(700, 700, 2, 8, 0.05, act="tanh", h0="random")
-    check(prob, "fp32", num_ctas=C)
+@pytest.mark.parametrize("prec", ["fp32", "fp16"])
+@pytest.mark.parametrize("C,H", [(1, 300), (3, 700), (148, 700)])
+def test_cta_counts(cuda_device, C, H, prec):
+    prob = inputs.make_problem(H, H, 2, 8, 0.05, act="tanh", h0="random")
+    check(prob, prec, num_ctas=C)
 
 
 def test_T0_T1_repeat_and_smaller_batch(cuda_device):
