@@ -77,13 +77,16 @@ def test_lstm_parity_small(cuda_device, prec, H, B, T, d, pattern):
 def test_integer_exact_bitwise(cuda_device, cell, prec):
     """Integer inputs: every partial sum < 2^24, so any order is exact."""
     act = "identity" if cell == "rnn" else "relu"
-    prob = inputs.make_integer_problem(200, 48, 4, 5, 0.02, cell=cell, act=act)
+    if prec == "fp32":
+        prob = inputs.make_integer_problem(200, 48, 4, 5, 0.02, cell=cell, act=act)
+    else:  # fp16 staging of h is exact only for integers up to 2^11
+        prob = inputs.make_integer_problem(200, 6, 4, 3, 0.01, cell=cell, act=act)
     if cell == "lstm":
         # gates saturate; keep the exactness claim to the RNN path, check LSTM by tolerance
         check(prob, prec)
         return
     o = oracle.forward(prob)
-    assert np.abs(o["y"]).max() < 2 ** 24
+    assert np.abs(o["y"]).max() < (2 ** 24 if prec == "fp32" else 2 ** 11)
     g = run_gpu(prob, prec)
     assert np.array_equal(g["y"].astype(np.float64), o["y"])
 
