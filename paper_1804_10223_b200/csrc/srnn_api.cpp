@@ -75,7 +75,7 @@ int elem_bytes(bool f16, int bt) { return f16 ? 2 * bt : 4 * bt; }
 
 size_t smem_for(const srnn_plan* p, int units_max, int bt, int n_tiles) {
     size_t s = (static_cast<size_t>(p->cfg.hidden) * elem_bytes(p->f16, bt) + 15) & ~static_cast<size_t>(15);
-    s += static_cast<size_t>(p->G) * units_max * bt * 4;
+    s += 2 * static_cast<size_t>(p->G) * units_max * bt * 4;  // zs + b' staging
     if (p->G == 4) s += static_cast<size_t>(n_tiles) * units_max * bt * 4;
     return s + 16;
 }
@@ -100,19 +100,29 @@ void free_device(srnn_plan* p) {
 }
 
 // Estimated cycles of one tile-step on the busiest CTA (planner cost model,
-// DESIGN.md Sec. 5): shared-memory wavefronts vs issue, plus the reduction
-// latency, plus the exchange round trip.
+// DESIGN.md Sec. 5), calibrated on B200 at C2:
+//   operate  = max(shared-memory wavefronts, issue over 4 SMSPs, the longest
+//              warp's dependent LDS->FMA chain)
+//   load     = poll rounds (one round trip each) + tagged-word ingress bytes
+//   reduce   = xor-butterfly latency, epilogue per item round, exchange RTT.
 double cost_model(const Layout& lay, int bt, int H, int n_tiles, bool f16) {
     const double wf = static_cast<double>(lay.wavefronts_max_cta);
-    const double issue = static_cast<double>(lay.issue_max_cta) * (2 + bt) / 4.0;
+    const double instr_per_slot = f16 ? (3.0 + bt) : (2.0 + bt);
+    const double issue = static_cast<double>(lay.issue_max_cta) * instr_per_slot / 4.0;
+    const double chain = lay.slots_used * 11.0;
     int lg = 0;
     while ((1 << lg) < lay.lanes_per_row) ++lg;
     const double reduce = lg * (30.0 + 2.0 * bt);
-    const double chain = lay.slots_used * 4.0;
     const double words_per_unit = f16 ? (bt == 4 ? 2.0 : 1.0) : bt;
-    const double ingress = static_cast<double>(H) * words_per_unit * 8.0 / 48.0;
-    const double sync = lay.num_ctas > 1 ? 900.0 + 2.0 * lay.num_ctas : 600.0;
-    return n_tiles * (std::max(std::max(wf, issue), chain) + reduce + ingress + sync);
+    const double chunks = static_cast<double>(H) * words_per_unit / 2.0;
+    const double k = f16 ? 8.0 : 4.0;
+    const double groups = std::ceil(chunks / (lay.threads * k));
+    const double load = groups * 900.0 + chunks * 16.0 / 48.0;
+    int umax = 0;
+    for (int c = 0; c < lay.num_ctas; ++c) umax = std::max(umax, lay.cta_unit0[c + 1] - lay.cta_unit0[c]);
+    const double epi = std::ceil(static_cast<double>(umax) * bt / lay.threads) * 300.0;
+    const double sync = lay.num_ctas > 1 ? 1200.0 : 600.0;
+    return n_tiles * (std::max(std::max(wf, issue), chain) + load + reduce + epi + sync);
 }
 
 }  // namespace
@@ -310,7 +320,7 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
         if (smem > static_cast<size_t>(p->smem_optin)) continue;
         for (int L : cands_l) {
             const int rows_max = G * umax;
-            const int threads = std::max(((rows_max * L + 31) / 32) * 32, ((umax * p->BT + 31) / 32) * 32);
+            const int threads = ((rows_max * L + 31) / 32) * 32;
             if (threads > 1024) continue;
             const int np0 = std::max(1, min_np(in, L));
             if (np0 > max_np(p->f16)) continue;

@@ -129,8 +129,7 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
     for (int c = 0; c <= C; ++c) lay.cta_unit0[c] = static_cast<int32_t>((static_cast<int64_t>(c) * H) / C);
     for (int c = 0; c < C; ++c) umax = std::max(umax, lay.cta_unit0[c + 1] - lay.cta_unit0[c]);
     const int rows_max = G * umax;
-    // enough warps for the rows, and enough threads for the epilogue (one per unit x sample)
-    lay.warps = std::max(std::max(1, (rows_max + rpw - 1) / rpw), (umax * in.BT + 31) / 32);
+    lay.warps = std::max(1, (rows_max + rpw - 1) / rpw);
     lay.threads = lay.warps * 32;
     const size_t n_img = static_cast<size_t>(C) * NP * lay.threads;
     lay.col.assign(n_img, 0);

@@ -286,52 +286,61 @@ struct LoadK {
     static constexpr int value = F16 ? (NP <= 48 ? 8 : 4) : 4;
 };
 
+__device__ __forceinline__ void cp_async_f32(float* dst_smem, const float* src) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst_smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <int NP, int BT, int G, bool F16>
 __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent_kernel(const RecParams p) {
     using F = Fmt<F16, BT>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int H = p.H;
-    unsigned char* hs = smem;                                                    // [H][BT] h_{s-1} (offset 0)
-    float* zs = reinterpret_cast<float*>(smem + ((static_cast<size_t>(H) * F::E + 15) & ~static_cast<size_t>(15)));
-    float* cs = zs + G * p.units_max * BT;                                       // LSTM c [n_tiles][Umax][BT]
-    int* s_abort = reinterpret_cast<int*>(cs + (G == 4 ? p.n_tiles * p.units_max * BT : 0));
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
     const int cta = blockIdx.x;
     const int u0 = p.cta_unit0[cta];
     const int U = p.cta_unit0[cta + 1] - u0;
+    const int n_items = U * BT;                       // epilogue items (unit, sample) of one tile
+    const int item_rounds = (n_items + nt - 1) / nt;  // uniform within the CTA
+    const int umax_bt = p.units_max * BT;
+    // shared memory: hs [H][BT] at offset 0 (E bytes per unit), then fp32 areas
+    unsigned char* hs = smem;
+    float* zs = reinterpret_cast<float*>(smem + ((static_cast<size_t>(H) * F::E + 15) & ~static_cast<size_t>(15)));
+    float* bps = zs + G * umax_bt;                           // b'_s of this tile: [item][G]
+    float* cs = bps + G * umax_bt;                           // LSTM c: [n_tiles][item]
+    int* s_abort = reinterpret_cast<int*>(cs + (G == 4 ? p.n_tiles * umax_bt : 0));
+
     const int L = p.lanes_per_row;
     const int n_w = p.warp_slots[cta * (p.threads >> 5) + warp];
     const int n_words = H * F::WPR;
     const int tile_stride = (n_words + 1) & ~1;
+    const int GH = G * H;
 
     // ---- prologue: weights HBM -> registers (once per forward) ----
     Weights<NP, BT, F16> W;
     W.load(p, static_cast<size_t>(cta) * NP * p.threads + tid, n_w);
 
-    // Epilogue role: thread e < U*BT owns (unit e / BT, sample e % BT).
-    const bool epi = tid < U * BT;
-    const int eu = epi ? tid / BT : 0;
-    const int eb = epi ? tid - eu * BT : 0;
-    const int unit = u0 + eu;
     const int krow = warp * (32 / L) + lane / L;  // local row of this lane
     const bool row_leader = (lane % L) == 0 && krow < G * U;
+    if (tid == 0) *s_abort = 0;
 
-    if (tid == 0) {
-        *s_abort = 0;
-        if (U * BT > p.threads) atomicCAS(p.status, 0, -7 /* SRNN_ERR_UNSUPPORTED: planner bug */);
-    }
-
-    // Publish h of (step s, tile k) as tagged words (all threads call: shuffles).
-    auto publish = [&](int s, int k, float h) {
+    // Publish item e's h of (step s, tile k) as tagged words.  Called by all
+    // threads of the CTA (the fp16 pairing uses a shuffle); `ok` masks items.
+    auto publish = [&](int s, int k, int e, bool ok, float h) {
         unsigned long long* dst = p.xbuf + static_cast<size_t>((s & 1) * p.n_tiles + k) * tile_stride;
         const uint32_t tag = p.epoch + static_cast<uint32_t>(s);
+        const int unit = u0 + e / BT, eb = e % BT;
         if (!F16) {
-            if (epi) st_relaxed_u64(dst + unit * BT + eb, pack_tagged(h, tag));
+            if (ok) st_relaxed_u64(dst + unit * BT + eb, pack_tagged(h, tag));
         } else {
             const uint32_t hb = __half_as_ushort(__float2half_rn(h));
             const uint32_t nb = __shfl_down_sync(0xffffffffu, hb, 1);
-            if (epi && (BT == 1 || (eb & 1) == 0)) {
+            if (ok && (BT == 1 || (eb & 1) == 0)) {
                 const uint32_t lo = BT == 1 ? hb : (hb | (nb << 16));
                 st_relaxed_u64(dst + unit * F::WPR + (eb >> 1), (static_cast<unsigned long long>(tag) << 32) | lo);
             }
@@ -340,31 +349,40 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
 
     // ---- publish h_0 (tag = epoch) and initialise c ----
     for (int k = 0; k < p.n_tiles; ++k) {
-        const int bg = k * BT + eb;
-        float h = 0.0f;
-        if (epi) {
-            h = (p.h0 != nullptr && bg < p.B) ? p.h0[static_cast<size_t>(bg) * H + unit] : 0.0f;
-            if (G == 4)
-                cs[(k * p.units_max + eu) * BT + eb] =
-                    (p.c0 != nullptr && bg < p.B) ? p.c0[static_cast<size_t>(bg) * H + unit] : 0.0f;
+        for (int j = 0; j < item_rounds; ++j) {
+            const int e = tid + j * nt;
+            const bool ok = e < n_items;
+            const int unit = u0 + e / BT, bg = k * BT + e % BT;
+            float h = 0.0f;
+            if (ok) {
+                h = (p.h0 != nullptr && bg < p.B) ? p.h0[static_cast<size_t>(bg) * H + unit] : 0.0f;
+                if (G == 4)
+                    cs[k * umax_bt + e] = (p.c0 != nullptr && bg < p.B) ? p.c0[static_cast<size_t>(bg) * H + unit] : 0.0f;
+            }
+            publish(0, k, e, ok, h);
         }
-        publish(0, k, h);
     }
     const bool grid_sync = (p.flags & kFlagGridSync) != 0u;
     if (grid_sync) cg::this_grid().sync();
     __syncthreads();
 
-    const int GH = G * H;
     for (int s = 1; s <= p.T; ++s) {
         for (int k = 0; k < p.n_tiles; ++k) {
-            const int bg = k * BT + eb;
-            // b'_s prefetch for the epilogue (in flight while we spin).
-            float bp[G];
-            if (epi) {
+            // b'_s of this tile -> shared memory, asynchronously (in flight while we spin)
+            for (int j = 0; j < item_rounds; ++j) {
+                const int e = tid + j * nt;
+                if (e < n_items) {
+                    const int unit = u0 + e / BT, bg = k * BT + e % BT;
 #pragma unroll
-                for (int q = 0; q < G; ++q)
-                    bp[q] = bg < p.B ? __ldg(p.bprime + (static_cast<size_t>(s - 1) * p.B + bg) * GH + q * H + unit) : 0.0f;
+                    for (int q = 0; q < G; ++q) {
+                        if (bg < p.B)
+                            cp_async_f32(&bps[e * G + q], p.bprime + (static_cast<size_t>(s - 1) * p.B + bg) * GH + q * H + unit);
+                        else
+                            bps[e * G + q] = 0.0f;
+                    }
+                }
             }
+            cp_async_commit();
             // ---- load: h_{s-1} tile k -> hs ----
             const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
                 p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
@@ -389,34 +407,41 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                     for (int b = 0; b < BT; ++b) zs[krow * BT + b] = acc[b];
                 }
             }
+            cp_async_wait_all();
             __syncthreads();
 
             // ---- epilogue: activation / gates, y, tagged publish of h_s ----
-            float h = 0.0f;
-            if (epi) {
-                if (G == 1) {
-                    h = activation(p.act, zs[eu * BT + eb] + bp[0]);
-                } else {
-                    const float zi = zs[(0 * U + eu) * BT + eb] + bp[0];
-                    const float zf = zs[(1 * U + eu) * BT + eb] + bp[1 % G];
-                    const float zg = zs[(2 * U + eu) * BT + eb] + bp[2 % G];
-                    const float zo = zs[(3 * U + eu) * BT + eb] + bp[3 % G];
-                    float* cp = &cs[(k * p.units_max + eu) * BT + eb];
-                    const float c = sigmoidf_acc(zf) * (*cp) + sigmoidf_acc(zi) * tanhf(zg);
-                    *cp = c;
-                    h = sigmoidf_acc(zo) * tanhf(c);
-                    if (s == p.T && p.cT != nullptr && bg < p.B) p.cT[static_cast<size_t>(bg) * H + unit] = c;
-                }
-                if (bg < p.B) {
-                    if (p.y != nullptr) p.y[(static_cast<size_t>(s - 1) * p.B + bg) * H + unit] = h;
-                    if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + unit] = h;
-                }
-                if (p.flags & kFlagJitter) {
-                    const uint32_t r = (static_cast<uint32_t>(cta) * 2654435761u) ^ (static_cast<uint32_t>(s * 40503 + k));
-                    __nanosleep((r >> 7) & 2047u);
-                }
+            if ((p.flags & kFlagJitter) && tid == 0) {
+                const uint32_t r = (static_cast<uint32_t>(cta) * 2654435761u) ^ (static_cast<uint32_t>(s * 40503 + k));
+                __nanosleep((r >> 7) & 2047u);
             }
-            publish(s, k, h);
+            for (int j = 0; j < item_rounds; ++j) {
+                const int e = tid + j * nt;
+                const bool ok = e < n_items;
+                float h = 0.0f;
+                if (ok) {
+                    const int unit = u0 + e / BT, bg = k * BT + e % BT;
+                    if (G == 1) {
+                        h = activation(p.act, zs[e] + bps[e]);
+                    } else {
+                        const int ub = U * BT;
+                        const float zi = zs[0 * ub + e] + bps[e * G + 0];
+                        const float zf = zs[1 * ub + e] + bps[e * G + 1 % G];
+                        const float zg = zs[2 * ub + e] + bps[e * G + 2 % G];
+                        const float zo = zs[3 * ub + e] + bps[e * G + 3 % G];
+                        float* cp = &cs[k * umax_bt + e];
+                        const float c = sigmoidf_acc(zf) * (*cp) + sigmoidf_acc(zi) * tanhf(zg);
+                        *cp = c;
+                        h = sigmoidf_acc(zo) * tanhf(c);
+                        if (s == p.T && p.cT != nullptr && bg < p.B) p.cT[static_cast<size_t>(bg) * H + unit] = c;
+                    }
+                    if (bg < p.B) {
+                        if (p.y != nullptr) p.y[(static_cast<size_t>(s - 1) * p.B + bg) * H + unit] = h;
+                        if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + unit] = h;
+                    }
+                }
+                publish(s, k, e, ok, h);
+            }
             if (grid_sync) cg::this_grid().sync();
         }
     }

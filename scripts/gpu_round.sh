@@ -1,10 +1,11 @@
 #!/bin/bash
-# One GPU session: tests, bench, variants, ncu.  Output under gpurun_out/.
+# One GPU session: tests, timing variants, bench, ncu.  Output under gpurun_out/.
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q -x ${TESTSEL:-} > gpurun_out/gpu_tests.log 2>&1; echo tests=$?
+if [ -z "$NOTEST" ]; then timeout 1200 python -m pytest tests -m gpu -q -x ${TESTSEL:-} > gpurun_out/gpu_tests.log 2>&1; echo tests=$?; fi
 rm -f gpurun_out/qt.log
-for args in "" "--L 32" "--L 16" "--flags 32" "--flags 1" "--prec fp32" "--prec fp32 --L 32"; do
+IFS=';' read -ra VARS <<< "${QT:-;--L 32;--L 16;--d 0;--d 0 --flags 1;--flags 1;--prec fp32}"
+for args in "${VARS[@]}"; do
   timeout 120 python scripts/quick_time.py $args >> gpurun_out/qt.log 2>&1
 done
 if [ -n "$BENCH" ]; then timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$?; fi
