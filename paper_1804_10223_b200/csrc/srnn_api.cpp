@@ -191,6 +191,10 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     // narrower tiles when B_max < 4 or when h staging would not fit.
     p->f16 = c.prec == SRNN_PREC_FP16W_FP32ACC && (c.flags & SRNN_FLAG_FP32_STAGING) == 0;
     int bt = c.batch >= 4 ? 4 : (c.batch >= 2 ? 2 : 1);
+    if (const char* e = std::getenv("SRNN_BT")) {  // experiment override: batch tile width
+        const int v = std::atoi(e);
+        if (v == 1 || v == 2 || v == 4) bt = std::min(bt, v);
+    }
     // fp16 register pairs carry the hs byte offset in 16 bits: H * E <= 65536
     while (p->f16 && bt > 1 && static_cast<int64_t>(c.hidden) * elem_bytes(true, bt) > 65536) bt /= 2;
     if (p->f16 && static_cast<int64_t>(c.hidden) * elem_bytes(true, bt) > 65536) {

@@ -1,0 +1,234 @@
+// microbench_exchange.cu -- B200 floors for the per-step inter-CTA exchange
+// (SURVEY.md Sec. 7 step 3): what one timestep costs with NO compute, for the
+// synchronisation schemes the recurrent kernel can use.
+//
+//   pingpong      2 CTAs bounce a tagged word through L2: one-way latency
+//   gridsync      cooperative-groups grid.sync() per step
+//   a2a_flag      every CTA publishes one tagged word, polls all 148
+//   a2a_bulk      every CTA publishes its slice of tagged words (fp16 pairs +
+//                 tag, the kernel's format) and polls the whole h (batch poll)
+//   a2a_sent      poll one sentinel word per producer, then one bulk read
+//   a2a_relacq    raw data + st.release flag per producer; ld.acquire flag,
+//                 then plain bulk read of the raw data (half the bytes)
+//
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mb scripts/microbench_exchange.cu
+// run:   ./mb [units_per_cta=16] [words_per_unit=2] [steps=2000]
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+namespace cg = cooperative_groups;
+
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+    unsigned long long r;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ ulonglong2 ld_relaxed_v2(const ulonglong2* p) {
+    ulonglong2 r;
+    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(r.x), "=l"(r.y) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned r;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ uint4 ld_cg_v4(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.relaxed.gpu.global.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+
+struct Args {
+    int steps, upc, wpu;  // units per CTA, tagged words per unit
+    unsigned long long* words;  // [2][ncta*upc*wpu]
+    unsigned* flags;            // [ncta]
+    uint2* raw;                 // [2][ncta*upc] raw fp16x4 data
+    long long* out;
+};
+
+__global__ void k_pingpong(Args a) {
+    if (threadIdx.x != 0 || blockIdx.x > 1) return;
+    unsigned long long* w = a.words;
+    long long t0 = clock64();
+    for (int s = 1; s <= a.steps; ++s) {
+        if (blockIdx.x == (s & 1)) {
+            while (ld_relaxed(w) != static_cast<unsigned long long>(s - 1)) {
+            }
+            st_relaxed(w, s);
+        }
+    }
+    if (blockIdx.x == 0) a.out[0] = clock64() - t0;
+}
+
+__global__ void k_gridsync(Args a) {
+    cg::grid_group g = cg::this_grid();
+    for (int s = 0; s < a.steps; ++s) g.sync();
+}
+
+__global__ void k_a2a_flag(Args a) {
+    const int n = gridDim.x;
+    for (int s = 1; s <= a.steps; ++s) {
+        if (threadIdx.x == 0) st_relaxed(a.words + blockIdx.x, s);
+        if (threadIdx.x < n)
+            while (ld_relaxed(a.words + threadIdx.x) < static_cast<unsigned long long>(s)) {
+            }
+        __syncthreads();
+    }
+}
+
+// tagged bulk: word = (tag << 32) | payload
+__global__ void k_a2a_bulk(Args a) {
+    const int n = gridDim.x;
+    const int per = a.upc * a.wpu;
+    const int total = n * per;
+    const int chunks = total / 2;
+    for (int s = 1; s <= a.steps; ++s) {
+        unsigned long long* dst = a.words + static_cast<size_t>(s & 1) * total;
+        for (int i = threadIdx.x; i < per; i += blockDim.x)
+            st_relaxed(dst + blockIdx.x * per + i, (static_cast<unsigned long long>(s) << 32) | i);
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(dst);
+        // batch poll, <= 8 chunks per thread in flight
+        for (int base = threadIdx.x; base < chunks; base += 8 * blockDim.x) {
+            ulonglong2 v[8];
+            unsigned pend = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                int idx = base + j * blockDim.x;
+                if (idx < chunks) {
+                    v[j] = ld_relaxed_v2(src + idx);
+                    pend |= 1u << j;
+                }
+            }
+            while (pend) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if ((pend >> j & 1) && (v[j].x >> 32) == static_cast<unsigned long long>(s) &&
+                        (v[j].y >> 32) == static_cast<unsigned long long>(s))
+                        pend &= ~(1u << j);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (pend >> j & 1) v[j] = ld_relaxed_v2(src + base + j * blockDim.x);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// sentinel: poll the last word of each producer's slice, then one bulk read
+__global__ void k_a2a_sent(Args a) {
+    const int n = gridDim.x;
+    const int per = a.upc * a.wpu;
+    const int total = n * per;
+    const int chunks = total / 2;
+    __shared__ unsigned long long sink;
+    unsigned long long acc = 0;
+    for (int s = 1; s <= a.steps; ++s) {
+        unsigned long long* dst = a.words + static_cast<size_t>(s & 1) * total;
+        for (int i = threadIdx.x; i < per; i += blockDim.x)
+            st_relaxed(dst + blockIdx.x * per + i, (static_cast<unsigned long long>(s) << 32) | i);
+        if (threadIdx.x < n)
+            while ((ld_relaxed(dst + threadIdx.x * per + per - 1) >> 32) != static_cast<unsigned long long>(s)) {
+            }
+        __syncthreads();
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(dst);
+        for (int idx = threadIdx.x; idx < chunks; idx += blockDim.x) {
+            ulonglong2 v = ld_relaxed_v2(src + idx);
+            while ((v.x >> 32) != static_cast<unsigned long long>(s) || (v.y >> 32) != static_cast<unsigned long long>(s))
+                v = ld_relaxed_v2(src + idx);
+            acc += v.x;
+        }
+        __syncthreads();
+    }
+    if (acc == 12345) sink = acc;
+}
+
+// release/acquire: raw fp16x4 per unit (8 B), one flag per producer
+__global__ void k_a2a_relacq(Args a) {
+    const int n = gridDim.x;
+    const int per = a.upc;  // units
+    const int total = n * per;
+    __shared__ unsigned long long sink;
+    unsigned acc = 0;
+    for (int s = 1; s <= a.steps; ++s) {
+        uint2* dst = a.raw + static_cast<size_t>(s & 1) * total;
+        for (int i = threadIdx.x; i < per; i += blockDim.x) dst[blockIdx.x * per + i] = make_uint2(s, i);
+        __syncthreads();
+        if (threadIdx.x == 0) st_release(a.flags + blockIdx.x, s);
+        if (threadIdx.x < n)
+            while (ld_acquire(a.flags + threadIdx.x) < static_cast<unsigned>(s)) {
+            }
+        __syncthreads();
+        const uint4* src = reinterpret_cast<const uint4*>(dst);
+        for (int idx = threadIdx.x; idx < total / 2; idx += blockDim.x) {
+            uint4 v = ld_cg_v4(src + idx);
+            acc += v.x + v.z;
+        }
+        __syncthreads();
+    }
+    if (acc == 12345) sink = acc;
+}
+
+static float run(void* fn, Args a, int grid, int block) {
+    void* args[] = {&a};
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaMemset(a.words, 0, static_cast<size_t>(2) * 148 * 64 * 8 * 8);
+    cudaMemset(a.flags, 0, 148 * 4 * 4);
+    cudaLaunchCooperativeKernel(fn, grid, block, args, 0, 0);  // warm
+    cudaDeviceSynchronize();
+    cudaMemset(a.words, 0, static_cast<size_t>(2) * 148 * 64 * 8 * 8);
+    cudaMemset(a.flags, 0, 148 * 4 * 4);
+    cudaEventRecord(e0);
+    cudaLaunchCooperativeKernel(fn, grid, block, args, 0, 0);
+    cudaEventRecord(e1);
+    cudaError_t err = cudaDeviceSynchronize();
+    if (err != cudaSuccess) {
+        printf("error %s\n", cudaGetErrorString(err));
+        exit(1);
+    }
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    return ms * 1000.0f / a.steps;
+}
+
+int main(int argc, char** argv) {
+    Args a;
+    a.upc = argc > 1 ? atoi(argv[1]) : 16;
+    a.wpu = argc > 2 ? atoi(argv[2]) : 2;
+    a.steps = argc > 3 ? atoi(argv[3]) : 2000;
+    int ncta = 148;
+    cudaMalloc(&a.words, static_cast<size_t>(2) * 148 * 64 * 8 * 8);
+    cudaMalloc(&a.flags, 148 * 4 * 4);
+    cudaMalloc(&a.raw, static_cast<size_t>(2) * 148 * 64 * 8);
+    cudaMalloc(&a.out, 64);
+    cudaMemset(a.words, 0, static_cast<size_t>(2) * 148 * 64 * 8 * 8);
+    printf("{\"units_per_cta\": %d, \"words_per_unit\": %d, \"steps\": %d", a.upc, a.wpu, a.steps);
+    float pp = run(reinterpret_cast<void*>(k_pingpong), a, 2, 32);
+    long long cyc;
+    cudaMemcpy(&cyc, a.out, 8, cudaMemcpyDeviceToHost);
+    printf(", \"pingpong_us_per_hop\": %.4f, \"pingpong_cycles_per_hop\": %.1f", pp, static_cast<double>(cyc) / a.steps);
+    for (int blk : {512}) {
+        printf(", \"gridsync_us\": %.4f", run(reinterpret_cast<void*>(k_gridsync), a, ncta, blk));
+        printf(", \"a2a_flag_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_flag), a, ncta, blk));
+        printf(", \"a2a_bulk_tagged_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_bulk), a, ncta, blk));
+        printf(", \"a2a_sentinel_then_bulk_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_sent), a, ncta, blk));
+        printf(", \"a2a_release_acquire_raw_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_relacq), a, ncta, blk));
+    }
+    printf(", \"bytes_tagged_per_cta\": %d, \"bytes_raw_per_cta\": %d}\n", ncta * a.upc * a.wpu * 8, ncta * a.upc * 8);
+    return 0;
+}

@@ -26,7 +26,10 @@ def main():
     ap.add_argument("--C", type=int, default=0)
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--bt", type=int, default=0, help="SRNN_BT override (batch tile)")
     a = ap.parse_args()
+    if a.bt:
+        os.environ["SRNN_BT"] = str(a.bt)
     prob = inputs.make_problem(a.H, a.H, a.B, a.T, a.d, cell=a.cell)
     m = from_problem(prob, prec=a.prec, flags=a.flags, num_ctas=a.C, lanes_per_row=a.L)
     x = torch.from_numpy(prob["x"]).cuda()
