@@ -83,6 +83,7 @@ typedef enum { SRNN_PREC_FP32 = 0, SRNN_PREC_FP16W_FP32ACC = 1 } srnn_prec_t;
 #define SRNN_FLAG_FP32_STAGING   (1u << 5) /* fp16 mode: stage/exchange h in fp32 and keep fp32
                                               register pairs (ablation; default fp16 staging and
                                               one register per pair)        */
+#define SRNN_FLAG_PROFILE        (1u << 6) /* record per-CTA phase timestamps (srnn_plan_debug_timeline) */
 
 typedef struct {
     int32_t hidden;     /* H >= 1, <= 65536 (u16 column index)                          */
@@ -193,6 +194,13 @@ srnn_status_t srnn_plan_status(srnn_plan_t plan);
  * Errors: SRNN_ERR_STATE before load, SRNN_ERR_INVALID_VALUE if too small. */
 srnn_status_t srnn_plan_export_layout(srnn_plan_t plan, int32_t *col_out, float *val_out,
                                       int32_t *row_out, int64_t capacity);
+
+/* Debug: with SRNN_FLAG_PROFILE, copy the clock64 stamps of the last forward
+ * to host `out` as [num_ctas][T][num_tiles][4] int64: step start, h staged,
+ * operate+reduce done, h published (SM cycle counter of that CTA's SM).
+ * `capacity` in elements; returns the element count via *count.
+ * Errors: SRNN_ERR_STATE without the flag or before a forward. */
+srnn_status_t srnn_plan_debug_timeline(srnn_plan_t plan, int64_t *out, int64_t capacity, int64_t *count);
 
 /* Human-readable name of a status code (static storage). */
 const char *srnn_status_string(srnn_status_t status);

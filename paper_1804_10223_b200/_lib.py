@@ -27,10 +27,11 @@ FLAG_HOST_ONLY = 1 << 2
 FLAG_SIMT_GEMM = 1 << 3
 FLAG_DEBUG_JITTER = 1 << 4
 FLAG_FP32_STAGING = 1 << 5
+FLAG_PROFILE = 1 << 6
 
 EXPORTED = ["srnn_plan_create", "srnn_plan_query", "srnn_load_weights", "srnn_forward", "srnn_input_projection",
             "srnn_recurrence", "srnn_forward_host", "srnn_plan_status", "srnn_plan_export_layout",
-            "srnn_status_string", "srnn_version", "srnn_destroy"]
+            "srnn_status_string", "srnn_version", "srnn_destroy", "srnn_plan_debug_timeline"]
 
 
 class SrnnError(RuntimeError):
@@ -85,6 +86,7 @@ def load_library(path: str = LIB_PATH):
         "srnn_status_string": ([I32], ctypes.c_char_p),
         "srnn_version": ([], ctypes.c_char_p),
         "srnn_destroy": ([P], I32),
+        "srnn_plan_debug_timeline": ([P, P, I64, ctypes.POINTER(I64)], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -254,6 +256,15 @@ class SparseRNN:
         _check("srnn_forward_host", self.lib.srnn_forward_host(self.handle, T, B, _ptr(x), _ptr(h0), _ptr(c0),
                                                                _ptr(y), _ptr(hT), _ptr(cT)))
         return (y, hT, cT) if self.G == 4 else (y, hT)
+
+    def debug_timeline(self):
+        """[num_ctas, T, n_tiles, 4] clock64 stamps of the last forward (SRNN_FLAG_PROFILE)."""
+        n = ctypes.c_int64()
+        _check("srnn_plan_debug_timeline", self.lib.srnn_plan_debug_timeline(self.handle, None, 0, ctypes.byref(n)))
+        out = np.empty(n.value, np.int64)
+        _check("srnn_plan_debug_timeline",
+               self.lib.srnn_plan_debug_timeline(self.handle, _ptr(out), n.value, ctypes.byref(n)))
+        return out
 
     def status(self):
         """srnn_plan_status after a stream sync; raises on a device-side error."""

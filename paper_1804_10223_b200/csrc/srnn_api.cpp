@@ -48,6 +48,8 @@ struct srnn_plan {
     cudaStream_t stream = nullptr;
     float *d_x = nullptr, *d_h0 = nullptr, *d_c0 = nullptr, *d_y = nullptr, *d_hT = nullptr, *d_cT = nullptr;
     unsigned long long timeout_ns = 2000000000ull;
+    long long* d_prof = nullptr;
+    int64_t prof_elems = 0;
 };
 
 namespace {
@@ -95,6 +97,7 @@ void free_device(srnn_plan* p) {
     cudaFree(p->d_y);
     cudaFree(p->d_hT);
     cudaFree(p->d_cT);
+    cudaFree(p->d_prof);
     if (p->stream) cudaStreamDestroy(p->stream);
     p->d_img = nullptr;
 }
@@ -503,6 +506,16 @@ srnn_status_t srnn_recurrence(srnn_plan_t p, int32_t T, int32_t B, const float* 
     rp.xbuf = p->d_xbuf;
     rp.status = p->d_status;
     rp.timeout_ns = p->timeout_ns;
+    if (p->cfg.flags & SRNN_FLAG_PROFILE) {
+        const int64_t need = static_cast<int64_t>(p->lay.num_ctas) * T * rp.n_tiles * 4;
+        if (need > p->prof_elems) {
+            cudaFree(p->d_prof);
+            p->d_prof = nullptr;
+            if (cudaMalloc(&p->d_prof, need * 8) != cudaSuccess) return SRNN_ERR_CUDA;
+        }
+        p->prof_elems = need;
+        rp.profile = p->d_prof;
+    }
     int e = launch_recurrent(p->np_inst, p->BT, p->G, p->f16 ? 1 : 0, rp, p->lay.num_ctas, p->smem_bytes, stream,
                              false, nullptr, nullptr);
     if (e != 0) return SRNN_ERR_CUDA;
@@ -577,6 +590,17 @@ srnn_status_t srnn_plan_export_layout(srnn_plan_t p, int32_t* col_out, float* va
     if (val_out) std::memcpy(val_out, p->lay.val.data(), n * 4);
     if (row_out) std::memcpy(row_out, p->lay.row.data(), n * 4);
     return SRNN_OK;
+}
+
+srnn_status_t srnn_plan_debug_timeline(srnn_plan_t p, int64_t* out, int64_t capacity, int64_t* count) {
+    if (!p || !count) return SRNN_ERR_INVALID_VALUE;
+    if (!(p->cfg.flags & SRNN_FLAG_PROFILE) || !p->d_prof) return SRNN_ERR_STATE;
+    *count = p->prof_elems;
+    if (!out) return SRNN_OK;
+    if (capacity < p->prof_elems) return SRNN_ERR_INVALID_VALUE;
+    DeviceGuard g(p->cfg.device);
+    return cudaMemcpy(out, p->d_prof, p->prof_elems * 8, cudaMemcpyDeviceToHost) == cudaSuccess ? SRNN_OK
+                                                                                                : SRNN_ERR_CUDA;
 }
 
 srnn_status_t srnn_destroy(srnn_plan_t p) {

@@ -39,6 +39,7 @@ namespace cg = cooperative_groups;
 // Flag bits mirrored from include/srnn.h (device side only needs these).
 constexpr uint32_t kFlagGridSync = 1u << 0;
 constexpr uint32_t kFlagJitter = 1u << 4;
+constexpr uint32_t kFlagProfile = 1u << 6;
 
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -368,6 +369,10 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
 
     for (int s = 1; s <= p.T; ++s) {
         for (int k = 0; k < p.n_tiles; ++k) {
+            long long* prof = (p.flags & kFlagProfile) && p.profile != nullptr && tid == 0
+                                  ? p.profile + ((static_cast<size_t>(cta) * p.T + (s - 1)) * p.n_tiles + k) * 4
+                                  : nullptr;
+            if (prof) prof[0] = clock64();
             // b'_s of this tile -> shared memory, asynchronously (in flight while we spin)
             for (int j = 0; j < item_rounds; ++j) {
                 const int e = tid + j * nt;
@@ -390,6 +395,7 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                                                             !grid_sync, p.status, p.timeout_ns))
                 *s_abort = 1;
             __syncthreads();
+            if (prof) prof[1] = clock64();
             if (*s_abort) goto done;
 
             // ---- operate + reduce ----
@@ -409,6 +415,7 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
             }
             cp_async_wait_all();
             __syncthreads();
+            if (prof) prof[2] = clock64();
 
             // ---- epilogue: activation / gates, y, tagged publish of h_s ----
             if ((p.flags & kFlagJitter) && tid == 0) {
@@ -442,6 +449,7 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                 }
                 publish(s, k, e, ok, h);
             }
+            if (prof) prof[3] = clock64();
             if (grid_sync) cg::this_grid().sync();
         }
     }

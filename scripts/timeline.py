@@ -1,0 +1,53 @@
+"""Per-phase timeline of the persistent kernel (SRNN_FLAG_PROFILE): where a step goes.
+
+usage: python scripts/timeline.py [--H 2304 --B 4 --d 0.3 --T 256 --prec fp16 --L 0 --bt 0 --flags 0]
+Prints median / p90 cycles per phase over CTAs and steps (skipping the first 8 steps).
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1804_10223_b200 import FLAG_PROFILE, from_problem, inputs  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--H", type=int, default=2304)
+ap.add_argument("--B", type=int, default=4)
+ap.add_argument("--d", type=float, default=0.3)
+ap.add_argument("--T", type=int, default=256)
+ap.add_argument("--prec", default="fp16")
+ap.add_argument("--cell", default="rnn")
+ap.add_argument("--L", type=int, default=0)
+ap.add_argument("--C", type=int, default=0)
+ap.add_argument("--bt", type=int, default=0)
+ap.add_argument("--flags", type=int, default=0)
+a = ap.parse_args()
+if a.bt:
+    os.environ["SRNN_BT"] = str(a.bt)
+prob = inputs.make_problem(a.H, a.H, a.B, a.T, a.d, cell=a.cell)
+m = from_problem(prob, prec=a.prec, flags=a.flags | FLAG_PROFILE, num_ctas=a.C, lanes_per_row=a.L)
+x = torch.from_numpy(prob["x"]).cuda()
+for _ in range(3):
+    m.forward(x)
+torch.cuda.synchronize()
+m.status()
+inf = m.info()
+tl = m.debug_timeline().reshape(inf["num_ctas"], a.T, -1, 4)
+nt = tl.shape[2]
+flat = tl.reshape(inf["num_ctas"], a.T * nt, 4).astype(np.float64)
+load = flat[:, :, 1] - flat[:, :, 0]
+oper = flat[:, :, 2] - flat[:, :, 1]
+epi = flat[:, :, 3] - flat[:, :, 2]
+gap = flat[:, 1:, 0] - flat[:, :-1, 3]
+period = flat[:, 1:, 0] - flat[:, :-1, 0]
+sk = 8 * nt
+res = {"cfg": vars(a), "plan": {k: inf[k] for k in ("num_ctas", "threads_per_cta", "lanes_per_row", "pairs_per_lane",
+                                                     "slots_used", "batch_tile", "wavefronts_per_step_max")}}
+for name, v in (("load", load[:, sk:]), ("operate", oper[:, sk:]), ("epilogue", epi[:, sk:]), ("gap", gap[:, sk:]),
+                ("tile_period", period[:, sk:])):
+    res[name] = {"median": float(np.median(v)), "p10": float(np.percentile(v, 10)), "p90": float(np.percentile(v, 90))}
+print(json.dumps(res))
