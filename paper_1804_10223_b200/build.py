@@ -48,6 +48,8 @@ def _compile(src, verbose=False):
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
     os.replace(obj + ".tmp", obj)
+    with open(obj + ".ptxas.log", "w") as f:
+        f.write(r.stderr)
     return obj, r.stderr
 
 
@@ -61,10 +63,10 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
         for obj, log in ex.map(lambda s: _compile(s, verbose), srcs):
             objs.append(obj)
             logs.append(log)
-    with open(os.path.join(OBJ, "ptxas.log"), "a") as f:
-        for log in logs:
-            if log:
-                f.write(log)
+    with open(os.path.join(OBJ, "ptxas.log"), "w") as f:
+        for o in objs:
+            if os.path.exists(o + ".ptxas.log"):
+                f.write(open(o + ".ptxas.log").read())
     newest = max(os.path.getmtime(o) for o in objs)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
         cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB + ".tmp"] + objs + ["-cudart", "static"]

@@ -77,7 +77,7 @@ int elem_bytes(bool f16, int bt) { return f16 ? 2 * bt : 4 * bt; }
 
 size_t smem_for(const srnn_plan* p, int units_max, int bt, int n_tiles) {
     size_t s = (static_cast<size_t>(p->cfg.hidden) * elem_bytes(p->f16, bt) + 15) & ~static_cast<size_t>(15);
-    s += 2 * static_cast<size_t>(p->G) * units_max * bt * 4;  // zs + b' staging
+    s += 3 * static_cast<size_t>(p->G) * units_max * bt * 4;  // zs + double-buffered b' staging
     if (p->G == 4) s += static_cast<size_t>(n_tiles) * units_max * bt * 4;
     return s + 16;
 }
@@ -190,10 +190,11 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
         delete p;
         return SRNN_ERR_INVALID_VALUE;
     }
-    // Batch tile: the paper's wide load interleaves 4 samples;
-    // narrower tiles when B_max < 4 or when h staging would not fit.
     p->f16 = c.prec == SRNN_PREC_FP16W_FP32ACC && (c.flags & SRNN_FLAG_FP32_STAGING) == 0;
-    int bt = c.batch >= 4 ? 4 : (c.batch >= 2 ? 2 : 1);
+    // Batch tile: the paper's wide load interleaves 4 samples.
+    // We keep >= 2 tiles whenever B >= 2 so the exchange of one tile overlaps
+    // the compute of the next (tiles are independent sequences).
+    int bt = c.batch >= 8 ? 4 : (c.batch >= 4 ? 2 : 1);
     if (const char* e = std::getenv("SRNN_BT")) {  // experiment override: batch tile width
         const int v = std::atoi(e);
         if (v == 1 || v == 2 || v == 4) bt = std::min(bt, v);

@@ -138,12 +138,12 @@ struct Fmt {
 template <bool F16, int BT, int K>
 __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, unsigned char* hs, int n_words,
                                           uint32_t want, bool spin, int32_t* status,
-                                          unsigned long long timeout_ns) {
+                                          unsigned long long timeout_ns, int first = 0) {
     const int n_chunks = (n_words + 1) >> 1;
     const int nt = blockDim.x;
     Watchdog wd{0ull, 0u};
     bool ok = true;
-    for (int base = threadIdx.x; base < n_chunks; base += K * nt) {
+    for (int base = threadIdx.x + first; base < n_chunks; base += K * nt) {
         ulonglong2 v[K];
         uint32_t pend = 0u;
 #pragma unroll
@@ -183,6 +183,62 @@ __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, un
     }
     return ok;
 }
+
+// Register prefetch of the first KP chunks per thread of a tile: issued one
+// tile-phase early (while the current tile computes), validated when the
+// tile is due.  Chunks beyond KP*nt go through load_tile synchronously.
+template <bool F16, int BT, int KP>
+struct Prefetch {
+    ulonglong2 v[KP];
+    __device__ __forceinline__ void issue(const ulonglong2* __restrict__ src, int n_words) {
+        const int n_chunks = (n_words + 1) >> 1;
+#pragma unroll
+        for (int j = 0; j < KP; ++j) {
+            const int idx = threadIdx.x + j * blockDim.x;
+            if (idx < n_chunks) v[j] = ld_relaxed_v2(src + idx);
+        }
+    }
+    __device__ __forceinline__ bool finish(const ulonglong2* __restrict__ src, unsigned char* hs, int n_words,
+                                           uint32_t want, bool spin, int32_t* status,
+                                           unsigned long long timeout_ns) {
+        const int n_chunks = (n_words + 1) >> 1;
+        const int nt = blockDim.x;
+        uint32_t pend = 0u;
+#pragma unroll
+        for (int j = 0; j < KP; ++j)
+            if (threadIdx.x + j * nt < n_chunks) pend |= 1u << j;
+        Watchdog wd{0ull, 0u};
+        bool ok = true;
+        while (true) {
+#pragma unroll
+            for (int j = 0; j < KP; ++j) {
+                if (pend & (1u << j)) {
+                    const int idx = threadIdx.x + j * nt;
+                    const bool has1 = 2 * idx + 1 < n_words;
+                    if (tag_of(v[j].x) == want && (!has1 || tag_of(v[j].y) == want)) {
+                        Fmt<F16, BT>::store(hs, idx, v[j].x, v[j].y, has1);
+                        pend &= ~(1u << j);
+                    }
+                }
+            }
+            if (pend == 0u) break;
+            if (!spin) {
+                atomicCAS(status, 0, -4);
+                break;
+            }
+            if (watchdog_tick(wd, status, timeout_ns)) {
+                ok = false;
+                break;
+            }
+#pragma unroll
+            for (int j = 0; j < KP; ++j)
+                if (pend & (1u << j)) v[j] = ld_relaxed_v2(src + threadIdx.x + j * nt);
+        }
+        if (ok && n_chunks > KP * nt)
+            ok = load_tile<F16, BT, 4>(src, hs, n_words, want, spin, status, timeout_ns, KP * nt);
+        return ok;
+    }
+};
 
 // ---------------------------------------------------------------------------
 // Register-resident weights and the operate stage.
@@ -312,8 +368,8 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     // shared memory: hs [H][BT] at offset 0 (E bytes per unit), then fp32 areas
     unsigned char* hs = smem;
     float* zs = reinterpret_cast<float*>(smem + ((static_cast<size_t>(H) * F::E + 15) & ~static_cast<size_t>(15)));
-    float* bps = zs + G * umax_bt;                           // b'_s of this tile: [item][G]
-    float* cs = bps + G * umax_bt;                           // LSTM c: [n_tiles][item]
+    float* bps = zs + G * umax_bt;                           // b'_s, double-buffered: [2][item][G]
+    float* cs = bps + 2 * G * umax_bt;                       // LSTM c: [n_tiles][item]
     int* s_abort = reinterpret_cast<int*>(cs + (G == 4 ? p.n_tiles * umax_bt : 0));
 
     const int L = p.lanes_per_row;
@@ -367,33 +423,53 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     if (grid_sync) cg::this_grid().sync();
     __syncthreads();
 
+    // Prefetch of tile (s, k): its h_{s-1} tagged words into registers and its
+    // b'_s rows into bps[buf] (cp.async).  With >= 2 batch tiles the next
+    // tile's input was published one tile-phase ago, so it is issued before the
+    // current tile computes and lands while it does ("as we
+    // process iteration n, we can load the states for iteration n+1").
+    Prefetch<F16, BT, 4> pf;
+    const bool early = p.n_tiles > 1 && !grid_sync;
+    auto issue_tile = [&](int s, int k, int buf) {
+        pf.issue(reinterpret_cast<const ulonglong2*>(p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) *
+                                                                 tile_stride),
+                 n_words);
+        float* bb = bps + buf * G * umax_bt;
+        for (int j = 0; j < item_rounds; ++j) {
+            const int e = tid + j * nt;
+            if (e < n_items) {
+                const int unit = u0 + e / BT, bg = k * BT + e % BT;
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    if (bg < p.B)
+                        cp_async_f32(&bb[e * G + q], p.bprime + (static_cast<size_t>(s - 1) * p.B + bg) * GH + q * H + unit);
+                    else
+                        bb[e * G + q] = 0.0f;
+                }
+            }
+        }
+        cp_async_commit();
+    };
+    int buf = 0;
+    issue_tile(1, 0, 0);
+
     for (int s = 1; s <= p.T; ++s) {
         for (int k = 0; k < p.n_tiles; ++k) {
             long long* prof = (p.flags & kFlagProfile) && p.profile != nullptr && tid == 0
                                   ? p.profile + ((static_cast<size_t>(cta) * p.T + (s - 1)) * p.n_tiles + k) * 4
                                   : nullptr;
             if (prof) prof[0] = clock64();
-            // b'_s of this tile -> shared memory, asynchronously (in flight while we spin)
-            for (int j = 0; j < item_rounds; ++j) {
-                const int e = tid + j * nt;
-                if (e < n_items) {
-                    const int unit = u0 + e / BT, bg = k * BT + e % BT;
-#pragma unroll
-                    for (int q = 0; q < G; ++q) {
-                        if (bg < p.B)
-                            cp_async_f32(&bps[e * G + q], p.bprime + (static_cast<size_t>(s - 1) * p.B + bg) * GH + q * H + unit);
-                        else
-                            bps[e * G + q] = 0.0f;
-                    }
-                }
-            }
-            cp_async_commit();
             // ---- load: h_{s-1} tile k -> hs ----
-            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
-                p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
-            if (!load_tile<F16, BT, LoadK<NP, F16>::value>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
-                                                            !grid_sync, p.status, p.timeout_ns))
-                *s_abort = 1;
+            {
+                const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
+                    p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
+                if (!pf.finish(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1), !grid_sync, p.status,
+                               p.timeout_ns))
+                    *s_abort = 1;
+            }
+            const int ns = k + 1 < p.n_tiles ? s : s + 1, nk = k + 1 < p.n_tiles ? k + 1 : 0;
+            const bool issued_early = early && ns <= p.T;
+            if (issued_early) issue_tile(ns, nk, buf ^ 1);
             __syncthreads();
             if (prof) prof[1] = clock64();
             if (*s_abort) goto done;
@@ -404,16 +480,22 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
 #pragma unroll
                 for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
                 W.operate(acc, hs, n_w);
-                for (int m = L >> 1; m >= 1; m >>= 1) {
 #pragma unroll
-                    for (int b = 0; b < BT; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], m);
+                for (int m = 16; m >= 1; m >>= 1) {
+                    if (m < L) {
+#pragma unroll
+                        for (int b = 0; b < BT; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], m);
+                    }
                 }
                 if (row_leader) {
 #pragma unroll
                     for (int b = 0; b < BT; ++b) zs[krow * BT + b] = acc[b];
                 }
             }
-            cp_async_wait_all();
+            if (issued_early)
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            else
+                cp_async_wait_all();
             __syncthreads();
             if (prof) prof[2] = clock64();
 
@@ -422,35 +504,40 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                 const uint32_t r = (static_cast<uint32_t>(cta) * 2654435761u) ^ (static_cast<uint32_t>(s * 40503 + k));
                 __nanosleep((r >> 7) & 2047u);
             }
-            for (int j = 0; j < item_rounds; ++j) {
-                const int e = tid + j * nt;
-                const bool ok = e < n_items;
-                float h = 0.0f;
-                if (ok) {
-                    const int unit = u0 + e / BT, bg = k * BT + e % BT;
-                    if (G == 1) {
-                        h = activation(p.act, zs[e] + bps[e]);
-                    } else {
-                        const int ub = U * BT;
-                        const float zi = zs[0 * ub + e] + bps[e * G + 0];
-                        const float zf = zs[1 * ub + e] + bps[e * G + 1 % G];
-                        const float zg = zs[2 * ub + e] + bps[e * G + 2 % G];
-                        const float zo = zs[3 * ub + e] + bps[e * G + 3 % G];
-                        float* cp = &cs[k * umax_bt + e];
-                        const float c = sigmoidf_acc(zf) * (*cp) + sigmoidf_acc(zi) * tanhf(zg);
-                        *cp = c;
-                        h = sigmoidf_acc(zo) * tanhf(c);
-                        if (s == p.T && p.cT != nullptr && bg < p.B) p.cT[static_cast<size_t>(bg) * H + unit] = c;
+            {
+                const float* bb = bps + buf * G * umax_bt;
+                for (int j = 0; j < item_rounds; ++j) {
+                    const int e = tid + j * nt;
+                    const bool ok = e < n_items;
+                    float h = 0.0f;
+                    if (ok) {
+                        const int unit = u0 + e / BT, bg = k * BT + e % BT;
+                        if (G == 1) {
+                            h = activation(p.act, zs[e] + bb[e]);
+                        } else {
+                            const int ub = U * BT;
+                            const float zi = zs[0 * ub + e] + bb[e * G + 0];
+                            const float zf = zs[1 * ub + e] + bb[e * G + 1 % G];
+                            const float zg = zs[2 * ub + e] + bb[e * G + 2 % G];
+                            const float zo = zs[3 * ub + e] + bb[e * G + 3 % G];
+                            float* cp = &cs[k * umax_bt + e];
+                            const float c = sigmoidf_acc(zf) * (*cp) + sigmoidf_acc(zi) * tanhf(zg);
+                            *cp = c;
+                            h = sigmoidf_acc(zo) * tanhf(c);
+                            if (s == p.T && p.cT != nullptr && bg < p.B) p.cT[static_cast<size_t>(bg) * H + unit] = c;
+                        }
+                        if (bg < p.B) {
+                            if (p.y != nullptr) p.y[(static_cast<size_t>(s - 1) * p.B + bg) * H + unit] = h;
+                            if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + unit] = h;
+                        }
                     }
-                    if (bg < p.B) {
-                        if (p.y != nullptr) p.y[(static_cast<size_t>(s - 1) * p.B + bg) * H + unit] = h;
-                        if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + unit] = h;
-                    }
+                    publish(s, k, e, ok, h);
                 }
-                publish(s, k, e, ok, h);
             }
             if (prof) prof[3] = clock64();
             if (grid_sync) cg::this_grid().sync();
+            buf ^= 1;
+            if (!issued_early && ns <= p.T) issue_tile(ns, nk, buf);
         }
     }
 done:
