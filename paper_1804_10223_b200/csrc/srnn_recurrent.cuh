@@ -40,6 +40,10 @@ namespace cg = cooperative_groups;
 constexpr uint32_t kFlagGridSync = 1u << 0;
 constexpr uint32_t kFlagJitter = 1u << 4;
 constexpr uint32_t kFlagProfile = 1u << 6;
+#ifndef SRNN_POLL_BACKOFF_NS
+#define SRNN_POLL_BACKOFF_NS 64
+#endif
+constexpr uint32_t kPollBackoffNs = SRNN_POLL_BACKOFF_NS;
 
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -175,6 +179,7 @@ __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, un
                 ok = false;
                 break;
             }
+            __nanosleep(kPollBackoffNs);
 #pragma unroll
             for (int j = 0; j < K; ++j)
                 if (pend & (1u << j)) v[j] = ld_relaxed_v2(src + base + j * nt);
@@ -230,6 +235,7 @@ struct Prefetch {
                 ok = false;
                 break;
             }
+            __nanosleep(kPollBackoffNs);  // stale: back off instead of flooding the LSU
 #pragma unroll
             for (int j = 0; j < KP; ++j)
                 if (pend & (1u << j)) v[j] = ld_relaxed_v2(src + threadIdx.x + j * nt);
@@ -469,7 +475,6 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
             }
             const int ns = k + 1 < p.n_tiles ? s : s + 1, nk = k + 1 < p.n_tiles ? k + 1 : 0;
             const bool issued_early = early && ns <= p.T;
-            if (issued_early) issue_tile(ns, nk, buf ^ 1);
             __syncthreads();
             if (prof) prof[1] = clock64();
             if (*s_abort) goto done;
@@ -492,6 +497,11 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                     for (int b = 0; b < BT; ++b) zs[krow * BT + b] = acc[b];
                 }
             }
+            // The next tile's input was published by the other CTAs at the end
+            // of the previous tile-phase: issuing its loads only now (after this
+            // tile's operate) lets them land during the epilogue instead of
+            // returning stale words.
+            if (issued_early) issue_tile(ns, nk, buf ^ 1);
             if (issued_early)
                 asm volatile("cp.async.wait_group 1;" ::: "memory");
             else
