@@ -76,8 +76,8 @@ int inst_for(int slots, bool f16) {
 int elem_bytes(bool f16, int bt) { return f16 ? 2 * bt : 4 * bt; }
 
 size_t smem_for(const srnn_plan* p, int units_max, int bt, int n_tiles) {
-    size_t s = (static_cast<size_t>(p->cfg.hidden) * elem_bytes(p->f16, bt) + 15) & ~static_cast<size_t>(15);
-    s += 3 * static_cast<size_t>(p->G) * units_max * bt * 4;  // zs + double-buffered b' staging
+    // hs double buffer + LSTM cell state + abort flag (srnn_recurrent.cuh)
+    size_t s = 2 * ((static_cast<size_t>(p->cfg.hidden) * elem_bytes(p->f16, bt) + 15) & ~static_cast<size_t>(15));
     if (p->G == 4) s += static_cast<size_t>(n_tiles) * units_max * bt * 4;
     return s + 16;
 }
@@ -121,9 +121,7 @@ double cost_model(const Layout& lay, int bt, int H, int n_tiles, bool f16) {
     const double k = f16 ? 8.0 : 4.0;
     const double groups = std::ceil(chunks / (lay.threads * k));
     const double load = groups * 900.0 + chunks * 16.0 / 48.0;
-    int umax = 0;
-    for (int c = 0; c < lay.num_ctas; ++c) umax = std::max(umax, lay.cta_unit0[c + 1] - lay.cta_unit0[c]);
-    const double epi = std::ceil(static_cast<double>(umax) * bt / lay.threads) * 300.0;
+    const double epi = 150.0;  // row-leader lanes, in parallel
     const double sync = lay.num_ctas > 1 ? 1200.0 : 600.0;
     return n_tiles * (std::max(std::max(wf, issue), chain) + load + reduce + epi + sync);
 }
@@ -327,6 +325,7 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
         const size_t smem = smem_for(p, umax, p->BT, p->n_tiles_max);
         if (smem > static_cast<size_t>(p->smem_optin)) continue;
         for (int L : cands_l) {
+            if (G == 4 && L > 8) continue;  // the 4 gate rows of a unit must share a warp
             const int rows_max = G * umax;
             const int threads = ((rows_max * L + 31) / 32) * 32;
             if (threads > 1024) continue;

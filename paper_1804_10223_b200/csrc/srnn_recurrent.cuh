@@ -364,19 +364,15 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     using F = Fmt<F16, BT>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int H = p.H;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int cta = blockIdx.x;
     const int u0 = p.cta_unit0[cta];
     const int U = p.cta_unit0[cta + 1] - u0;
-    const int n_items = U * BT;                       // epilogue items (unit, sample) of one tile
-    const int item_rounds = (n_items + nt - 1) / nt;  // uniform within the CTA
-    const int umax_bt = p.units_max * BT;
-    // shared memory: hs [H][BT] at offset 0 (E bytes per unit), then fp32 areas
-    unsigned char* hs = smem;
-    float* zs = reinterpret_cast<float*>(smem + ((static_cast<size_t>(H) * F::E + 15) & ~static_cast<size_t>(15)));
-    float* bps = zs + G * umax_bt;                           // b'_s, double-buffered: [2][item][G]
-    float* cs = bps + 2 * G * umax_bt;                       // LSTM c: [n_tiles][item]
-    int* s_abort = reinterpret_cast<int*>(cs + (G == 4 ? p.n_tiles * umax_bt : 0));
+    // shared memory: hs[2] (double-buffered h_{s-1} tile, E bytes per unit),
+    // then the LSTM cell state of every (tile, unit, sample)
+    const size_t hs_bytes = (static_cast<size_t>(H) * F::E + 15) & ~static_cast<size_t>(15);
+    float* cs = reinterpret_cast<float*>(smem + 2 * hs_bytes);
+    int* s_abort = reinterpret_cast<int*>(cs + (G == 4 ? p.n_tiles * p.units_max * BT : 0));
 
     const int L = p.lanes_per_row;
     const int n_w = p.warp_slots[cta * (p.threads >> 5) + warp];
@@ -388,76 +384,63 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     Weights<NP, BT, F16> W;
     W.load(p, static_cast<size_t>(cta) * NP * p.threads + tid, n_w);
 
-    const int krow = warp * (32 / L) + lane / L;  // local row of this lane
-    const bool row_leader = (lane % L) == 0 && krow < G * U;
+    // Row of this lane: local row k = unit_local * G + gate (srnn_packer.cpp).
+    const int krow = warp * (32 / L) + lane / L;
+    const bool row_valid = krow < G * U;
+    const bool row_leader = (lane % L) == 0 && row_valid;
+    const int ul = krow / G, gate = krow % G;      // local unit, gate of this row
+    const int unit = u0 + ul;
+    const bool unit_leader = row_leader && gate == 0;  // owns h (and c) of its unit
     if (tid == 0) *s_abort = 0;
 
-    // Publish item e's h of (step s, tile k) as tagged words.  Called by all
-    // threads of the CTA (the fp16 pairing uses a shuffle); `ok` masks items.
-    auto publish = [&](int s, int k, int e, bool ok, float h) {
+    // Publish the BT values of unit `unit`, (step s, tile k) as tagged words.
+    auto publish = [&](int s, int k, const float (&h)[BT]) {
         unsigned long long* dst = p.xbuf + static_cast<size_t>((s & 1) * p.n_tiles + k) * tile_stride;
-        const uint32_t tag = p.epoch + static_cast<uint32_t>(s);
-        const int unit = u0 + e / BT, eb = e % BT;
+        const uint64_t tag = static_cast<uint64_t>(p.epoch + static_cast<uint32_t>(s)) << 32;
         if (!F16) {
-            if (ok) st_relaxed_u64(dst + unit * BT + eb, pack_tagged(h, tag));
+#pragma unroll
+            for (int b = 0; b < BT; ++b) st_relaxed_u64(dst + unit * BT + b, tag | __float_as_uint(h[b]));
         } else {
-            const uint32_t hb = __half_as_ushort(__float2half_rn(h));
-            const uint32_t nb = __shfl_down_sync(0xffffffffu, hb, 1);
-            if (ok && (BT == 1 || (eb & 1) == 0)) {
-                const uint32_t lo = BT == 1 ? hb : (hb | (nb << 16));
-                st_relaxed_u64(dst + unit * F::WPR + (eb >> 1), (static_cast<unsigned long long>(tag) << 32) | lo);
+#pragma unroll
+            for (int w = 0; w < F::WPR; ++w) {
+                uint32_t lo = __half_as_ushort(__float2half_rn(h[2 * w]));
+                if (2 * w + 1 < BT) lo |= static_cast<uint32_t>(__half_as_ushort(__float2half_rn(h[(2 * w + 1) % BT]))) << 16;
+                st_relaxed_u64(dst + unit * F::WPR + w, tag | lo);
             }
         }
     };
 
     // ---- publish h_0 (tag = epoch) and initialise c ----
-    for (int k = 0; k < p.n_tiles; ++k) {
-        for (int j = 0; j < item_rounds; ++j) {
-            const int e = tid + j * nt;
-            const bool ok = e < n_items;
-            const int unit = u0 + e / BT, bg = k * BT + e % BT;
-            float h = 0.0f;
-            if (ok) {
-                h = (p.h0 != nullptr && bg < p.B) ? p.h0[static_cast<size_t>(bg) * H + unit] : 0.0f;
+    if (unit_leader) {
+        for (int k = 0; k < p.n_tiles; ++k) {
+            float h[BT];
+#pragma unroll
+            for (int b = 0; b < BT; ++b) {
+                const int bg = k * BT + b;
+                h[b] = (p.h0 != nullptr && bg < p.B) ? p.h0[static_cast<size_t>(bg) * H + unit] : 0.0f;
                 if (G == 4)
-                    cs[k * umax_bt + e] = (p.c0 != nullptr && bg < p.B) ? p.c0[static_cast<size_t>(bg) * H + unit] : 0.0f;
+                    cs[(k * p.units_max + ul) * BT + b] =
+                        (p.c0 != nullptr && bg < p.B) ? p.c0[static_cast<size_t>(bg) * H + unit] : 0.0f;
             }
-            publish(0, k, e, ok, h);
+            publish(0, k, h);
         }
     }
     const bool grid_sync = (p.flags & kFlagGridSync) != 0u;
     if (grid_sync) cg::this_grid().sync();
-    __syncthreads();
 
-    // Prefetch of tile (s, k): its h_{s-1} tagged words into registers and its
-    // b'_s rows into bps[buf] (cp.async).  With >= 2 batch tiles the next
-    // tile's input was published one tile-phase ago, so it is issued before the
-    // current tile computes and lands while it does ("as we
-    // process iteration n, we can load the states for iteration n+1").
+    // Register prefetch of tile (s, k)'s h_{s-1} tagged words.  With >= 2
+    // batch tiles the next tile's input was published one tile-phase ago and
+    // its loads are issued right after this tile's operate, landing while the
+    // epilogue runs ("as we process iteration n, we can load the
+    // states for iteration n+1").
     Prefetch<F16, BT, 4> pf;
     const bool early = p.n_tiles > 1 && !grid_sync;
-    auto issue_tile = [&](int s, int k, int buf) {
-        pf.issue(reinterpret_cast<const ulonglong2*>(p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) *
-                                                                 tile_stride),
-                 n_words);
-        float* bb = bps + buf * G * umax_bt;
-        for (int j = 0; j < item_rounds; ++j) {
-            const int e = tid + j * nt;
-            if (e < n_items) {
-                const int unit = u0 + e / BT, bg = k * BT + e % BT;
-#pragma unroll
-                for (int q = 0; q < G; ++q) {
-                    if (bg < p.B)
-                        cp_async_f32(&bb[e * G + q], p.bprime + (static_cast<size_t>(s - 1) * p.B + bg) * GH + q * H + unit);
-                    else
-                        bb[e * G + q] = 0.0f;
-                }
-            }
-        }
-        cp_async_commit();
+    auto tile_src = [&](int s, int k) {
+        return reinterpret_cast<const ulonglong2*>(p.xbuf +
+                                                   static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
     };
-    int buf = 0;
-    issue_tile(1, 0, 0);
+    pf.issue(tile_src(1, 0), n_words);
+    int parity = 0;
 
     for (int s = 1; s <= p.T; ++s) {
         for (int k = 0; k < p.n_tiles; ++k) {
@@ -465,89 +448,91 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                                   ? p.profile + ((static_cast<size_t>(cta) * p.T + (s - 1)) * p.n_tiles + k) * 4
                                   : nullptr;
             if (prof) prof[0] = clock64();
-            // ---- load: h_{s-1} tile k -> hs ----
-            {
-                const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
-                    p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
-                if (!pf.finish(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1), !grid_sync, p.status,
-                               p.timeout_ns))
-                    *s_abort = 1;
+            // b'_s of this lane's row for the BT samples (lands during operate)
+            float bp[BT];
+#pragma unroll
+            for (int b = 0; b < BT; ++b) {
+                const int bg = k * BT + b;
+                bp[b] = (row_leader && bg < p.B)
+                            ? __ldg(p.bprime + (static_cast<size_t>(s - 1) * p.B + bg) * GH + gate * H + unit)
+                            : 0.0f;
             }
-            const int ns = k + 1 < p.n_tiles ? s : s + 1, nk = k + 1 < p.n_tiles ? k + 1 : 0;
-            const bool issued_early = early && ns <= p.T;
+            // ---- load: h_{s-1} tile k -> hs[parity] ----
+            unsigned char* hs = smem + parity * hs_bytes;
+            if (!pf.finish(tile_src(s, k), hs, n_words, p.epoch + static_cast<uint32_t>(s - 1), !grid_sync, p.status,
+                           p.timeout_ns))
+                *s_abort = 1;
             __syncthreads();
             if (prof) prof[1] = clock64();
             if (*s_abort) goto done;
+            const int ns = k + 1 < p.n_tiles ? s : s + 1, nk = k + 1 < p.n_tiles ? k + 1 : 0;
 
             // ---- operate + reduce ----
-            {
-                float acc[BT];
+            float acc[BT];
 #pragma unroll
-                for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
-                W.operate(acc, hs, n_w);
+            for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
+            W.operate(acc, hs, n_w);
+            if (early && ns <= p.T) pf.issue(tile_src(ns, nk), n_words);
 #pragma unroll
-                for (int m = 16; m >= 1; m >>= 1) {
-                    if (m < L) {
+            for (int m = 16; m >= 1; m >>= 1) {
+                if (m < L) {
 #pragma unroll
-                        for (int b = 0; b < BT; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], m);
-                    }
-                }
-                if (row_leader) {
-#pragma unroll
-                    for (int b = 0; b < BT; ++b) zs[krow * BT + b] = acc[b];
+                    for (int b = 0; b < BT; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], m);
                 }
             }
-            // The next tile's input was published by the other CTAs at the end
-            // of the previous tile-phase: issuing its loads only now (after this
-            // tile's operate) lets them land during the epilogue instead of
-            // returning stale words.
-            if (issued_early) issue_tile(ns, nk, buf ^ 1);
-            if (issued_early)
-                asm volatile("cp.async.wait_group 1;" ::: "memory");
-            else
-                cp_async_wait_all();
-            __syncthreads();
             if (prof) prof[2] = clock64();
 
-            // ---- epilogue: activation / gates, y, tagged publish of h_s ----
-            if ((p.flags & kFlagJitter) && tid == 0) {
-                const uint32_t r = (static_cast<uint32_t>(cta) * 2654435761u) ^ (static_cast<uint32_t>(s * 40503 + k));
-                __nanosleep((r >> 7) & 2047u);
-            }
-            {
-                const float* bb = bps + buf * G * umax_bt;
-                for (int j = 0; j < item_rounds; ++j) {
-                    const int e = tid + j * nt;
-                    const bool ok = e < n_items;
-                    float h = 0.0f;
-                    if (ok) {
-                        const int unit = u0 + e / BT, bg = k * BT + e % BT;
-                        if (G == 1) {
-                            h = activation(p.act, zs[e] + bb[e]);
-                        } else {
-                            const int ub = U * BT;
-                            const float zi = zs[0 * ub + e] + bb[e * G + 0];
-                            const float zf = zs[1 * ub + e] + bb[e * G + 1 % G];
-                            const float zg = zs[2 * ub + e] + bb[e * G + 2 % G];
-                            const float zo = zs[3 * ub + e] + bb[e * G + 3 % G];
-                            float* cp = &cs[k * umax_bt + e];
-                            const float c = sigmoidf_acc(zf) * (*cp) + sigmoidf_acc(zi) * tanhf(zg);
-                            *cp = c;
-                            h = sigmoidf_acc(zo) * tanhf(c);
-                            if (s == p.T && p.cT != nullptr && bg < p.B) p.cT[static_cast<size_t>(bg) * H + unit] = c;
-                        }
+            // ---- epilogue in the row-leader lanes: z = acc + b'; g / gates; publish ----
+            float z[BT];
+#pragma unroll
+            for (int b = 0; b < BT; ++b) z[b] = acc[b] + bp[b];
+            if (G == 4) {
+                // gates i, f, g, o of a unit are rows 4u..4u+3: lanes +0, +L, +2L, +3L
+                float zf[BT], zg[BT], zo[BT];
+#pragma unroll
+                for (int b = 0; b < BT; ++b) {
+                    zf[b] = __shfl_down_sync(0xffffffffu, z[b], L);
+                    zg[b] = __shfl_down_sync(0xffffffffu, z[b], 2 * L);
+                    zo[b] = __shfl_down_sync(0xffffffffu, z[b], 3 * L);
+                }
+                if (unit_leader) {
+                    float h[BT];
+#pragma unroll
+                    for (int b = 0; b < BT; ++b) {
+                        float* cp = &cs[(k * p.units_max + ul) * BT + b];
+                        const float c = sigmoidf_acc(zf[b]) * (*cp) + sigmoidf_acc(z[b]) * tanhf(zg[b]);
+                        *cp = c;
+                        h[b] = sigmoidf_acc(zo[b]) * tanhf(c);
+                        const int bg = k * BT + b;
                         if (bg < p.B) {
-                            if (p.y != nullptr) p.y[(static_cast<size_t>(s - 1) * p.B + bg) * H + unit] = h;
-                            if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + unit] = h;
+                            if (p.y != nullptr) p.y[(static_cast<size_t>(s - 1) * p.B + bg) * H + unit] = h[b];
+                            if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + unit] = h[b];
+                            if (s == p.T && p.cT != nullptr) p.cT[static_cast<size_t>(bg) * H + unit] = c;
                         }
                     }
-                    publish(s, k, e, ok, h);
+                    publish(s, k, h);
                 }
+            } else if (unit_leader) {
+                float h[BT];
+#pragma unroll
+                for (int b = 0; b < BT; ++b) {
+                    h[b] = activation(p.act, z[b]);
+                    const int bg = k * BT + b;
+                    if (bg < p.B) {
+                        if (p.y != nullptr) p.y[(static_cast<size_t>(s - 1) * p.B + bg) * H + unit] = h[b];
+                        if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + unit] = h[b];
+                    }
+                }
+                if ((p.flags & kFlagJitter) != 0u) {
+                    const uint32_t r = (static_cast<uint32_t>(cta) * 2654435761u) ^ (static_cast<uint32_t>(s * 40503 + k));
+                    __nanosleep((r >> 7) & 2047u);
+                }
+                publish(s, k, h);
             }
             if (prof) prof[3] = clock64();
             if (grid_sync) cg::this_grid().sync();
-            buf ^= 1;
-            if (!issued_early && ns <= p.T) issue_tile(ns, nk, buf);
+            if (!early && ns <= p.T) pf.issue(tile_src(ns, nk), n_words);
+            parity ^= 1;
         }
     }
 done:
