@@ -98,6 +98,7 @@ typedef struct {
     uint32_t flags;     /* SRNN_FLAG_* bits                                              */
     int32_t num_ctas;   /* 0 = planner's choice; else force this CTA count (<= SMs)     */
     int32_t lanes_per_row; /* 0 = planner's choice; else 1,2,4,8,16 or 32              */
+    int32_t batch_tile; /* 0 = planner's choice; else 1, 2 or 4 samples staged per h tile */
 } srnn_config_t;
 
 /* What the planner decided (srnn_plan_query). Fields marked (L) are final

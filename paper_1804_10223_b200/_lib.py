@@ -44,7 +44,8 @@ class Config(ctypes.Structure):
     _fields_ = [("hidden", ctypes.c_int32), ("input", ctypes.c_int32), ("batch", ctypes.c_int32),
                 ("max_steps", ctypes.c_int32), ("density", ctypes.c_float), ("cell", ctypes.c_int32),
                 ("act", ctypes.c_int32), ("prec", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("flags", ctypes.c_uint32), ("num_ctas", ctypes.c_int32), ("lanes_per_row", ctypes.c_int32)]
+                ("flags", ctypes.c_uint32), ("num_ctas", ctypes.c_int32), ("lanes_per_row", ctypes.c_int32),
+                ("batch_tile", ctypes.c_int32)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -119,10 +120,10 @@ class SparseRNN:
     """
 
     def __init__(self, hidden, input, batch, max_steps, density, cell="rnn", act="relu", prec="fp16",
-                 device=0, flags=0, num_ctas=0, lanes_per_row=0):
+                 device=0, flags=0, num_ctas=0, lanes_per_row=0, batch_tile=0):
         self.lib = load_library()
         self.cfg = Config(hidden, input, batch, max_steps, float(density), CELL[cell], ACT[act], PREC[prec],
-                          device, flags, num_ctas, lanes_per_row)
+                          device, flags, num_ctas, lanes_per_row, batch_tile)
         self.H, self.I, self.B_max, self.T_max = hidden, input, batch, max_steps
         self.G = 4 if cell == "lstm" else 1
         self.cell, self.prec = cell, prec
@@ -272,10 +273,11 @@ class SparseRNN:
         _check("srnn_plan_status", code)
 
 
-def from_problem(prob, prec="fp16", device=0, flags=0, num_ctas=0, lanes_per_row=0, batch=None, max_steps=None):
+def from_problem(prob, prec="fp16", device=0, flags=0, num_ctas=0, lanes_per_row=0, batch=None, max_steps=None,
+                 batch_tile=0):
     """Plan + load for a problem dict of ``paper_1804_10223_b200.inputs``."""
     m = SparseRNN(prob["H"], prob["I"], batch or prob["B"], prob["T"] if max_steps is None else max_steps,
                   prob["density"], prob["cell"], prob.get("act", "relu"), prec, device, flags, num_ctas,
-                  lanes_per_row)
+                  lanes_per_row, batch_tile)
     m.load_weights(prob["rowptr"], prob["col"], prob["val"], prob["wx"], prob["bias"])
     return m

@@ -159,6 +159,7 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
         (c.lanes_per_row < 1 || c.lanes_per_row > 32 || (c.lanes_per_row & (c.lanes_per_row - 1)) != 0))
         return SRNN_ERR_INVALID_VALUE;
     if (c.num_ctas < 0) return SRNN_ERR_INVALID_VALUE;
+    if (c.batch_tile != 0 && c.batch_tile != 1 && c.batch_tile != 2 && c.batch_tile != 4) return SRNN_ERR_INVALID_VALUE;
 
     srnn_plan* p = new (std::nothrow) srnn_plan();
     if (!p) return SRNN_ERR_INVALID_VALUE;
@@ -193,10 +194,12 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     // We keep >= 2 tiles whenever B >= 2 so the exchange of one tile overlaps
     // the compute of the next (tiles are independent sequences).
     int bt = c.batch >= 8 ? 4 : (c.batch >= 4 ? 2 : 1);
+    if (c.batch_tile == 1 || c.batch_tile == 2 || c.batch_tile == 4) bt = c.batch_tile;
     if (const char* e = std::getenv("SRNN_BT")) {  // experiment override: batch tile width
         const int v = std::atoi(e);
-        if (v == 1 || v == 2 || v == 4) bt = std::min(bt, v);
+        if (v == 1 || v == 2 || v == 4) bt = v;
     }
+    while (bt > 1 && bt > c.batch) bt /= 2;
     // fp16 register pairs carry the hs byte offset in 16 bits: H * E <= 65536
     while (p->f16 && bt > 1 && static_cast<int64_t>(c.hidden) * elem_bytes(true, bt) > 65536) bt /= 2;
     if (p->f16 && static_cast<int64_t>(c.hidden) * elem_bytes(true, bt) > 65536) {

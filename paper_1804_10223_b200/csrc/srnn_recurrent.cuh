@@ -393,9 +393,16 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     const bool unit_leader = row_leader && gate == 0;  // owns h (and c) of its unit
     if (tid == 0) *s_abort = 0;
 
+    // Per-lane bases hoisted out of the time loop.
+    unsigned long long* const xb_unit = p.xbuf + unit * F::WPR;
+    const float* const bp_row = p.bprime + gate * H + unit;
+    float* const y_unit = p.y != nullptr ? p.y + unit : nullptr;
+    const size_t bp_step = static_cast<size_t>(p.B) * GH, y_step = static_cast<size_t>(p.B) * H;
+    const int act = p.act;
+
     // Publish the BT values of unit `unit`, (step s, tile k) as tagged words.
     auto publish = [&](int s, int k, const float (&h)[BT]) {
-        unsigned long long* dst = p.xbuf + static_cast<size_t>((s & 1) * p.n_tiles + k) * tile_stride;
+        unsigned long long* dst = xb_unit + static_cast<size_t>((s & 1) * p.n_tiles + k) * tile_stride - unit * F::WPR;
         const uint64_t tag = static_cast<uint64_t>(p.epoch + static_cast<uint32_t>(s)) << 32;
         if (!F16) {
 #pragma unroll
@@ -450,13 +457,12 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
             if (prof) prof[0] = clock64();
             // b'_s of this lane's row for the BT samples (lands during operate)
             float bp[BT];
+            const float* bps = bp_row + static_cast<size_t>(s - 1) * bp_step + static_cast<size_t>(k * BT) * GH;
+            float* ys = y_unit != nullptr ? y_unit + static_cast<size_t>(s - 1) * y_step + static_cast<size_t>(k * BT) * H
+                                          : nullptr;
+            const int nb = min(BT, p.B - k * BT);  // real samples in this tile
 #pragma unroll
-            for (int b = 0; b < BT; ++b) {
-                const int bg = k * BT + b;
-                bp[b] = (row_leader && bg < p.B)
-                            ? __ldg(p.bprime + (static_cast<size_t>(s - 1) * p.B + bg) * GH + gate * H + unit)
-                            : 0.0f;
-            }
+            for (int b = 0; b < BT; ++b) bp[b] = (row_leader && b < nb) ? __ldg(bps + b * GH) : 0.0f;
             // ---- load: h_{s-1} tile k -> hs[parity] ----
             unsigned char* hs = smem + parity * hs_bytes;
             if (!pf.finish(tile_src(s, k), hs, n_words, p.epoch + static_cast<uint32_t>(s - 1), !grid_sync, p.status,
@@ -503,11 +509,13 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                         const float c = sigmoidf_acc(zf[b]) * (*cp) + sigmoidf_acc(z[b]) * tanhf(zg[b]);
                         *cp = c;
                         h[b] = sigmoidf_acc(zo[b]) * tanhf(c);
-                        const int bg = k * BT + b;
-                        if (bg < p.B) {
-                            if (p.y != nullptr) p.y[(static_cast<size_t>(s - 1) * p.B + bg) * H + unit] = h[b];
-                            if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + unit] = h[b];
-                            if (s == p.T && p.cT != nullptr) p.cT[static_cast<size_t>(bg) * H + unit] = c;
+                        if (b < nb) {
+                            if (ys != nullptr) ys[b * H] = h[b];
+                            if (s == p.T) {
+                                const int bg = k * BT + b;
+                                if (p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + unit] = h[b];
+                                if (p.cT != nullptr) p.cT[static_cast<size_t>(bg) * H + unit] = c;
+                            }
                         }
                     }
                     publish(s, k, h);
@@ -515,12 +523,12 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
             } else if (unit_leader) {
                 float h[BT];
 #pragma unroll
+                for (int b = 0; b < BT; ++b) h[b] = activation(act, z[b]);
+#pragma unroll
                 for (int b = 0; b < BT; ++b) {
-                    h[b] = activation(p.act, z[b]);
-                    const int bg = k * BT + b;
-                    if (bg < p.B) {
-                        if (p.y != nullptr) p.y[(static_cast<size_t>(s - 1) * p.B + bg) * H + unit] = h[b];
-                        if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + unit] = h[b];
+                    if (b < nb) {
+                        if (ys != nullptr) ys[b * H] = h[b];
+                        if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(k * BT + b) * H + unit] = h[b];
                     }
                 }
                 if ((p.flags & kFlagJitter) != 0u) {
