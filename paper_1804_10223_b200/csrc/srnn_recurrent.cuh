@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
         return reinterpret_cast<const ulonglong2*>(p.xbuf +
                                                    static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
     };
-    pf.issue(tile_src(1, 0), n_words);
+    if (early) pf.issue(tile_src(1, 0), n_words);
     int parity = 0;
 
     for (int s = 1; s <= p.T; ++s) {
@@ -465,9 +465,13 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
             for (int b = 0; b < BT; ++b) bp[b] = (row_leader && b < nb) ? __ldg(bps + b * GH) : 0.0f;
             // ---- load: h_{s-1} tile k -> hs[parity] ----
             unsigned char* hs = smem + parity * hs_bytes;
-            if (!pf.finish(tile_src(s, k), hs, n_words, p.epoch + static_cast<uint32_t>(s - 1), !grid_sync, p.status,
-                           p.timeout_ns))
-                *s_abort = 1;
+            {
+                const uint32_t want = p.epoch + static_cast<uint32_t>(s - 1);
+                const bool ok = early ? pf.finish(tile_src(s, k), hs, n_words, want, !grid_sync, p.status, p.timeout_ns)
+                                      : load_tile<F16, BT, LoadK<NP, F16>::value>(tile_src(s, k), hs, n_words, want,
+                                                                                   !grid_sync, p.status, p.timeout_ns);
+                if (!ok) *s_abort = 1;
+            }
             __syncthreads();
             if (prof) prof[1] = clock64();
             if (*s_abort) goto done;
@@ -539,7 +543,6 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
             }
             if (prof) prof[3] = clock64();
             if (grid_sync) cg::this_grid().sync();
-            if (!early && ns <= p.T) pf.issue(tile_src(ns, nk), n_words);
             parity ^= 1;
         }
     }
