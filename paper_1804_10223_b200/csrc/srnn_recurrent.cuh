@@ -467,9 +467,8 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
             unsigned char* hs = smem + parity * hs_bytes;
             {
                 const uint32_t want = p.epoch + static_cast<uint32_t>(s - 1);
-                const bool ok = early ? pf.finish(tile_src(s, k), hs, n_words, want, !grid_sync, p.status, p.timeout_ns)
-                                      : load_tile<F16, BT, LoadK<NP, F16>::value>(tile_src(s, k), hs, n_words, want,
-                                                                                   !grid_sync, p.status, p.timeout_ns);
+                if (!early) pf.issue(tile_src(s, k), n_words);  // single tile: input is being produced now
+                const bool ok = pf.finish(tile_src(s, k), hs, n_words, want, !grid_sync, p.status, p.timeout_ns);
                 if (!ok) *s_abort = 1;
             }
             __syncthreads();
