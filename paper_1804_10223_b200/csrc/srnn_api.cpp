@@ -75,11 +75,20 @@ int inst_for(int slots, bool f16) {
 
 int elem_bytes(bool f16, int bt) { return f16 ? 2 * bt : 4 * bt; }
 
+int words_per_unit(bool f16, int bt) { return f16 ? (bt == 4 ? 2 : 1) : bt; }
+
+// TMA staging capacity (16-byte chunks): the whole tile if it fits in 96 KB.
+int stage_chunks_for(const srnn_plan* p, int bt) {
+    const int64_t chunks = (static_cast<int64_t>(p->cfg.hidden) * words_per_unit(p->f16, bt) + 1) / 2;
+    return static_cast<int>(std::min<int64_t>(chunks, 96 * 1024 / 16));
+}
+
 size_t smem_for(const srnn_plan* p, int units_max, int bt, int n_tiles) {
-    // hs double buffer + LSTM cell state + abort flag (srnn_recurrent.cuh)
+    // hs double buffer + TMA staging + LSTM cell state + mbarrier + abort flag (srnn_recurrent.cuh)
     size_t s = 2 * ((static_cast<size_t>(p->cfg.hidden) * elem_bytes(p->f16, bt) + 15) & ~static_cast<size_t>(15));
+    s += static_cast<size_t>(stage_chunks_for(p, bt)) * 16;
     if (p->G == 4) s += static_cast<size_t>(n_tiles) * units_max * bt * 4;
-    return s + 16;
+    return ((s + 7) & ~static_cast<size_t>(7)) + 16;
 }
 
 void free_device(srnn_plan* p) {
@@ -225,7 +234,7 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     }
     if (!p->host_only) {
         DeviceGuard g(c.device);
-        const int wpr = p->f16 ? (bt == 4 ? 2 : 1) : bt;  // tagged words per unit
+        const int wpr = words_per_unit(p->f16, bt);  // tagged words per unit
         const size_t tile_stride = (static_cast<size_t>(c.hidden) * wpr + 1) & ~static_cast<size_t>(1);
         p->xbuf_words = 2 * static_cast<size_t>(p->n_tiles_max) * tile_stride;
         const size_t bp_elems = static_cast<size_t>(std::max(1, c.max_steps)) * c.batch * p->G * c.hidden;
@@ -492,6 +501,7 @@ srnn_status_t srnn_recurrence(srnn_plan_t p, int32_t T, int32_t B, const float* 
     int umax = 0;
     for (int c = 0; c < p->lay.num_ctas; ++c) umax = std::max(umax, p->lay.cta_unit0[c + 1] - p->lay.cta_unit0[c]);
     rp.units_max = umax;
+    rp.stage_chunks = stage_chunks_for(p, p->BT);
     rp.epoch = p->epoch;
     rp.flags = p->cfg.flags;
     if (p->f16)

@@ -247,6 +247,58 @@ struct Prefetch {
 };
 
 // ---------------------------------------------------------------------------
+// TMA staging of the tagged h words (sm_90+/sm_100 bulk async copy).
+// One elected thread moves a whole tile (or a segment of it) of tagged words
+// global -> shared memory with cp.async.bulk, completion on an mbarrier; all
+// threads then validate tags in shared memory and compact the values into hs.
+// No registers are held while the copy is in flight, so the next tile's copy
+// can be issued before the current tile computes.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of dst before async writes
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Validate one staged segment (chunks [c0, c1)) and compact it into hs.
+// Returns true if any chunk of this thread is stale.
+template <bool F16, int BT>
+__device__ __forceinline__ bool stage_pass(const ulonglong2* staging, unsigned char* hs, int c0, int c1, int n_words,
+                                           uint32_t want) {
+    bool stale = false;
+    for (int c = c0 + static_cast<int>(threadIdx.x); c < c1; c += blockDim.x) {
+        const ulonglong2 v = staging[c - c0];
+        const bool has1 = 2 * c + 1 < n_words;
+        stale |= !(tag_of(v.x) == want && (!has1 || tag_of(v.y) == want));
+        Fmt<F16, BT>::store(hs, c, v.x, v.y, has1);
+    }
+    return stale;
+}
+
+// ---------------------------------------------------------------------------
 // Register-resident weights and the operate stage.
 //   F32: two registers per pair, {hs byte offset, fp32 value}, FFMA.
 //   F16: one register per pair, (hs byte offset << 16) | fp16 value, and the
@@ -371,8 +423,10 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     // shared memory: hs[2] (double-buffered h_{s-1} tile, E bytes per unit),
     // then the LSTM cell state of every (tile, unit, sample)
     const size_t hs_bytes = (static_cast<size_t>(H) * F::E + 15) & ~static_cast<size_t>(15);
-    float* cs = reinterpret_cast<float*>(smem + 2 * hs_bytes);
-    int* s_abort = reinterpret_cast<int*>(cs + (G == 4 ? p.n_tiles * p.units_max * BT : 0));
+    ulonglong2* staging = reinterpret_cast<ulonglong2*>(smem + 2 * hs_bytes);  // [stage_chunks] tagged words
+    float* cs = reinterpret_cast<float*>(smem + 2 * hs_bytes + static_cast<size_t>(p.stage_chunks) * 16);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(cs + (G == 4 ? p.n_tiles * p.units_max * BT : 0));
+    int* s_abort = reinterpret_cast<int*>(mbar + 1);
 
     const int L = p.lanes_per_row;
     const int n_w = p.warp_slots[cta * (p.threads >> 5) + warp];
@@ -391,7 +445,11 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     const int ul = krow / G, gate = krow % G;      // local unit, gate of this row
     const int unit = u0 + ul;
     const bool unit_leader = row_leader && gate == 0;  // owns h (and c) of its unit
-    if (tid == 0) *s_abort = 0;
+    if (tid == 0) {
+        *s_abort = 0;
+        mbar_init(mbar, 1);
+    }
+    __syncthreads();
 
     // Per-lane bases hoisted out of the time loop.
     unsigned long long* const xb_unit = p.xbuf + unit * F::WPR;
@@ -440,13 +498,19 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     // its loads are issued right after this tile's operate, landing while the
     // epilogue runs ("as we process iteration n, we can load the
     // states for iteration n+1").
-    Prefetch<F16, BT, 4> pf;
     const bool early = p.n_tiles > 1 && !grid_sync;
+    const int n_chunks = (n_words + 1) >> 1;
+    const int stage_chunks = p.stage_chunks;
     auto tile_src = [&](int s, int k) {
         return reinterpret_cast<const ulonglong2*>(p.xbuf +
                                                    static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
     };
-    if (early) pf.issue(tile_src(1, 0), n_words);
+    uint32_t mbar_phase = 0;
+    auto issue_seg = [&](const ulonglong2* src, int c0) {  // thread 0 only
+        const int c1 = min(n_chunks, c0 + stage_chunks);
+        tma_load_1d(staging, src + c0, static_cast<uint32_t>(c1 - c0) * 16u, mbar);
+    };
+    if (early && tid == 0) issue_seg(tile_src(1, 0), 0);
     int parity = 0;
 
     for (int s = 1; s <= p.T; ++s) {
@@ -464,16 +528,37 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
 #pragma unroll
             for (int b = 0; b < BT; ++b) bp[b] = (row_leader && b < nb) ? __ldg(bps + b * GH) : 0.0f;
             // ---- load: h_{s-1} tile k -> hs[parity] ----
+            // TMA-stage the tagged words (segment by segment), validate the
+            // tags in shared memory, compact the values into hs; a stale
+            // segment is re-fetched whole after a short backoff.
             unsigned char* hs = smem + parity * hs_bytes;
             {
                 const uint32_t want = p.epoch + static_cast<uint32_t>(s - 1);
-                if (!early) pf.issue(tile_src(s, k), n_words);  // single tile: input is being produced now
-                const bool ok = pf.finish(tile_src(s, k), hs, n_words, want, !grid_sync, p.status, p.timeout_ns);
-                if (!ok) *s_abort = 1;
+                const ulonglong2* src = tile_src(s, k);
+                Watchdog wd{0ull, 0u};
+                for (int c0 = 0; c0 < n_chunks; c0 += stage_chunks) {
+                    bool prefetched = early && c0 == 0;
+                    while (true) {
+                        if (!prefetched && tid == 0) issue_seg(src, c0);
+                        prefetched = false;
+                        mbar_wait(mbar, mbar_phase);
+                        mbar_phase ^= 1u;
+                        const bool stale =
+                            stage_pass<F16, BT>(staging, hs, c0, min(n_chunks, c0 + stage_chunks), n_words, want);
+                        if (!__syncthreads_or(stale)) break;
+                        if (tid == 0) {
+                            if (grid_sync)
+                                atomicCAS(p.status, 0, -4 /* protocol violation */);
+                            else if (watchdog_tick(wd, p.status, p.timeout_ns))
+                                *s_abort = 1;
+                        }
+                        __syncthreads();
+                        if (*s_abort || grid_sync) break;
+                        __nanosleep(kPollBackoffNs);
+                    }
+                    if (*s_abort) break;
+                }
             }
-            __syncthreads();
-            if (prof) prof[1] = clock64();
-            if (*s_abort) goto done;
             const int ns = k + 1 < p.n_tiles ? s : s + 1, nk = k + 1 < p.n_tiles ? k + 1 : 0;
 
             // ---- operate + reduce ----
@@ -481,7 +566,8 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
 #pragma unroll
             for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
             W.operate(acc, hs, n_w);
-            if (early && ns <= p.T) pf.issue(tile_src(ns, nk), n_words);
+            // next tile's input was published one tile-phase ago: stage it now
+            if (early && ns <= p.T && tid == 0) issue_seg(tile_src(ns, nk), 0);
 #pragma unroll
             for (int m = 16; m >= 1; m >>= 1) {
                 if (m < L) {
