@@ -425,7 +425,8 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     const size_t hs_bytes = (static_cast<size_t>(H) * F::E + 15) & ~static_cast<size_t>(15);
     ulonglong2* staging = reinterpret_cast<ulonglong2*>(smem + 2 * hs_bytes);  // [stage_chunks] tagged words
     float* cs = reinterpret_cast<float*>(smem + 2 * hs_bytes + static_cast<size_t>(p.stage_chunks) * 16);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(cs + (G == 4 ? p.n_tiles * p.units_max * BT : 0));
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(cs + (G == 4 ? p.n_tiles * p.units_max * BT : 0)) + 7) & ~static_cast<uintptr_t>(7));
     int* s_abort = reinterpret_cast<int*>(mbar + 1);
 
     const int L = p.lanes_per_row;
@@ -559,6 +560,8 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                     if (*s_abort) break;
                 }
             }
+            if (prof) prof[1] = clock64();
+            if (*s_abort) goto done;
             const int ns = k + 1 < p.n_tiles ? s : s + 1, nk = k + 1 < p.n_tiles ? k + 1 : 0;
 
             // ---- operate + reduce ----
