@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libsrnn.so")
+LIB_PATH = os.environ.get("SRNN_LIB") or os.path.join(_PKG, "libsrnn.so")  # SRNN_LIB: A/B experiments only
 
 SRNN_OK = 0
 STATUS = {0: "SRNN_OK", -1: "SRNN_ERR_INVALID_VALUE", -2: "SRNN_ERR_NOT_ON_CHIP", -3: "SRNN_ERR_BAD_WEIGHTS",
