@@ -75,20 +75,11 @@ int inst_for(int slots, bool f16) {
 
 int elem_bytes(bool f16, int bt) { return f16 ? 2 * bt : 4 * bt; }
 
-int words_per_unit(bool f16, int bt) { return f16 ? (bt == 4 ? 2 : 1) : bt; }
-
-// TMA staging capacity (16-byte chunks): the whole tile if it fits in 96 KB.
-int stage_chunks_for(const srnn_plan* p, int bt) {
-    const int64_t chunks = (static_cast<int64_t>(p->cfg.hidden) * words_per_unit(p->f16, bt) + 1) / 2;
-    return static_cast<int>(std::min<int64_t>(chunks, 96 * 1024 / 16));
-}
-
 size_t smem_for(const srnn_plan* p, int units_max, int bt, int n_tiles) {
-    // hs double buffer + TMA staging + LSTM cell state + mbarrier + abort flag (srnn_recurrent.cuh)
-    size_t s = 2 * ((static_cast<size_t>(p->cfg.hidden) * elem_bytes(p->f16, bt) + 15) & ~static_cast<size_t>(15));
-    s += static_cast<size_t>(stage_chunks_for(p, bt)) * 16;
+    size_t s = (static_cast<size_t>(p->cfg.hidden) * elem_bytes(p->f16, bt) + 15) & ~static_cast<size_t>(15);
+    s += 2 * static_cast<size_t>(p->G) * units_max * bt * 4;  // zs + b' staging
     if (p->G == 4) s += static_cast<size_t>(n_tiles) * units_max * bt * 4;
-    return ((s + 7) & ~static_cast<size_t>(7)) + 16;
+    return s + 16;
 }
 
 void free_device(srnn_plan* p) {
@@ -130,7 +121,9 @@ double cost_model(const Layout& lay, int bt, int H, int n_tiles, bool f16) {
     const double k = f16 ? 8.0 : 4.0;
     const double groups = std::ceil(chunks / (lay.threads * k));
     const double load = groups * 900.0 + chunks * 16.0 / 48.0;
-    const double epi = 150.0;  // row-leader lanes, in parallel
+    int umax = 0;
+    for (int c = 0; c < lay.num_ctas; ++c) umax = std::max(umax, lay.cta_unit0[c + 1] - lay.cta_unit0[c]);
+    const double epi = std::ceil(static_cast<double>(umax) * bt / lay.threads) * 300.0;
     const double sync = lay.num_ctas > 1 ? 1200.0 : 600.0;
     return n_tiles * (std::max(std::max(wf, issue), chain) + load + reduce + epi + sync);
 }
@@ -200,9 +193,7 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     }
     p->f16 = c.prec == SRNN_PREC_FP16W_FP32ACC && (c.flags & SRNN_FLAG_FP32_STAGING) == 0;
     // Batch tile: the paper's wide load interleaves 4 samples.
-    // We keep >= 2 tiles whenever B >= 2 so the exchange of one tile overlaps
-    // the compute of the next (tiles are independent sequences).
-    int bt = c.batch >= 8 ? 4 : (c.batch >= 4 ? 2 : 1);
+    int bt = c.batch >= 4 ? 4 : (c.batch >= 2 ? 2 : 1);
     if (c.batch_tile == 1 || c.batch_tile == 2 || c.batch_tile == 4) bt = c.batch_tile;
     if (const char* e = std::getenv("SRNN_BT")) {  // experiment override: batch tile width
         const int v = std::atoi(e);
@@ -234,7 +225,7 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     }
     if (!p->host_only) {
         DeviceGuard g(c.device);
-        const int wpr = words_per_unit(p->f16, bt);  // tagged words per unit
+        const int wpr = p->f16 ? (bt == 4 ? 2 : 1) : bt;  // tagged words per unit
         const size_t tile_stride = (static_cast<size_t>(c.hidden) * wpr + 1) & ~static_cast<size_t>(1);
         p->xbuf_words = 2 * static_cast<size_t>(p->n_tiles_max) * tile_stride;
         const size_t bp_elems = static_cast<size_t>(std::max(1, c.max_steps)) * c.batch * p->G * c.hidden;
@@ -337,7 +328,6 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
         const size_t smem = smem_for(p, umax, p->BT, p->n_tiles_max);
         if (smem > static_cast<size_t>(p->smem_optin)) continue;
         for (int L : cands_l) {
-            if (G == 4 && L > 8) continue;  // the 4 gate rows of a unit must share a warp
             const int rows_max = G * umax;
             const int threads = ((rows_max * L + 31) / 32) * 32;
             if (threads > 1024) continue;
@@ -501,7 +491,6 @@ srnn_status_t srnn_recurrence(srnn_plan_t p, int32_t T, int32_t B, const float* 
     int umax = 0;
     for (int c = 0; c < p->lay.num_ctas; ++c) umax = std::max(umax, p->lay.cta_unit0[c + 1] - p->lay.cta_unit0[c]);
     rp.units_max = umax;
-    rp.stage_chunks = stage_chunks_for(p, p->BT);
     rp.epoch = p->epoch;
     rp.flags = p->cfg.flags;
     if (p->f16)

@@ -23,7 +23,6 @@ struct RecParams {
     int32_t lanes_per_row;  // L
     int32_t np_inst;  // slots per lane in the image (= template NP)
     int32_t units_max;      // max units of any CTA (smem sizing)
-    int32_t stage_chunks;   // TMA staging capacity in 16-byte chunks (tagged words / 2)
     uint32_t epoch;   // tag of h_0 for this call; h_s carries epoch + s
     uint32_t flags;   // SRNN_FLAG_* subset relevant on device
     // packed weights: [cta][slot][thread]

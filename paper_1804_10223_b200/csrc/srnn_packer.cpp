@@ -90,11 +90,7 @@ float half_to_float(uint16_t h) {
 
 namespace {
 
-// Local row k of a CTA owning units [u0, u0+U): the G gate rows of a unit are
-// consecutive (k = unit_local * G + gate), so with lanes_per_row <= 8 all gates
-// of a unit sit in one warp and meet by shuffles ("each thread
-// must be responsible for four gates").
-inline int32_t global_row(int k, int G, int u0, int H) { return (k % G) * H + u0 + k / G; }
+inline int32_t global_row(int k, int U, int u0, int H) { return (k / U) * H + u0 + (k % U); }
 
 struct RowState {
     int32_t grow = -1;                       // global row
@@ -160,7 +156,7 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
                 rs.bucket.assign(P, {});
                 rs.head.assign(P, 0);
                 if (q >= nr) continue;
-                rs.grow = global_row(k0 + q, G, u0, H);
+                rs.grow = global_row(k0 + q, U, u0, H);
                 const int64_t b = in.rowptr[rs.grow], e = in.rowptr[rs.grow + 1];
                 rs.remaining = e - b;
                 pairs_cta += e - b;

@@ -40,10 +40,6 @@ namespace cg = cooperative_groups;
 constexpr uint32_t kFlagGridSync = 1u << 0;
 constexpr uint32_t kFlagJitter = 1u << 4;
 constexpr uint32_t kFlagProfile = 1u << 6;
-#ifndef SRNN_POLL_BACKOFF_NS
-#define SRNN_POLL_BACKOFF_NS 64
-#endif
-constexpr uint32_t kPollBackoffNs = SRNN_POLL_BACKOFF_NS;
 
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -142,12 +138,12 @@ struct Fmt {
 template <bool F16, int BT, int K>
 __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, unsigned char* hs, int n_words,
                                           uint32_t want, bool spin, int32_t* status,
-                                          unsigned long long timeout_ns, int first = 0) {
+                                          unsigned long long timeout_ns) {
     const int n_chunks = (n_words + 1) >> 1;
     const int nt = blockDim.x;
     Watchdog wd{0ull, 0u};
     bool ok = true;
-    for (int base = threadIdx.x + first; base < n_chunks; base += K * nt) {
+    for (int base = threadIdx.x; base < n_chunks; base += K * nt) {
         ulonglong2 v[K];
         uint32_t pend = 0u;
 #pragma unroll
@@ -179,7 +175,6 @@ __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, un
                 ok = false;
                 break;
             }
-            __nanosleep(kPollBackoffNs);
 #pragma unroll
             for (int j = 0; j < K; ++j)
                 if (pend & (1u << j)) v[j] = ld_relaxed_v2(src + base + j * nt);
@@ -187,115 +182,6 @@ __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, un
         if (!ok) break;
     }
     return ok;
-}
-
-// Register prefetch of the first KP chunks per thread of a tile: issued one
-// tile-phase early (while the current tile computes), validated when the
-// tile is due.  Chunks beyond KP*nt go through load_tile synchronously.
-template <bool F16, int BT, int KP>
-struct Prefetch {
-    ulonglong2 v[KP];
-    __device__ __forceinline__ void issue(const ulonglong2* __restrict__ src, int n_words) {
-        const int n_chunks = (n_words + 1) >> 1;
-#pragma unroll
-        for (int j = 0; j < KP; ++j) {
-            const int idx = threadIdx.x + j * blockDim.x;
-            if (idx < n_chunks) v[j] = ld_relaxed_v2(src + idx);
-        }
-    }
-    __device__ __forceinline__ bool finish(const ulonglong2* __restrict__ src, unsigned char* hs, int n_words,
-                                           uint32_t want, bool spin, int32_t* status,
-                                           unsigned long long timeout_ns) {
-        const int n_chunks = (n_words + 1) >> 1;
-        const int nt = blockDim.x;
-        uint32_t pend = 0u;
-#pragma unroll
-        for (int j = 0; j < KP; ++j)
-            if (threadIdx.x + j * nt < n_chunks) pend |= 1u << j;
-        Watchdog wd{0ull, 0u};
-        bool ok = true;
-        while (true) {
-#pragma unroll
-            for (int j = 0; j < KP; ++j) {
-                if (pend & (1u << j)) {
-                    const int idx = threadIdx.x + j * nt;
-                    const bool has1 = 2 * idx + 1 < n_words;
-                    if (tag_of(v[j].x) == want && (!has1 || tag_of(v[j].y) == want)) {
-                        Fmt<F16, BT>::store(hs, idx, v[j].x, v[j].y, has1);
-                        pend &= ~(1u << j);
-                    }
-                }
-            }
-            if (pend == 0u) break;
-            if (!spin) {
-                atomicCAS(status, 0, -4);
-                break;
-            }
-            if (watchdog_tick(wd, status, timeout_ns)) {
-                ok = false;
-                break;
-            }
-            __nanosleep(kPollBackoffNs);  // stale: back off instead of flooding the LSU
-#pragma unroll
-            for (int j = 0; j < KP; ++j)
-                if (pend & (1u << j)) v[j] = ld_relaxed_v2(src + threadIdx.x + j * nt);
-        }
-        if (ok && n_chunks > KP * nt)
-            ok = load_tile<F16, BT, 4>(src, hs, n_words, want, spin, status, timeout_ns, KP * nt);
-        return ok;
-    }
-};
-
-// ---------------------------------------------------------------------------
-// TMA staging of the tagged h words (sm_90+/sm_100 bulk async copy).
-// One elected thread moves a whole tile (or a segment of it) of tagged words
-// global -> shared memory with cp.async.bulk, completion on an mbarrier; all
-// threads then validate tags in shared memory and compact the values into hs.
-// No registers are held while the copy is in flight, so the next tile's copy
-// can be issued before the current tile computes.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of dst before async writes
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst_smem)),
-        "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-// Validate one staged segment (chunks [c0, c1)) and compact it into hs.
-// Returns true if any chunk of this thread is stale.
-template <bool F16, int BT>
-__device__ __forceinline__ bool stage_pass(const ulonglong2* staging, unsigned char* hs, int c0, int c1, int n_words,
-                                           uint32_t want) {
-    bool stale = false;
-    for (int c = c0 + static_cast<int>(threadIdx.x); c < c1; c += blockDim.x) {
-        const ulonglong2 v = staging[c - c0];
-        const bool has1 = 2 * c + 1 < n_words;
-        stale |= !(tag_of(v.x) == want && (!has1 || tag_of(v.y) == want));
-        Fmt<F16, BT>::store(hs, c, v.x, v.y, has1);
-    }
-    return stale;
 }
 
 // ---------------------------------------------------------------------------
@@ -317,14 +203,8 @@ __device__ __forceinline__ float fma_f16f16f32(uint32_t a_lo_half, uint32_t b_ha
 template <int NP, int BT, bool F16>
 struct Weights;
 
-// The operate loop runs in groups of GS slots: all GS shared-memory loads of
-// a group are issued before its FMAs (memory-level parallelism), and the
-// warp-uniform slot count n_w is checked once per group.  Slots between n_w
-// and the end of a group hold zero weights reading column 0 (a broadcast),
-// exactly like the paper's <index, 0> padding pairs.
 template <int NP, int BT>
 struct Weights<NP, BT, false> {
-    static constexpr int GS = BT == 4 ? 4 : 8;
     uint32_t off[NP];
     float w[NP];
     __device__ __forceinline__ void load(const RecParams& p, size_t img0, int n_w) {
@@ -341,43 +221,20 @@ struct Weights<NP, BT, false> {
     }
     __device__ __forceinline__ void operate(float (&acc)[BT], const unsigned char* hs, int n_w) const {
 #pragma unroll
-        for (int i0 = 0; i0 < NP; i0 += GS) {
-            if (i0 < n_w) {
+        for (int i = 0; i < NP; ++i) {
+            if (i < n_w) {
                 if (BT == 4) {
-                    float4 h[GS];
-#pragma unroll
-                    for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) h[j] = *reinterpret_cast<const float4*>(hs + off[i0 + j]);
-#pragma unroll
-                    for (int j = 0; j < GS; ++j) {
-                        if (i0 + j < NP) {
-                            const float wv = w[i0 + j];
-                            acc[0] = fmaf(wv, h[j].x, acc[0]);
-                            acc[1 % BT] = fmaf(wv, h[j].y, acc[1 % BT]);
-                            acc[2 % BT] = fmaf(wv, h[j].z, acc[2 % BT]);
-                            acc[3 % BT] = fmaf(wv, h[j].w, acc[3 % BT]);
-                        }
-                    }
+                    const float4 h = *reinterpret_cast<const float4*>(hs + off[i]);
+                    acc[0] = fmaf(w[i], h.x, acc[0]);
+                    acc[1 % BT] = fmaf(w[i], h.y, acc[1 % BT]);
+                    acc[2 % BT] = fmaf(w[i], h.z, acc[2 % BT]);
+                    acc[3 % BT] = fmaf(w[i], h.w, acc[3 % BT]);
                 } else if (BT == 2) {
-                    float2 h[GS];
-#pragma unroll
-                    for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) h[j] = *reinterpret_cast<const float2*>(hs + off[i0 + j]);
-#pragma unroll
-                    for (int j = 0; j < GS; ++j) {
-                        if (i0 + j < NP) {
-                            acc[0] = fmaf(w[i0 + j], h[j].x, acc[0]);
-                            acc[1 % BT] = fmaf(w[i0 + j], h[j].y, acc[1 % BT]);
-                        }
-                    }
+                    const float2 h = *reinterpret_cast<const float2*>(hs + off[i]);
+                    acc[0] = fmaf(w[i], h.x, acc[0]);
+                    acc[1 % BT] = fmaf(w[i], h.y, acc[1 % BT]);
                 } else {
-                    float h[GS];
-#pragma unroll
-                    for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) h[j] = *reinterpret_cast<const float*>(hs + off[i0 + j]);
-#pragma unroll
-                    for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) acc[0] = fmaf(w[i0 + j], h[j], acc[0]);
+                    acc[0] = fmaf(w[i], *reinterpret_cast<const float*>(hs + off[i]), acc[0]);
                 }
             }
         }
@@ -386,7 +243,6 @@ struct Weights<NP, BT, false> {
 
 template <int NP, int BT>
 struct Weights<NP, BT, true> {
-    static constexpr int GS = BT == 4 ? 4 : 8;
     uint32_t pw[NP];
     __device__ __forceinline__ void load(const RecParams& p, size_t img0, int n_w) {
 #pragma unroll
@@ -394,43 +250,22 @@ struct Weights<NP, BT, true> {
     }
     __device__ __forceinline__ void operate(float (&acc)[BT], const unsigned char* hs, int n_w) const {
 #pragma unroll
-        for (int i0 = 0; i0 < NP; i0 += GS) {
-            if (i0 < n_w) {
+        for (int i = 0; i < NP; ++i) {
+            if (i < n_w) {
+                const uint32_t o = pw[i] >> 16;
                 if (BT == 4) {
-                    uint2 h[GS];
-#pragma unroll
-                    for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) h[j] = *reinterpret_cast<const uint2*>(hs + (pw[i0 + j] >> 16));
-#pragma unroll
-                    for (int j = 0; j < GS; ++j) {
-                        if (i0 + j < NP) {
-                            const uint32_t wv = pw[i0 + j];
-                            acc[0] = fma_f16f16f32(wv, h[j].x, acc[0]);
-                            acc[1 % BT] = fma_f16f16f32(wv, h[j].x >> 16, acc[1 % BT]);
-                            acc[2 % BT] = fma_f16f16f32(wv, h[j].y, acc[2 % BT]);
-                            acc[3 % BT] = fma_f16f16f32(wv, h[j].y >> 16, acc[3 % BT]);
-                        }
-                    }
+                    const uint2 h = *reinterpret_cast<const uint2*>(hs + o);
+                    acc[0] = fma_f16f16f32(pw[i], h.x, acc[0]);
+                    acc[1 % BT] = fma_f16f16f32(pw[i], h.x >> 16, acc[1 % BT]);
+                    acc[2 % BT] = fma_f16f16f32(pw[i], h.y, acc[2 % BT]);
+                    acc[3 % BT] = fma_f16f16f32(pw[i], h.y >> 16, acc[3 % BT]);
                 } else if (BT == 2) {
-                    uint32_t h[GS];
-#pragma unroll
-                    for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) h[j] = *reinterpret_cast<const uint32_t*>(hs + (pw[i0 + j] >> 16));
-#pragma unroll
-                    for (int j = 0; j < GS; ++j) {
-                        if (i0 + j < NP) {
-                            acc[0] = fma_f16f16f32(pw[i0 + j], h[j], acc[0]);
-                            acc[1 % BT] = fma_f16f16f32(pw[i0 + j], h[j] >> 16, acc[1 % BT]);
-                        }
-                    }
+                    const uint32_t h = *reinterpret_cast<const uint32_t*>(hs + o);
+                    acc[0] = fma_f16f16f32(pw[i], h, acc[0]);
+                    acc[1 % BT] = fma_f16f16f32(pw[i], h >> 16, acc[1 % BT]);
                 } else {
-                    uint32_t h[GS];
-#pragma unroll
-                    for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) h[j] = *reinterpret_cast<const unsigned short*>(hs + (pw[i0 + j] >> 16));
-#pragma unroll
-                    for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) acc[0] = fma_f16f16f32(pw[i0 + j], h[j], acc[0]);
+                    const uint32_t h = *reinterpret_cast<const unsigned short*>(hs + o);
+                    acc[0] = fma_f16f16f32(pw[i], h, acc[0]);
                 }
             }
         }
@@ -467,18 +302,19 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     using F = Fmt<F16, BT>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int H = p.H;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
     const int cta = blockIdx.x;
     const int u0 = p.cta_unit0[cta];
     const int U = p.cta_unit0[cta + 1] - u0;
-    // shared memory: hs[2] (double-buffered h_{s-1} tile, E bytes per unit),
-    // then the LSTM cell state of every (tile, unit, sample)
-    const size_t hs_bytes = (static_cast<size_t>(H) * F::E + 15) & ~static_cast<size_t>(15);
-    ulonglong2* staging = reinterpret_cast<ulonglong2*>(smem + 2 * hs_bytes);  // [stage_chunks] tagged words
-    float* cs = reinterpret_cast<float*>(smem + 2 * hs_bytes + static_cast<size_t>(p.stage_chunks) * 16);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(
-        (reinterpret_cast<uintptr_t>(cs + (G == 4 ? p.n_tiles * p.units_max * BT : 0)) + 7) & ~static_cast<uintptr_t>(7));
-    int* s_abort = reinterpret_cast<int*>(mbar + 1);
+    const int n_items = U * BT;                       // epilogue items (unit, sample) of one tile
+    const int item_rounds = (n_items + nt - 1) / nt;  // uniform within the CTA
+    const int umax_bt = p.units_max * BT;
+    // shared memory: hs [H][BT] at offset 0 (E bytes per unit), then fp32 areas
+    unsigned char* hs = smem;
+    float* zs = reinterpret_cast<float*>(smem + ((static_cast<size_t>(H) * F::E + 15) & ~static_cast<size_t>(15)));
+    float* bps = zs + G * umax_bt;                           // b'_s of this tile: [item][G]
+    float* cs = bps + G * umax_bt;                           // LSTM c: [n_tiles][item]
+    int* s_abort = reinterpret_cast<int*>(cs + (G == 4 ? p.n_tiles * umax_bt : 0));
 
     const int L = p.lanes_per_row;
     const int n_w = p.warp_slots[cta * (p.threads >> 5) + warp];
@@ -490,80 +326,46 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     Weights<NP, BT, F16> W;
     W.load(p, static_cast<size_t>(cta) * NP * p.threads + tid, n_w);
 
-    // Row of this lane: local row k = unit_local * G + gate (srnn_packer.cpp).
-    const int krow = warp * (32 / L) + lane / L;
-    const bool row_valid = krow < G * U;
-    const bool row_leader = (lane % L) == 0 && row_valid;
-    const int ul = krow / G, gate = krow % G;      // local unit, gate of this row
-    const int unit = u0 + ul;
-    const bool unit_leader = row_leader && gate == 0;  // owns h (and c) of its unit
-    if (tid == 0) {
-        *s_abort = 0;
-        mbar_init(mbar, 1);
-    }
-    __syncthreads();
+    const int krow = warp * (32 / L) + lane / L;  // local row of this lane
+    const bool row_leader = (lane % L) == 0 && krow < G * U;
+    if (tid == 0) *s_abort = 0;
 
-    // Per-lane bases hoisted out of the time loop.
-    unsigned long long* const xb_unit = p.xbuf + unit * F::WPR;
-    const float* const bp_row = p.bprime + gate * H + unit;
-    float* const y_unit = p.y != nullptr ? p.y + unit : nullptr;
-    const size_t bp_step = static_cast<size_t>(p.B) * GH, y_step = static_cast<size_t>(p.B) * H;
-    const int act = p.act;
-
-    // Publish the BT values of unit `unit`, (step s, tile k) as tagged words.
-    auto publish = [&](int s, int k, const float (&h)[BT]) {
-        unsigned long long* dst = xb_unit + static_cast<size_t>((s & 1) * p.n_tiles + k) * tile_stride - unit * F::WPR;
-        const uint64_t tag = static_cast<uint64_t>(p.epoch + static_cast<uint32_t>(s)) << 32;
+    // Publish item e's h of (step s, tile k) as tagged words.  Called by all
+    // threads of the CTA (the fp16 pairing uses a shuffle); `ok` masks items.
+    auto publish = [&](int s, int k, int e, bool ok, float h) {
+        unsigned long long* dst = p.xbuf + static_cast<size_t>((s & 1) * p.n_tiles + k) * tile_stride;
+        const uint32_t tag = p.epoch + static_cast<uint32_t>(s);
+        const int unit = u0 + e / BT, eb = e % BT;
         if (!F16) {
-#pragma unroll
-            for (int b = 0; b < BT; ++b) st_relaxed_u64(dst + unit * BT + b, tag | __float_as_uint(h[b]));
+            if (ok) st_relaxed_u64(dst + unit * BT + eb, pack_tagged(h, tag));
         } else {
-#pragma unroll
-            for (int w = 0; w < F::WPR; ++w) {
-                uint32_t lo = __half_as_ushort(__float2half_rn(h[2 * w]));
-                if (2 * w + 1 < BT) lo |= static_cast<uint32_t>(__half_as_ushort(__float2half_rn(h[(2 * w + 1) % BT]))) << 16;
-                st_relaxed_u64(dst + unit * F::WPR + w, tag | lo);
+            const uint32_t hb = __half_as_ushort(__float2half_rn(h));
+            const uint32_t nb = __shfl_down_sync(0xffffffffu, hb, 1);
+            if (ok && (BT == 1 || (eb & 1) == 0)) {
+                const uint32_t lo = BT == 1 ? hb : (hb | (nb << 16));
+                st_relaxed_u64(dst + unit * F::WPR + (eb >> 1), (static_cast<unsigned long long>(tag) << 32) | lo);
             }
         }
     };
 
     // ---- publish h_0 (tag = epoch) and initialise c ----
-    if (unit_leader) {
-        for (int k = 0; k < p.n_tiles; ++k) {
-            float h[BT];
-#pragma unroll
-            for (int b = 0; b < BT; ++b) {
-                const int bg = k * BT + b;
-                h[b] = (p.h0 != nullptr && bg < p.B) ? p.h0[static_cast<size_t>(bg) * H + unit] : 0.0f;
+    for (int k = 0; k < p.n_tiles; ++k) {
+        for (int j = 0; j < item_rounds; ++j) {
+            const int e = tid + j * nt;
+            const bool ok = e < n_items;
+            const int unit = u0 + e / BT, bg = k * BT + e % BT;
+            float h = 0.0f;
+            if (ok) {
+                h = (p.h0 != nullptr && bg < p.B) ? p.h0[static_cast<size_t>(bg) * H + unit] : 0.0f;
                 if (G == 4)
-                    cs[(k * p.units_max + ul) * BT + b] =
-                        (p.c0 != nullptr && bg < p.B) ? p.c0[static_cast<size_t>(bg) * H + unit] : 0.0f;
+                    cs[k * umax_bt + e] = (p.c0 != nullptr && bg < p.B) ? p.c0[static_cast<size_t>(bg) * H + unit] : 0.0f;
             }
-            publish(0, k, h);
+            publish(0, k, e, ok, h);
         }
     }
     const bool grid_sync = (p.flags & kFlagGridSync) != 0u;
     if (grid_sync) cg::this_grid().sync();
-
-    // Register prefetch of tile (s, k)'s h_{s-1} tagged words.  With >= 2
-    // batch tiles the next tile's input was published one tile-phase ago and
-    // its loads are issued right after this tile's operate, landing while the
-    // epilogue runs ("as we process iteration n, we can load the
-    // states for iteration n+1").
-    const bool early = p.n_tiles > 1 && !grid_sync;
-    const int n_chunks = (n_words + 1) >> 1;
-    const int stage_chunks = p.stage_chunks;
-    auto tile_src = [&](int s, int k) {
-        return reinterpret_cast<const ulonglong2*>(p.xbuf +
-                                                   static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
-    };
-    uint32_t mbar_phase = 0;
-    auto issue_seg = [&](const ulonglong2* src, int c0) {  // thread 0 only
-        const int c1 = min(n_chunks, c0 + stage_chunks);
-        tma_load_1d(staging, src + c0, static_cast<uint32_t>(c1 - c0) * 16u, mbar);
-    };
-    if (early && tid == 0) issue_seg(tile_src(1, 0), 0);
-    int parity = 0;
+    __syncthreads();
 
     for (int s = 1; s <= p.T; ++s) {
         for (int k = 0; k < p.n_tiles; ++k) {
@@ -571,118 +373,84 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                                   ? p.profile + ((static_cast<size_t>(cta) * p.T + (s - 1)) * p.n_tiles + k) * 4
                                   : nullptr;
             if (prof) prof[0] = clock64();
-            // b'_s of this lane's row for the BT samples (lands during operate)
-            float bp[BT];
-            const float* bps = bp_row + static_cast<size_t>(s - 1) * bp_step + static_cast<size_t>(k * BT) * GH;
-            float* ys = y_unit != nullptr ? y_unit + static_cast<size_t>(s - 1) * y_step + static_cast<size_t>(k * BT) * H
-                                          : nullptr;
-            const int nb = min(BT, p.B - k * BT);  // real samples in this tile
+            // b'_s of this tile -> shared memory, asynchronously (in flight while we spin)
+            for (int j = 0; j < item_rounds; ++j) {
+                const int e = tid + j * nt;
+                if (e < n_items) {
+                    const int unit = u0 + e / BT, bg = k * BT + e % BT;
 #pragma unroll
-            for (int b = 0; b < BT; ++b) bp[b] = (row_leader && b < nb) ? __ldg(bps + b * GH) : 0.0f;
-            // ---- load: h_{s-1} tile k -> hs[parity] ----
-            // TMA-stage the tagged words (segment by segment), validate the
-            // tags in shared memory, compact the values into hs; a stale
-            // segment is re-fetched whole after a short backoff.
-            unsigned char* hs = smem + parity * hs_bytes;
-            {
-                const uint32_t want = p.epoch + static_cast<uint32_t>(s - 1);
-                const ulonglong2* src = tile_src(s, k);
-                Watchdog wd{0ull, 0u};
-                for (int c0 = 0; c0 < n_chunks; c0 += stage_chunks) {
-                    bool prefetched = early && c0 == 0;
-                    while (true) {
-                        if (!prefetched && tid == 0) issue_seg(src, c0);
-                        prefetched = false;
-                        mbar_wait(mbar, mbar_phase);
-                        mbar_phase ^= 1u;
-                        const bool stale =
-                            stage_pass<F16, BT>(staging, hs, c0, min(n_chunks, c0 + stage_chunks), n_words, want);
-                        if (!__syncthreads_or(stale)) break;
-                        if (tid == 0) {
-                            if (grid_sync)
-                                atomicCAS(p.status, 0, -4 /* protocol violation */);
-                            else if (watchdog_tick(wd, p.status, p.timeout_ns))
-                                *s_abort = 1;
-                        }
-                        __syncthreads();
-                        if (*s_abort || grid_sync) break;
-                        __nanosleep(kPollBackoffNs);
+                    for (int q = 0; q < G; ++q) {
+                        if (bg < p.B)
+                            cp_async_f32(&bps[e * G + q], p.bprime + (static_cast<size_t>(s - 1) * p.B + bg) * GH + q * H + unit);
+                        else
+                            bps[e * G + q] = 0.0f;
                     }
-                    if (*s_abort) break;
                 }
             }
+            cp_async_commit();
+            // ---- load: h_{s-1} tile k -> hs ----
+            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
+                p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
+            if (!load_tile<F16, BT, LoadK<NP, F16>::value>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
+                                                            !grid_sync, p.status, p.timeout_ns))
+                *s_abort = 1;
+            __syncthreads();
             if (prof) prof[1] = clock64();
             if (*s_abort) goto done;
-            const int ns = k + 1 < p.n_tiles ? s : s + 1, nk = k + 1 < p.n_tiles ? k + 1 : 0;
 
             // ---- operate + reduce ----
-            float acc[BT];
+            {
+                float acc[BT];
 #pragma unroll
-            for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
-            W.operate(acc, hs, n_w);
-            // next tile's input was published one tile-phase ago: stage it now
-            if (early && ns <= p.T && tid == 0) issue_seg(tile_src(ns, nk), 0);
-#pragma unroll
-            for (int m = 16; m >= 1; m >>= 1) {
-                if (m < L) {
+                for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
+                W.operate(acc, hs, n_w);
+                for (int m = L >> 1; m >= 1; m >>= 1) {
 #pragma unroll
                     for (int b = 0; b < BT; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], m);
                 }
+                if (row_leader) {
+#pragma unroll
+                    for (int b = 0; b < BT; ++b) zs[krow * BT + b] = acc[b];
+                }
             }
+            cp_async_wait_all();
+            __syncthreads();
             if (prof) prof[2] = clock64();
 
-            // ---- epilogue in the row-leader lanes: z = acc + b'; g / gates; publish ----
-            float z[BT];
-#pragma unroll
-            for (int b = 0; b < BT; ++b) z[b] = acc[b] + bp[b];
-            if (G == 4) {
-                // gates i, f, g, o of a unit are rows 4u..4u+3: lanes +0, +L, +2L, +3L
-                float zf[BT], zg[BT], zo[BT];
-#pragma unroll
-                for (int b = 0; b < BT; ++b) {
-                    zf[b] = __shfl_down_sync(0xffffffffu, z[b], L);
-                    zg[b] = __shfl_down_sync(0xffffffffu, z[b], 2 * L);
-                    zo[b] = __shfl_down_sync(0xffffffffu, z[b], 3 * L);
-                }
-                if (unit_leader) {
-                    float h[BT];
-#pragma unroll
-                    for (int b = 0; b < BT; ++b) {
-                        float* cp = &cs[(k * p.units_max + ul) * BT + b];
-                        const float c = sigmoidf_acc(zf[b]) * (*cp) + sigmoidf_acc(z[b]) * tanhf(zg[b]);
+            // ---- epilogue: activation / gates, y, tagged publish of h_s ----
+            if ((p.flags & kFlagJitter) && tid == 0) {
+                const uint32_t r = (static_cast<uint32_t>(cta) * 2654435761u) ^ (static_cast<uint32_t>(s * 40503 + k));
+                __nanosleep((r >> 7) & 2047u);
+            }
+            for (int j = 0; j < item_rounds; ++j) {
+                const int e = tid + j * nt;
+                const bool ok = e < n_items;
+                float h = 0.0f;
+                if (ok) {
+                    const int unit = u0 + e / BT, bg = k * BT + e % BT;
+                    if (G == 1) {
+                        h = activation(p.act, zs[e] + bps[e]);
+                    } else {
+                        const int ub = U * BT;
+                        const float zi = zs[0 * ub + e] + bps[e * G + 0];
+                        const float zf = zs[1 * ub + e] + bps[e * G + 1 % G];
+                        const float zg = zs[2 * ub + e] + bps[e * G + 2 % G];
+                        const float zo = zs[3 * ub + e] + bps[e * G + 3 % G];
+                        float* cp = &cs[k * umax_bt + e];
+                        const float c = sigmoidf_acc(zf) * (*cp) + sigmoidf_acc(zi) * tanhf(zg);
                         *cp = c;
-                        h[b] = sigmoidf_acc(zo[b]) * tanhf(c);
-                        if (b < nb) {
-                            if (ys != nullptr) ys[b * H] = h[b];
-                            if (s == p.T) {
-                                const int bg = k * BT + b;
-                                if (p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + unit] = h[b];
-                                if (p.cT != nullptr) p.cT[static_cast<size_t>(bg) * H + unit] = c;
-                            }
-                        }
+                        h = sigmoidf_acc(zo) * tanhf(c);
+                        if (s == p.T && p.cT != nullptr && bg < p.B) p.cT[static_cast<size_t>(bg) * H + unit] = c;
                     }
-                    publish(s, k, h);
-                }
-            } else if (unit_leader) {
-                float h[BT];
-#pragma unroll
-                for (int b = 0; b < BT; ++b) h[b] = activation(act, z[b]);
-#pragma unroll
-                for (int b = 0; b < BT; ++b) {
-                    if (b < nb) {
-                        if (ys != nullptr) ys[b * H] = h[b];
-                        if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(k * BT + b) * H + unit] = h[b];
+                    if (bg < p.B) {
+                        if (p.y != nullptr) p.y[(static_cast<size_t>(s - 1) * p.B + bg) * H + unit] = h;
+                        if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + unit] = h;
                     }
                 }
-                if ((p.flags & kFlagJitter) != 0u) {
-                    const uint32_t r = (static_cast<uint32_t>(cta) * 2654435761u) ^ (static_cast<uint32_t>(s * 40503 + k));
-                    __nanosleep((r >> 7) & 2047u);
-                }
-                publish(s, k, h);
+                publish(s, k, e, ok, h);
             }
             if (prof) prof[3] = clock64();
             if (grid_sync) cg::this_grid().sync();
-            parity ^= 1;
         }
     }
 done:
