@@ -2,6 +2,8 @@
 // capacity planning, weight loading through the packer
 // (a2), and the forward entry points that enqueue the input-projection GEMM
 // (a1) and the persistent recurrent kernel (a3-a9).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -38,6 +40,13 @@ struct srnn_plan {
     int32_t* d_unit0 = nullptr;
     int32_t* d_wslots = nullptr;
     float* d_wx = nullptr;
+    // fp16 mode tensor-core GEMM: W_x and x rounded to fp16, K padded to a multiple of 8
+    bool tc_gemm = false;
+    int k_pad = 0;
+    void* d_wx16 = nullptr;
+    void* d_x16 = nullptr;  // [T_max*B_max][k_pad]
+    alignas(64) CUtensorMap map_x16;
+    alignas(64) CUtensorMap map_wx16;
     float* d_bias = nullptr;
     float* d_bprime = nullptr;      // [T_max][B_max][G*H]
     unsigned long long* d_xbuf = nullptr;
@@ -87,6 +96,8 @@ void free_device(srnn_plan* p) {
     cudaFree(p->d_unit0);
     cudaFree(p->d_wslots);
     cudaFree(p->d_wx);
+    cudaFree(p->d_wx16);
+    cudaFree(p->d_x16);
     cudaFree(p->d_bias);
     cudaFree(p->d_bprime);
     cudaFree(p->d_xbuf);
@@ -100,6 +111,25 @@ void free_device(srnn_plan* p) {
     cudaFree(p->d_prof);
     if (p->stream) cudaStreamDestroy(p->stream);
     p->d_img = nullptr;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+bool encode_fp16_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k_pad) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    cuuint64_t dims[2] = {k_pad, rows};
+    cuuint64_t strides[1] = {k_pad * 2};
+    cuuint32_t box[2] = {64, 128};  // 64 fp16 = one 128-byte swizzle row, 128 rows (srnn_gemm_tc.cu)
+    cuuint32_t estr[2] = {1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // Estimated cycles of one tile-step on the busiest CTA (planner cost model,
@@ -419,6 +449,26 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
         if (e == cudaSuccess) e = cudaMemcpy(p->d_wslots, l.warp_slots.data(), l.warp_slots.size() * 4, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMalloc(&p->d_wx, wx_n * 4);
         if (e == cudaSuccess) e = cudaMemcpy(p->d_wx, wx, wx_n * 4, cudaMemcpyHostToDevice);
+        cudaFree(p->d_wx16);
+        cudaFree(p->d_x16);
+        p->d_wx16 = p->d_x16 = nullptr;
+        p->tc_gemm = fp16 && (p->cfg.flags & SRNN_FLAG_SIMT_GEMM) == 0;
+        if (e == cudaSuccess && p->tc_gemm) {
+            // W_x and x rounded to fp16 (RNE) for the tensor-core input GEMM (srnn_gemm_tc.cu)
+            const int I = p->cfg.input;
+            p->k_pad = (I + 7) & ~7;
+            std::vector<uint16_t> w16(static_cast<size_t>(R) * p->k_pad, 0);
+            for (int r = 0; r < R; ++r)
+                for (int i = 0; i < I; ++i)
+                    w16[static_cast<size_t>(r) * p->k_pad + i] = float_to_half_rne(wx[static_cast<size_t>(r) * I + i]);
+            const size_t xrows = static_cast<size_t>(std::max(1, p->cfg.max_steps)) * p->cfg.batch;
+            e = cudaMalloc(&p->d_wx16, w16.size() * 2);
+            if (e == cudaSuccess) e = cudaMemcpy(p->d_wx16, w16.data(), w16.size() * 2, cudaMemcpyHostToDevice);
+            if (e == cudaSuccess) e = cudaMalloc(&p->d_x16, xrows * p->k_pad * 2);
+            if (e == cudaSuccess && (!encode_fp16_kmajor(&p->map_wx16, p->d_wx16, R, p->k_pad) ||
+                                     !encode_fp16_kmajor(&p->map_x16, p->d_x16, xrows, p->k_pad)))
+                return SRNN_ERR_CUDA;
+        }
         if (e == cudaSuccess) e = cudaMalloc(&p->d_bias, static_cast<size_t>(R) * 4);
         if (e == cudaSuccess) {
             if (bias)
@@ -448,6 +498,16 @@ srnn_status_t srnn_input_projection(srnn_plan_t p, int32_t T, int32_t B, const f
         return SRNN_ERR_INVALID_VALUE;
     if (T == 0) return SRNN_OK;
     DeviceGuard g(p->cfg.device);
+    if (p->tc_gemm) {
+        const int64_t M = static_cast<int64_t>(T) * B;
+        const int I = p->cfg.input;
+        int e = I == p->k_pad ? launch_f32_to_f16(x, p->d_x16, M * I, stream)
+                              : launch_f32_to_f16_padded(x, p->d_x16, M, I, p->k_pad, stream);
+        if (e == 0)
+            e = launch_gemm_tc(&p->map_x16, &p->map_wx16, p->d_bias, bprime, static_cast<int>(M), p->G * p->cfg.hidden,
+                               p->k_pad, stream);
+        return e == 0 ? SRNN_OK : SRNN_ERR_CUDA;
+    }
     GemmParams gp;
     gp.M = static_cast<int64_t>(T) * B;
     gp.N = p->G * p->cfg.hidden;

@@ -1,0 +1,247 @@
+// srnn_gemm_tc.cu -- step a1 in fp16 mode on the 5th-generation tensor cores.
+//
+// The input projection for all timesteps at once (Eq. 2: "W x_t
+// ... has no dependency, so it can be processed in parallel and added to b,
+// becoming b'"):
+//
+//     b'[m][n] = bias[n] + sum_k x16[m][k] * Wx16[n][k]     (fp16 in, fp32 accumulate)
+//
+// x (fp32, [T*B][I]) is first rounded to fp16 (RNE) by a small kernel; W_x is
+// rounded once at srnn_load_weights.  One CTA computes a 128 x 128 output
+// tile with tcgen05.mma (cta_group::1, kind::f16, M=128 N=128 K=16) from
+// shared-memory operands staged by TMA (cp.async.bulk.tensor, 128-byte
+// swizzle, 4-stage mbarrier pipeline); the accumulator lives in TMEM and is
+// read back by four epilogue warps with tcgen05.ld, + bias, stored as fp32.
+//
+//   warp 0: TMA producer (one elected lane)    warp 1: TMEM alloc + MMA issuer
+//   warps 2-5: epilogue (TMEM lane quarter = warp % 4)
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "srnn_internal.h"
+
+namespace srnn {
+namespace {
+
+constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 64, TC_STAGES = 4, TC_THREADS = 192;
+constexpr uint32_t TC_TILE_BYTES = TC_BM * TC_BK * 2;  // 16 KB per operand tile
+constexpr uint32_t TC_TMEM_COLS = 128;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred P1;\nLAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra LAB_WAIT;\n}\n" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            su32(dst)),
+        "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
+    const uint64_t addr = su32(p);
+    return ((addr >> 4) & 0x3FFFull) | (1ull << 16) /* LBO (unused for SW128 K-major) */ |
+           ((1024ull >> 4) << 32) /* SBO */ | (1ull << 46) /* sm100 descriptor version */ |
+           (2ull << 61) /* SWIZZLE_128B */;
+}
+// Instruction descriptor, kind::f16: D f32, A/B f16, both K-major, M = 128, N = 128.
+constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | ((TC_BN >> 3) << 17) | ((TC_BM >> 4) << 24);
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    gemm_tc_f16_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                       const float* __restrict__ bias, float* __restrict__ C, int M, int N, int K) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte alignment for the 128B-swizzled operand tiles
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* sA = smem;
+    unsigned char* sB = smem + TC_STAGES * TC_TILE_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * TC_STAGES * TC_TILE_BYTES);
+    uint64_t* empty = full + TC_STAGES;
+    uint64_t* tmem_full = empty + TC_STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * TC_BN;
+    const int nk = (K + TC_BK - 1) / TC_BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TC_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+    }
+    if (warp == 1) {  // TMEM allocation (whole warp)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                     "r"(TC_TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---- TMA producer ----
+        for (int kb = 0; kb < nk; ++kb) {
+            const int s = kb % TC_STAGES;
+            if (kb >= TC_STAGES) mbar_wait(&empty[s], ((kb / TC_STAGES) - 1) & 1);
+            mbar_expect_tx(&full[s], 2 * TC_TILE_BYTES);
+            tma_load_2d(sA + s * TC_TILE_BYTES, &map_a, &full[s], kb * TC_BK, m0);
+            tma_load_2d(sB + s * TC_TILE_BYTES, &map_b, &full[s], kb * TC_BK, n0);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---- MMA issuer: D[tmem] (+)= A[smem] * B[smem]^T ----
+        for (int kb = 0; kb < nk; ++kb) {
+            const int s = kb % TC_STAGES;
+            mbar_wait(&full[s], (kb / TC_STAGES) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t da = smem_desc_sw128(sA + s * TC_TILE_BYTES);
+            const uint64_t db = smem_desc_sw128(sB + s * TC_TILE_BYTES);
+#pragma unroll
+            for (int k = 0; k < TC_BK / 16; ++k) {
+                const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+                // advance 16 fp16 (32 bytes) along K inside the swizzled row: +2 in the >>4 address field
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                    "l"(da + 2ull * k), "l"(db + 2ull * k), "r"(kIdesc), "r"(accum)
+                    : "memory");
+            }
+            // free the smem stage once these MMAs have read it
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             su32(&empty[s]))
+                         : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         su32(tmem_full))
+                     : "memory");
+    } else if (warp >= 2) {
+        // ---- epilogue: TMEM -> registers -> + bias -> global ----
+        const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
+        const int row = m0 + quarter * 32 + lane;
+        mbar_wait(tmem_full, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+        for (int c = 0; c < TC_BN; c += 32) {
+            uint32_t v[32];
+            const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(c);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (row < M) {
+                float* crow = C + static_cast<size_t>(row) * N + n0 + c;
+                const int nvalid = min(32, N - (n0 + c));
+                if (nvalid == 32 && (N & 3) == 0) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        float4 o;
+                        o.x = __uint_as_float(v[j + 0]) + (bias ? __ldg(bias + n0 + c + j + 0) : 0.0f);
+                        o.y = __uint_as_float(v[j + 1]) + (bias ? __ldg(bias + n0 + c + j + 1) : 0.0f);
+                        o.z = __uint_as_float(v[j + 2]) + (bias ? __ldg(bias + n0 + c + j + 2) : 0.0f);
+                        o.w = __uint_as_float(v[j + 3]) + (bias ? __ldg(bias + n0 + c + j + 3) : 0.0f);
+                        *reinterpret_cast<float4*>(crow + j) = o;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < nvalid) crow[j] = __uint_as_float(v[j]) + (bias ? __ldg(bias + n0 + c + j) : 0.0f);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS)
+                     : "memory");
+    }
+}
+
+// fp32 -> fp16 (RNE), 4 elements per thread where aligned.
+__global__ void f32_to_f16_kernel(const float* __restrict__ in, __half* __restrict__ out, int64_t n) {
+    const int64_t i4 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    if (i4 + 3 < n) {
+        const float4 v = *reinterpret_cast<const float4*>(in + i4);
+        __half2 a = __floats2half2_rn(v.x, v.y), b = __floats2half2_rn(v.z, v.w);
+        *reinterpret_cast<__half2*>(out + i4) = a;
+        *reinterpret_cast<__half2*>(out + i4 + 2) = b;
+    } else {
+        for (int64_t i = i4; i < n; ++i) out[i] = __float2half_rn(in[i]);
+    }
+}
+
+// fp32 [rows][cols] -> fp16 [rows][ld_out] (RNE), zero padding in columns [cols, ld_out).
+__global__ void f32_to_f16_padded_kernel(const float* __restrict__ in, __half* __restrict__ out, int64_t rows,
+                                         int cols, int ld_out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= rows * ld_out) return;
+    const int64_t r = i / ld_out;
+    const int c = static_cast<int>(i - r * ld_out);
+    out[i] = c < cols ? __float2half_rn(in[r * cols + c]) : __float2half_rn(0.0f);
+}
+
+}  // namespace
+
+int launch_f32_to_f16_padded(const float* in, void* out, int64_t rows, int cols, int ld_out, void* stream) {
+    const int64_t n = rows * ld_out;
+    if (n <= 0) return 0;
+    f32_to_f16_padded_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        in, static_cast<__half*>(out), rows, cols, ld_out);
+    return static_cast<int>(cudaGetLastError());
+}
+
+size_t gemm_tc_smem_bytes() { return 2 * TC_STAGES * TC_TILE_BYTES + 1024 /* align */ + 256 /* barriers */; }
+
+int launch_f32_to_f16(const float* in, void* out, int64_t n, void* stream) {
+    if (n <= 0) return 0;
+    const int64_t threads = (n + 3) / 4;
+    const int blocks = static_cast<int>((threads + 255) / 256);
+    f32_to_f16_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(in, static_cast<__half*>(out), n);
+    return static_cast<int>(cudaGetLastError());
+}
+
+int launch_gemm_tc(const void* map_a, const void* map_b, const float* bias, float* C, int M, int N, int K,
+                   void* stream) {
+    if (M <= 0 || N <= 0) return 0;
+    static bool attr_set = false;
+    const size_t smem = gemm_tc_smem_bytes();
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_tc_f16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return static_cast<int>(e);
+        attr_set = true;
+    }
+    dim3 grid((N + TC_BN - 1) / TC_BN, (M + TC_BM - 1) / TC_BM);
+    gemm_tc_f16_kernel<<<grid, TC_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(
+        *static_cast<const CUtensorMap*>(map_a), *static_cast<const CUtensorMap*>(map_b), bias, C, M, N, K);
+    return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace srnn

@@ -58,6 +58,11 @@ int launch_recurrent(int np, int bt, int g, int f16, const RecParams& p, int num
                      size_t smem_bytes, void* stream, bool query_only, int* regs_out,
                      int* max_blocks_per_sm_out);
 int launch_gemm_f32(const GemmParams& p, void* stream);
+// fp16 tensor-core input GEMM (srnn_gemm_tc.cu); maps are CUtensorMap*.
+int launch_gemm_tc(const void* map_a, const void* map_b, const float* bias, float* C, int M, int N, int K,
+                   void* stream);
+int launch_f32_to_f16(const float* in, void* out, int64_t n, void* stream);
+int launch_f32_to_f16_padded(const float* in, void* out, int64_t rows, int cols, int ld_out, void* stream);
 
 // Compiled register-slot instances (pairs per lane); 96 exists only for the
 // fp16 mode (one register per pair).

@@ -169,6 +169,25 @@ def test_input_projection_alone(cuda_device):
     assert np.abs(bp.cpu().numpy() - ref).max() <= 1e-5
 
 
+@pytest.mark.parametrize("H,I,B,T,cell", [(384, 200, 3, 7, "rnn"), (200, 100, 3, 5, "rnn"), (2304, 2304, 4, 256, "rnn"),
+                                        (130, 64, 2, 9, "lstm"), (1024, 1024, 4, 100, "lstm")])
+def test_input_projection_tensor_cores(cuda_device, H, I, B, T, cell):
+    """fp16 mode: tcgen05 GEMM on fp16-rounded x and W_x, fp32 accumulate.
+    Against the oracle fed the same fp16-rounded operands (fp32 vs fp64
+    accumulation only) and against the unquantised oracle (fp16 rounding)."""
+    import torch
+    prob = inputs.make_problem(H, I, B, T, 0.05, cell=cell)
+    m = from_problem(prob, prec="fp16")
+    bp = m.input_projection(torch.from_numpy(prob["x"]).cuda())
+    torch.cuda.synchronize()
+    got = bp.cpu().numpy().astype(np.float64)
+    q = lambda a: np.asarray(a, np.float32).astype(np.float16).astype(np.float64)
+    ref_q = oracle.input_projection(q(prob["x"]), q(prob["wx"]), prob["bias"])
+    ref = oracle.input_projection(prob["x"], prob["wx"], prob["bias"])
+    assert np.abs(got - ref_q).max() <= 1e-4 * max(1.0, np.sqrt(I / 256))
+    assert np.abs(got - ref).max() <= 1e-2
+
+
 def test_forward_host_matches_device(cuda_device):
     prob = inputs.make_problem(640, 640, 4, 10, 0.1, act="relu", h0="random")
     m = from_problem(prob, prec="fp16")
