@@ -349,6 +349,13 @@ def main():
             "gpu_launches": 2 * args.steps,
             "clocks": clocks,
         }
+        gemm_flops = 2.0 * T * B * cfg["I"] * prob["G"] * H
+        out["input_gemm"] = {"kernel": "gemm_tc_f16_kernel (tcgen05) + f32_to_f16" if prec == "fp16" else
+                             "gemm_f32_nt_kernel (SIMT fp32)", "ms": t_gemm * 1000,
+                             "achieved_tflops": gemm_flops / t_gemm / 1e12,
+                             "peak_tflops": 1663.3 if prec == "fp16" else None,
+                             "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; fp16 has the same dense rate)",
+                             "frac": (gemm_flops / t_gemm / 1e12) / 1663.3 if prec == "fp16" else None}
         if not args.no_cublas and world == 1:
             cb = cublas_dense_baseline(H, B, T, dev)
             cb["speedup_vs_graph"] = cb["graph_us_per_timestep"] / (t_rec * 1e6 / T)
