@@ -221,3 +221,23 @@ def test_C4_lstm_speech_full(cuda_device):
     cfg = {k: v for k, v in inputs.CONFIGS["C4_speech"].items() if k != "prec"}
     prob = inputs.make_problem(**cfg)
     check(prob, "fp32")
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_batch_partition_bit_identical(cuda_device, world):
+    """shards run separately (here sequentially on one GPU,
+    same plan layout) and concatenated equal the single run bit for bit."""
+    import torch
+    from paper_1804_10223_b200.multigpu import shard
+    prob = inputs.make_problem(1152, 1152, 8, 32, 0.1, act="tanh", h0="random")
+    m = from_problem(prob, prec="fp16", batch_tile=4)
+    x = torch.from_numpy(prob["x"]).cuda()
+    h0 = torch.from_numpy(prob["h0"]).cuda()
+    y_full, _ = m.forward(x, h0)
+    parts = []
+    for r in range(world):
+        s0, c = shard(8, world, r)
+        y, _ = m.forward(x[:, s0:s0 + c].contiguous(), h0[s0:s0 + c].contiguous())
+        parts.append(y)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts, 1), y_full)
