@@ -123,6 +123,8 @@ typedef struct {
     int64_t wavefronts_per_step_max; /* packer's predicted smem wavefronts of the busiest CTA per batch tile (L) */
     int64_t wavefronts_per_step_ideal; /* same, if every phase were conflict-free and unpadded (L) */
     int64_t conflict_wavefronts;       /* extra wavefronts from bank conflicts in that CTA (L)        */
+    int64_t smem_weight_bytes_per_cta; /* shared-memory weight tier (pairs beyond the register slots) (L) */
+    int64_t image_slots_per_lane;      /* register + shared-memory slots per lane in the image (L)     */
 } srnn_plan_info_t;
 
 /* Create a plan for the layer described by *cfg.
@@ -187,7 +189,7 @@ srnn_status_t srnn_forward_host(srnn_plan_t plan, int32_t T, int32_t B, const fl
 srnn_status_t srnn_plan_status(srnn_plan_t plan);
 
 /* Copy the packer's host-side layout for inspection/tests (works in
- * host-only mode).  Arrays are [num_ctas][pairs_per_lane][threads_per_cta]:
+ * host-only mode).  Arrays are [num_ctas][image_slots_per_lane][threads_per_cta]:
  *   col_out  int32: U_r column of each slot (padding slots: a valid column)
  *   val_out  float: value (fp16-rounded in FP16W mode; 0 for padding)
  *   row_out  int32: global row (gate*H+unit) the slot's lane works on, -1 if idle

@@ -55,7 +55,8 @@ class PlanInfo(ctypes.Structure):
                  "fits")] + \
                [(n, ctypes.c_int64) for n in
                 ("nnz", "slots_total", "smem_bytes_per_cta", "weight_image_bytes", "wavefronts_per_step_max",
-                 "wavefronts_per_step_ideal", "conflict_wavefronts")]
+                 "wavefronts_per_step_ideal", "conflict_wavefronts", "smem_weight_bytes_per_cta",
+                 "image_slots_per_lane")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -170,13 +171,13 @@ class SparseRNN:
 
     def export_layout(self):
         inf = self.info()
-        n = inf["num_ctas"] * inf["pairs_per_lane"] * inf["threads_per_cta"]
+        n = inf["num_ctas"] * inf["image_slots_per_lane"] * inf["threads_per_cta"]
         col = np.empty(n, np.int32)
         val = np.empty(n, np.float32)
         row = np.empty(n, np.int32)
         _check("srnn_plan_export_layout",
                self.lib.srnn_plan_export_layout(self.handle, _ptr(col), _ptr(val), _ptr(row), n))
-        shape = (inf["num_ctas"], inf["pairs_per_lane"], inf["threads_per_cta"])
+        shape = (inf["num_ctas"], inf["image_slots_per_lane"], inf["threads_per_cta"])
         return col.reshape(shape), val.reshape(shape), row.reshape(shape)
 
     # -- device calls (torch tensors; stream = torch's current stream) ----

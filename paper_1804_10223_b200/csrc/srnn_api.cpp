@@ -31,7 +31,8 @@ struct srnn_plan {
     bool loaded = false;
     // layout decisions
     Layout lay;
-    int np_inst = 0;
+    int np_inst = 0;   // register slots per lane (compiled instance)
+    int ns_slots = 0;  // shared-memory tier slots per lane
     int regs = 0;
     size_t smem_bytes = 0;
     int64_t nnz = 0;
@@ -296,7 +297,9 @@ srnn_status_t srnn_plan_query(srnn_plan_t p, srnn_plan_info_t* out) {
         out->nnz = p->nnz;
         out->slots_total = l.slots_total;
         out->smem_bytes_per_cta = static_cast<int64_t>(p->smem_bytes);
-        out->weight_image_bytes = static_cast<int64_t>(l.num_ctas) * p->np_inst * l.threads *
+        out->smem_weight_bytes_per_cta = static_cast<int64_t>(p->ns_slots) * l.threads * (p->f16 ? 4 : 8);
+        out->image_slots_per_lane = p->np_inst + p->ns_slots;
+        out->weight_image_bytes = static_cast<int64_t>(l.num_ctas) * (p->np_inst + p->ns_slots) * l.threads *
                                   (p->f16 ? 4 : 8);
         out->wavefronts_per_step_max = l.wavefronts_max_cta;
         out->wavefronts_per_step_ideal = l.wavefronts_ideal_cta;
@@ -351,31 +354,47 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
         cands_l = {32, 16, 8, 4, 2, 1};
     double best_cost = 1e300;
     Layout best;
-    int best_inst = 0;
+    int best_inst = 0, best_ns = 0;
     bool any = false;
+    const int pair_bytes = p->f16 ? 4 : 8;
     for (int C : cands_c) {
         const int umax = (H + C - 1) / C;
-        const size_t smem = smem_for(p, umax, p->BT, p->n_tiles_max);
-        if (smem > static_cast<size_t>(p->smem_optin)) continue;
+        const size_t smem_base = smem_for(p, umax, p->BT, p->n_tiles_max);
+        if (smem_base > static_cast<size_t>(p->smem_optin)) continue;
         for (int L : cands_l) {
             const int rows_max = G * umax;
             const int threads = ((rows_max * L + 31) / 32) * 32;
             if (threads > 1024) continue;
+            // largest register instance whose thread cap admits this CTA size
+            int reg_cap = -1;
+            for (int i = 0; i < kNumNP; ++i)
+                if (kNPList[i] <= max_np(p->f16) && threads <= max_threads_for(kNPList[i], p->f16)) reg_cap = kNPList[i];
+            if (reg_cap < 0) continue;
+            if (std::getenv("SRNN_FORCE_SMEM_TIER") != nullptr) reg_cap = kNPList[0];  // test hook
+            // shared-memory tier budget (slots per lane) after hs/zs/b'/c
+            const int64_t ns_cap =
+                (static_cast<int64_t>(p->smem_optin) - static_cast<int64_t>(smem_base) - 16) / (threads * pair_bytes);
             const int np0 = std::max(1, min_np(in, L));
-            if (np0 > max_np(p->f16)) continue;
-            const int np_hi = in.naive ? np0 : std::min(max_np(p->f16), np0 + std::max(2, np0 / 4));
+            if (np0 > reg_cap + ns_cap) continue;
+            const int np_hi = in.naive ? np0 : np0 + std::max(2, np0 / 4);
             for (int np = np0; np <= np_hi; ++np) {
-                const int inst = inst_for(np, p->f16);
-                if (inst < 0 || threads > max_threads_for(inst, p->f16)) break;
                 Layout lay;
                 if (!pack_layout(in, C, L, np, &lay)) continue;
-                const int inst_used = inst_for(std::max(1, lay.slots_used), p->f16);
-                if (inst_used < 0 || lay.threads > max_threads_for(inst_used, p->f16)) continue;
-                const double cst = cost_model(lay, p->BT, H, p->n_tiles_max, p->f16);
+                const int su = std::max(1, lay.slots_used);
+                int inst = inst_for(su, p->f16);
+                int ns = 0;
+                if (inst < 0 || inst > reg_cap) {  // registers + shared-memory tier
+                    inst = reg_cap;
+                    ns = ((su - reg_cap) + 3) & ~3;
+                    if (ns > ns_cap) continue;
+                }
+                double cst = cost_model(lay, p->BT, H, p->n_tiles_max, p->f16);
+                if (ns > 0) cst += static_cast<double>(ns) * lay.warps * 2.0;  // weight LDS + issue per smem slot
                 if (cst < best_cost) {
                     best_cost = cst;
                     best = std::move(lay);
-                    best_inst = inst_used;
+                    best_inst = inst;
+                    best_ns = ns;
                     any = true;
                 }
             }
@@ -387,14 +406,15 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
     {
         // pack with the same budget, then widen the image to np_inst slots (padding)
         fin = best;
-        if (best.np_budget != best_inst) {
+        const int width = best_inst + best_ns;
+        if (best.np_budget != width) {
             Layout w = best;
-            w.np_budget = best_inst;
-            const size_t n = static_cast<size_t>(w.num_ctas) * best_inst * w.threads;
+            w.np_budget = width;
+            const size_t n = static_cast<size_t>(w.num_ctas) * width * w.threads;
             w.col.assign(n, 0);
             w.val.assign(n, 0.0f);
             w.row.assign(n, -1);
-            const int nslot = std::min(best.np_budget, best_inst);
+            const int nslot = std::min(best.np_budget, width);
             for (int c = 0; c < w.num_ctas; ++c)
                 for (int i = 0; i < nslot; ++i)
                     for (int t = 0; t < w.threads; ++t) {
@@ -407,8 +427,10 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
     }
     int umax = 0;
     for (int c = 0; c < fin.num_ctas; ++c) umax = std::max(umax, fin.cta_unit0[c + 1] - fin.cta_unit0[c]);
-    p->smem_bytes = smem_for(p, umax, p->BT, p->n_tiles_max);
+    p->smem_bytes = smem_for(p, umax, p->BT, p->n_tiles_max) + 16 +
+                    static_cast<size_t>(best_ns) * fin.threads * pair_bytes;
     p->np_inst = best_inst;
+    p->ns_slots = best_ns;
     p->lay = std::move(fin);
     p->nnz = nnz;
     p->regs = (p->f16 ? 1 : 2) * best_inst + 60;  // host-only estimate; replaced by the compiled count below
@@ -416,7 +438,7 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
     if (!p->host_only) {
         DeviceGuard g(p->cfg.device);
         const Layout& l = p->lay;
-        const size_t n = static_cast<size_t>(l.num_ctas) * p->np_inst * l.threads;
+        const size_t n = static_cast<size_t>(l.num_ctas) * (p->np_inst + p->ns_slots) * l.threads;
         cudaFree(p->d_img);
         cudaFree(p->d_unit0);
         cudaFree(p->d_wslots);
@@ -548,6 +570,7 @@ srnn_status_t srnn_recurrence(srnn_plan_t p, int32_t T, int32_t B, const float* 
     rp.threads = p->lay.threads;
     rp.lanes_per_row = p->lay.lanes_per_row;
     rp.np_inst = p->np_inst;
+    rp.smem_slots = p->ns_slots;
     int umax = 0;
     for (int c = 0; c < p->lay.num_ctas; ++c) umax = std::max(umax, p->lay.cta_unit0[c + 1] - p->lay.cta_unit0[c]);
     rp.units_max = umax;

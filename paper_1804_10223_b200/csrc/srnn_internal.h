@@ -21,7 +21,8 @@ struct RecParams {
     int32_t act;      // srnn_act_t (RNN only)
     int32_t threads;  // threads per CTA
     int32_t lanes_per_row;  // L
-    int32_t np_inst;  // slots per lane in the image (= template NP)
+    int32_t np_inst;  // register slots per lane (= template NP)
+    int32_t smem_slots;  // shared-memory tier slots per lane (multiple of 4; image width = NP + smem_slots)
     int32_t units_max;      // max units of any CTA (smem sizing)
     uint32_t epoch;   // tag of h_0 for this call; h_s carries epoch + s
     uint32_t flags;   // SRNN_FLAG_* subset relevant on device
@@ -71,7 +72,7 @@ constexpr int kNPList[kNumNP] = {4, 8, 12, 16, 24, 32, 48, 64, 96};
 inline int max_np(bool f16) { return f16 ? 96 : 64; }
 // Must match MaxThreads<NP, F16> in srnn_recurrent.cuh.
 inline int max_threads_for(int np, bool f16) {
-    if (f16) return np <= 12 ? 640 : np <= 32 ? 512 : np <= 48 ? 384 : 256;
+    if (f16) return np <= 12 ? 640 : np <= 32 ? 512 : np <= 64 ? 384 : 256;
     return np <= 4 ? 768 : np <= 12 ? 640 : np <= 32 ? 512 : np <= 48 ? 384 : 256;
 }
 

@@ -272,6 +272,73 @@ struct Weights<NP, BT, true> {
     }
 };
 
+// Shared-memory weight tier (capacity planner): slots
+// [NP, n_w) of a lane live in shared memory as [slot][thread] words (a
+// conflict-free LDS.32/.64 per slot) instead of registers; the gather and the
+// FMAs are the same as for register slots.  Used only when a layer's pairs do
+// not fit the register file ("larger layer sizes").
+template <int BT, bool F16>
+__device__ __forceinline__ void operate_smem_tier(float (&acc)[BT], const unsigned char* hs, const void* ws,
+                                                  int np_reg, int n_w, int nt) {
+    for (int i0 = np_reg; i0 < n_w; i0 += 4) {
+        if (F16) {
+            const uint32_t* w32 = static_cast<const uint32_t*>(ws) + static_cast<size_t>(i0 - np_reg) * nt + threadIdx.x;
+            uint32_t wv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) wv[j] = w32[j * nt];
+            if (BT == 4) {
+                uint2 h[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) h[j] = *reinterpret_cast<const uint2*>(hs + (wv[j] >> 16));
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    acc[0] = fma_f16f16f32(wv[j], h[j].x, acc[0]);
+                    acc[1 % BT] = fma_f16f16f32(wv[j], h[j].x >> 16, acc[1 % BT]);
+                    acc[2 % BT] = fma_f16f16f32(wv[j], h[j].y, acc[2 % BT]);
+                    acc[3 % BT] = fma_f16f16f32(wv[j], h[j].y >> 16, acc[3 % BT]);
+                }
+            } else if (BT == 2) {
+                uint32_t h[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) h[j] = *reinterpret_cast<const uint32_t*>(hs + (wv[j] >> 16));
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    acc[0] = fma_f16f16f32(wv[j], h[j], acc[0]);
+                    acc[1 % BT] = fma_f16f16f32(wv[j], h[j] >> 16, acc[1 % BT]);
+                }
+            } else {
+                uint32_t h[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) h[j] = *reinterpret_cast<const unsigned short*>(hs + (wv[j] >> 16));
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[0] = fma_f16f16f32(wv[j], h[j], acc[0]);
+            }
+        } else {
+            const uint2* w64 = static_cast<const uint2*>(ws) + static_cast<size_t>(i0 - np_reg) * nt + threadIdx.x;
+            uint2 wv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) wv[j] = w64[j * nt];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float w = __uint_as_float(wv[j].y);
+                if (BT == 4) {
+                    const float4 h = *reinterpret_cast<const float4*>(hs + wv[j].x);
+                    acc[0] = fmaf(w, h.x, acc[0]);
+                    acc[1 % BT] = fmaf(w, h.y, acc[1 % BT]);
+                    acc[2 % BT] = fmaf(w, h.z, acc[2 % BT]);
+                    acc[3 % BT] = fmaf(w, h.w, acc[3 % BT]);
+                } else if (BT == 2) {
+                    const float2 h = *reinterpret_cast<const float2*>(hs + wv[j].x);
+                    acc[0] = fmaf(w, h.x, acc[0]);
+                    acc[1 % BT] = fmaf(w, h.y, acc[1 % BT]);
+                } else {
+                    acc[0] = fmaf(w, *reinterpret_cast<const float*>(hs + wv[j].x), acc[0]);
+                }
+            }
+        }
+    }
+}
+
 // Max threads per CTA of each instance.  The register file is split over
 // the 4 SM sub-partitions (16K registers each), so with W warps a thread may
 // hold at most 512 / ceil(W/4) registers: 256 threads -> 255, 384 -> 168,
@@ -279,7 +346,7 @@ struct Weights<NP, BT, true> {
 // count whose budget still holds its register-resident pairs.
 template <int NP, bool F16>
 struct MaxThreads {
-    static constexpr int value = F16 ? (NP <= 12 ? 640 : NP <= 32 ? 512 : NP <= 48 ? 384 : 256)
+    static constexpr int value = F16 ? (NP <= 12 ? 640 : NP <= 32 ? 512 : NP <= 64 ? 384 : 256)
                                      : (NP <= 4 ? 768 : NP <= 12 ? 640 : NP <= 32 ? 512 : NP <= 48 ? 384 : 256);
 };
 template <int NP, bool F16>
@@ -315,6 +382,8 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     float* bps = zs + G * umax_bt;                           // b'_s of this tile: [item][G]
     float* cs = bps + G * umax_bt;                           // LSTM c: [n_tiles][item]
     int* s_abort = reinterpret_cast<int*>(cs + (G == 4 ? p.n_tiles * umax_bt : 0));
+    unsigned char* ws = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(s_abort + 1) + 15) & ~static_cast<uintptr_t>(15));  // smem weight tier
 
     const int L = p.lanes_per_row;
     const int n_w = p.warp_slots[cta * (p.threads >> 5) + warp];
@@ -324,7 +393,19 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
 
     // ---- prologue: weights HBM -> registers (once per forward) ----
     Weights<NP, BT, F16> W;
-    W.load(p, static_cast<size_t>(cta) * NP * p.threads + tid, n_w);
+    const int ns = p.smem_slots;  // shared-memory tier slots per lane (multiple of 4)
+    const size_t img_cta = static_cast<size_t>(cta) * (NP + ns) * p.threads;
+    W.load(p, img_cta + tid, n_w);
+    if (ns > 0) {
+        const size_t n = static_cast<size_t>(ns) * p.threads;
+        if (F16) {
+            const uint32_t* src = p.img_f16 + img_cta + static_cast<size_t>(NP) * p.threads;
+            for (size_t i = tid; i < n; i += nt) reinterpret_cast<uint32_t*>(ws)[i] = src[i];
+        } else {
+            const uint2* src = p.img_f32 + img_cta + static_cast<size_t>(NP) * p.threads;
+            for (size_t i = tid; i < n; i += nt) reinterpret_cast<uint2*>(ws)[i] = src[i];
+        }
+    }
 
     const int krow = warp * (32 / L) + lane / L;  // local row of this lane
     const bool row_leader = (lane % L) == 0 && krow < G * U;
@@ -404,6 +485,7 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
 #pragma unroll
                 for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
                 W.operate(acc, hs, n_w);
+                if (n_w > NP) operate_smem_tier<BT, F16>(acc, hs, ws, NP, n_w, nt);
                 for (int m = L >> 1; m >= 1; m >>= 1) {
 #pragma unroll
                     for (int b = 0; b < BT; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], m);

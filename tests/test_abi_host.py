@@ -81,10 +81,10 @@ def test_packer_reconstructs_matrix_exactly(H, B, d, cell, pattern, naive):
     assert cnt.max() <= 1 and cnt.sum() == prob["nnz"]
     inf = m.info()
     assert inf["nnz"] == prob["nnz"]
-    assert 0 < inf["slots_used"] <= inf["pairs_per_lane"]
+    assert 0 < inf["slots_used"] <= inf["image_slots_per_lane"]
     # lanes of one row are L consecutive lanes carrying the same row id
     L = inf["lanes_per_row"]
-    r = row.reshape(inf["num_ctas"], inf["pairs_per_lane"], -1, L)
+    r = row.reshape(inf["num_ctas"], inf["image_slots_per_lane"], -1, L)
     assert (r == r[..., :1]).all()
     # padding slots read a valid column (any in-range index, R6)
     assert col.min() >= 0 and col.max() < H

@@ -241,3 +241,23 @@ def test_batch_partition_bit_identical(cuda_device, world):
         parts.append(y)
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(parts, 1), y_full)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp16"])
+@pytest.mark.parametrize("cell,B", [("rnn", 1), ("rnn", 4), ("rnn", 6), ("lstm", 2)])
+def test_smem_weight_tier_forced(cuda_device, monkeypatch, prec, cell, B):
+    """Shared-memory weight tier (a10), forced on a small layer: pairs beyond 4
+    register slots per lane live in shared memory."""
+    monkeypatch.setenv("SRNN_FORCE_SMEM_TIER", "1")
+    prob = inputs.make_problem(300, 64, B, 9, 0.15, cell=cell, act="tanh", h0="random")
+    g, o, err = check(prob, prec)
+    assert g["info"]["smem_weight_bytes_per_cta"] > 0 and g["info"]["pairs_per_lane"] == 4
+
+
+@pytest.mark.parametrize("H,d", [(13445, 0.02), (27648, 0.005)])
+def test_capacity_large_hidden_on_chip(cuda_device, H, d):
+    """a10 / SURVEY d-iv: 5x the largest dense layer this library fits (H_dense = 2689
+    at density 1, scripts/capacity.py) still runs fully on chip -- every output checked."""
+    prob = inputs.make_problem(H, 64, 1, 6, d, act="tanh", h0="random")
+    g, o, err = check(prob, "fp16")
+    print(H, d, g["info"])
