@@ -5,7 +5,7 @@ mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem,power.draw,temperature.gpu,clocks_event_reasons.active --format=csv > gpurun_out/smi.txt
 nvidia-smi --query-gpu=clocks.sm,power.draw,clocks_event_reasons.active --format=csv,noheader -lms 500 > gpurun_out/clk.txt &
 SMI=$!
-if [ -z "$NOTEST" ]; then timeout 1200 python -m pytest tests -m gpu -q -x ${TESTSEL:-} > gpurun_out/gpu_tests.log 2>&1; echo tests=$?; fi
+if [ -z "$NOTEST" ]; then if [ -n "$TESTK" ]; then timeout 1200 python -m pytest tests -m gpu -q -x -k "$TESTK" > gpurun_out/gpu_tests.log 2>&1; else timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/gpu_tests.log 2>&1; fi; echo tests=$?; fi
 rm -f gpurun_out/qt.log
 IFS=';' read -ra VARS <<< "${QT:-;--L 32;--L 16;--d 0;--d 0 --flags 1;--flags 1;--prec fp32}"
 for args in "${VARS[@]}"; do
