@@ -250,7 +250,7 @@ def test_smem_weight_tier_forced(cuda_device, monkeypatch, prec, cell, B):
     register slots per lane live in shared memory."""
     monkeypatch.setenv("SRNN_FORCE_SMEM_TIER", "1")
     prob = inputs.make_problem(300, 64, B, 9, 0.15, cell=cell, act="tanh", h0="random")
-    g, o, err = check(prob, prec)
+    g, o, err = check(prob, prec, lanes_per_row=1)
     assert g["info"]["smem_weight_bytes_per_cta"] > 0 and g["info"]["pairs_per_lane"] == 4
 
 
