@@ -357,47 +357,71 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
     int best_inst = 0, best_ns = 0;
     bool any = false;
     const int pair_bytes = p->f16 ? 4 : 8;
+    const int P = p->E >= 4 ? 128 / p->E : 32;  // lanes per shared-memory phase
+    // Evaluate one (CTAs, lanes per row, slot budget) candidate.
+    auto try_layout = [&](int C, int L, int np, int reg_cap, int64_t ns_cap) {
+        Layout lay;
+        if (!pack_layout(in, C, L, np, &lay)) return;
+        const int su = std::max(1, lay.slots_used);
+        int inst = inst_for(su, p->f16);
+        int ns = 0;
+        if (inst < 0 || inst > reg_cap) {  // registers + shared-memory tier
+            inst = reg_cap;
+            ns = ((su - reg_cap) + 3) & ~3;
+            if (ns > ns_cap) return;
+        }
+        double cst = cost_model(lay, p->BT, H, p->n_tiles_max, p->f16);
+        if (ns > 0) cst += static_cast<double>(ns) * lay.warps * 2.0;  // weight LDS + issue per smem slot
+        if (cst < best_cost) {
+            best_cost = cst;
+            best = std::move(lay);
+            best_inst = inst;
+            best_ns = ns;
+            any = true;
+        }
+    };
+    struct Cand { int C, L, np0, reg_cap; int64_t ns_cap; };
+    std::vector<Cand> feasible;
+    // phase 1: the minimum slot budget of every (CTAs, lanes per row)
     for (int C : cands_c) {
         const int umax = (H + C - 1) / C;
         const size_t smem_base = smem_for(p, umax, p->BT, p->n_tiles_max);
         if (smem_base > static_cast<size_t>(p->smem_optin)) continue;
+        // lower bound: ideal wavefronts of the busiest CTA (every phase full, no conflicts)
+        int64_t pairs_max = 0;
+        for (int c = 0; c < C; ++c) {
+            const int ua = static_cast<int>((static_cast<int64_t>(c) * H) / C);
+            const int ub = static_cast<int>((static_cast<int64_t>(c + 1) * H) / C);
+            int64_t pc = 0;
+            for (int g = 0; g < G; ++g) pc += rowptr[g * H + ub] - rowptr[g * H + ua];
+            pairs_max = std::max(pairs_max, pc);
+        }
+        if (any && static_cast<double>(pairs_max) / P * p->n_tiles_max > best_cost) continue;
         for (int L : cands_l) {
             const int rows_max = G * umax;
             const int threads = ((rows_max * L + 31) / 32) * 32;
             if (threads > 1024) continue;
-            // largest register instance whose thread cap admits this CTA size
-            int reg_cap = -1;
+            int reg_cap = -1;  // largest register instance whose thread cap admits this CTA size
             for (int i = 0; i < kNumNP; ++i)
                 if (kNPList[i] <= max_np(p->f16) && threads <= max_threads_for(kNPList[i], p->f16)) reg_cap = kNPList[i];
             if (reg_cap < 0) continue;
             if (std::getenv("SRNN_FORCE_SMEM_TIER") != nullptr) reg_cap = kNPList[0];  // test hook
-            // shared-memory tier budget (slots per lane) after hs/zs/b'/c
             const int64_t ns_cap =
                 (static_cast<int64_t>(p->smem_optin) - static_cast<int64_t>(smem_base) - 16) / (threads * pair_bytes);
             const int np0 = std::max(1, min_np(in, L));
             if (np0 > reg_cap + ns_cap) continue;
-            const int np_hi = in.naive ? np0 : np0 + std::max(2, np0 / 4);
-            for (int np = np0; np <= np_hi; ++np) {
-                Layout lay;
-                if (!pack_layout(in, C, L, np, &lay)) continue;
-                const int su = std::max(1, lay.slots_used);
-                int inst = inst_for(su, p->f16);
-                int ns = 0;
-                if (inst < 0 || inst > reg_cap) {  // registers + shared-memory tier
-                    inst = reg_cap;
-                    ns = ((su - reg_cap) + 3) & ~3;
-                    if (ns > ns_cap) continue;
-                }
-                double cst = cost_model(lay, p->BT, H, p->n_tiles_max, p->f16);
-                if (ns > 0) cst += static_cast<double>(ns) * lay.warps * 2.0;  // weight LDS + issue per smem slot
-                if (cst < best_cost) {
-                    best_cost = cst;
-                    best = std::move(lay);
-                    best_inst = inst;
-                    best_ns = ns;
-                    any = true;
-                }
-            }
+            if (any && np0 * 11.0 * p->n_tiles_max > best_cost) continue;  // dependent slot chain bound
+            feasible.push_back({C, L, np0, reg_cap, ns_cap});
+            try_layout(C, L, np0, reg_cap, ns_cap);
+        }
+    }
+    // phase 2: looser slot budgets (bank-aware slack) for the best (CTAs, lanes per row)
+    if (any && !in.naive) {
+        const int bc = best.num_ctas, bl = best.lanes_per_row;
+        for (const Cand& f : feasible) {
+            if (f.C != bc || f.L != bl) continue;
+            for (int extra : {1, 2, 4, std::max(1, f.np0 / 8), std::max(2, f.np0 / 4)})
+                try_layout(f.C, f.L, f.np0 + extra, f.reg_cap, f.ns_cap);
         }
     }
     if (!any) return SRNN_ERR_NOT_ON_CHIP;
