@@ -199,8 +199,10 @@ srnn_status_t srnn_plan_export_layout(srnn_plan_t plan, int32_t *col_out, float 
                                       int32_t *row_out, int64_t capacity);
 
 /* Debug: with SRNN_FLAG_PROFILE, copy the clock64 stamps of the last forward
- * to host `out` as [num_ctas][T][num_tiles][4] int64: step start, h staged,
- * operate+reduce done, h published (SM cycle counter of that CTA's SM).
+ * to host `out` as [num_ctas][T][num_tiles][8] int64 (SM cycle counter of
+ * that CTA's SM, thread 0): 0 step start, 1 h staged (after the barrier),
+ * 2 after the second barrier, 3 h published, 4 operate loop done, 5 butterfly
+ * done, 6 b' copies landed; 7 unused.
  * `capacity` in elements; returns the element count via *count.
  * Errors: SRNN_ERR_STATE without the flag or before a forward. */
 srnn_status_t srnn_plan_debug_timeline(srnn_plan_t plan, int64_t *out, int64_t capacity, int64_t *count);

@@ -616,7 +616,7 @@ srnn_status_t srnn_recurrence(srnn_plan_t p, int32_t T, int32_t B, const float* 
     rp.status = p->d_status;
     rp.timeout_ns = p->timeout_ns;
     if (p->cfg.flags & SRNN_FLAG_PROFILE) {
-        const int64_t need = static_cast<int64_t>(p->lay.num_ctas) * T * rp.n_tiles * 4;
+        const int64_t need = static_cast<int64_t>(p->lay.num_ctas) * T * rp.n_tiles * 8;
         if (need > p->prof_elems) {
             cudaFree(p->d_prof);
             p->d_prof = nullptr;

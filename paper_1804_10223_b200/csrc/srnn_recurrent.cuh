@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     for (int s = 1; s <= p.T; ++s) {
         for (int k = 0; k < p.n_tiles; ++k) {
             long long* prof = (p.flags & kFlagProfile) && p.profile != nullptr && tid == 0
-                                  ? p.profile + ((static_cast<size_t>(cta) * p.T + (s - 1)) * p.n_tiles + k) * 4
+                                  ? p.profile + ((static_cast<size_t>(cta) * p.T + (s - 1)) * p.n_tiles + k) * 8
                                   : nullptr;
             if (prof) prof[0] = clock64();
             // b'_s of this tile -> shared memory, asynchronously (in flight while we spin)
@@ -486,16 +486,19 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                 for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
                 W.operate(acc, hs, n_w);
                 if (n_w > NP) operate_smem_tier<BT, F16>(acc, hs, ws, NP, n_w, nt);
+                if (prof) prof[4] = clock64();
                 for (int m = L >> 1; m >= 1; m >>= 1) {
 #pragma unroll
                     for (int b = 0; b < BT; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], m);
                 }
+                if (prof) prof[5] = clock64();
                 if (row_leader) {
 #pragma unroll
                     for (int b = 0; b < BT; ++b) zs[krow * BT + b] = acc[b];
                 }
             }
             cp_async_wait_all();
+            if (prof) prof[6] = clock64();
             __syncthreads();
             if (prof) prof[2] = clock64();
 

@@ -36,18 +36,23 @@ for _ in range(3):
 torch.cuda.synchronize()
 m.status()
 inf = m.info()
-tl = m.debug_timeline().reshape(inf["num_ctas"], a.T, -1, 4)
+tl = m.debug_timeline().reshape(inf["num_ctas"], a.T, -1, 8)
 nt = tl.shape[2]
-flat = tl.reshape(inf["num_ctas"], a.T * nt, 4).astype(np.float64)
+flat = tl.reshape(inf["num_ctas"], a.T * nt, 8).astype(np.float64)
 load = flat[:, :, 1] - flat[:, :, 0]
 oper = flat[:, :, 2] - flat[:, :, 1]
+op_loop = flat[:, :, 4] - flat[:, :, 1]
+butterfly = flat[:, :, 5] - flat[:, :, 4]
+bwait = flat[:, :, 6] - flat[:, :, 5]
+bar2 = flat[:, :, 2] - flat[:, :, 6]
 epi = flat[:, :, 3] - flat[:, :, 2]
 gap = flat[:, 1:, 0] - flat[:, :-1, 3]
 period = flat[:, 1:, 0] - flat[:, :-1, 0]
 sk = 8 * nt
 res = {"cfg": vars(a), "plan": {k: inf[k] for k in ("num_ctas", "threads_per_cta", "lanes_per_row", "pairs_per_lane",
                                                      "slots_used", "batch_tile", "wavefronts_per_step_max")}}
-for name, v in (("load", load[:, sk:]), ("operate", oper[:, sk:]), ("epilogue", epi[:, sk:]), ("gap", gap[:, sk:]),
+for name, v in (("load", load[:, sk:]), ("operate", oper[:, sk:]), ("op_loop", op_loop[:, sk:]),
+                ("butterfly", butterfly[:, sk:]), ("bprime_wait", bwait[:, sk:]), ("barrier2", bar2[:, sk:]), ("epilogue", epi[:, sk:]), ("gap", gap[:, sk:]),
                 ("tile_period", period[:, sk:])):
     res[name] = {"median": float(np.median(v)), "p10": float(np.percentile(v, 10)), "p90": float(np.percentile(v, 90))}
 print(json.dumps(res))
