@@ -203,8 +203,14 @@ __device__ __forceinline__ float fma_f16f16f32(uint32_t a_lo_half, uint32_t b_ha
 template <int NP, int BT, bool F16>
 struct Weights;
 
+// The operate loop runs in groups of GS slots: all GS shared-memory loads of
+// a group are issued before its FMAs (memory-level parallelism), and the
+// warp-uniform slot count n_w is checked once per group.  Slots between n_w
+// and the end of a group hold zero weights reading column 0 (a broadcast),
+// exactly like the paper's <index, 0> padding pairs.
 template <int NP, int BT>
 struct Weights<NP, BT, false> {
+    static constexpr int GS = BT == 4 ? 4 : 8;
     uint32_t off[NP];
     float w[NP];
     __device__ __forceinline__ void load(const RecParams& p, size_t img0, int n_w) {
@@ -221,20 +227,43 @@ struct Weights<NP, BT, false> {
     }
     __device__ __forceinline__ void operate(float (&acc)[BT], const unsigned char* hs, int n_w) const {
 #pragma unroll
-        for (int i = 0; i < NP; ++i) {
-            if (i < n_w) {
+        for (int i0 = 0; i0 < NP; i0 += GS) {
+            if (i0 < n_w) {
                 if (BT == 4) {
-                    const float4 h = *reinterpret_cast<const float4*>(hs + off[i]);
-                    acc[0] = fmaf(w[i], h.x, acc[0]);
-                    acc[1 % BT] = fmaf(w[i], h.y, acc[1 % BT]);
-                    acc[2 % BT] = fmaf(w[i], h.z, acc[2 % BT]);
-                    acc[3 % BT] = fmaf(w[i], h.w, acc[3 % BT]);
+                    float4 h[GS];
+#pragma unroll
+                    for (int j = 0; j < GS; ++j)
+                        if (i0 + j < NP) h[j] = *reinterpret_cast<const float4*>(hs + off[i0 + j]);
+#pragma unroll
+                    for (int j = 0; j < GS; ++j) {
+                        if (i0 + j < NP) {
+                            const float wv = w[i0 + j];
+                            acc[0] = fmaf(wv, h[j].x, acc[0]);
+                            acc[1 % BT] = fmaf(wv, h[j].y, acc[1 % BT]);
+                            acc[2 % BT] = fmaf(wv, h[j].z, acc[2 % BT]);
+                            acc[3 % BT] = fmaf(wv, h[j].w, acc[3 % BT]);
+                        }
+                    }
                 } else if (BT == 2) {
-                    const float2 h = *reinterpret_cast<const float2*>(hs + off[i]);
-                    acc[0] = fmaf(w[i], h.x, acc[0]);
-                    acc[1 % BT] = fmaf(w[i], h.y, acc[1 % BT]);
+                    float2 h[GS];
+#pragma unroll
+                    for (int j = 0; j < GS; ++j)
+                        if (i0 + j < NP) h[j] = *reinterpret_cast<const float2*>(hs + off[i0 + j]);
+#pragma unroll
+                    for (int j = 0; j < GS; ++j) {
+                        if (i0 + j < NP) {
+                            acc[0] = fmaf(w[i0 + j], h[j].x, acc[0]);
+                            acc[1 % BT] = fmaf(w[i0 + j], h[j].y, acc[1 % BT]);
+                        }
+                    }
                 } else {
-                    acc[0] = fmaf(w[i], *reinterpret_cast<const float*>(hs + off[i]), acc[0]);
+                    float h[GS];
+#pragma unroll
+                    for (int j = 0; j < GS; ++j)
+                        if (i0 + j < NP) h[j] = *reinterpret_cast<const float*>(hs + off[i0 + j]);
+#pragma unroll
+                    for (int j = 0; j < GS; ++j)
+                        if (i0 + j < NP) acc[0] = fmaf(w[i0 + j], h[j], acc[0]);
                 }
             }
         }
@@ -243,6 +272,7 @@ struct Weights<NP, BT, false> {
 
 template <int NP, int BT>
 struct Weights<NP, BT, true> {
+    static constexpr int GS = BT == 4 ? 4 : 8;
     uint32_t pw[NP];
     __device__ __forceinline__ void load(const RecParams& p, size_t img0, int n_w) {
 #pragma unroll
@@ -250,22 +280,43 @@ struct Weights<NP, BT, true> {
     }
     __device__ __forceinline__ void operate(float (&acc)[BT], const unsigned char* hs, int n_w) const {
 #pragma unroll
-        for (int i = 0; i < NP; ++i) {
-            if (i < n_w) {
-                const uint32_t o = pw[i] >> 16;
+        for (int i0 = 0; i0 < NP; i0 += GS) {
+            if (i0 < n_w) {
                 if (BT == 4) {
-                    const uint2 h = *reinterpret_cast<const uint2*>(hs + o);
-                    acc[0] = fma_f16f16f32(pw[i], h.x, acc[0]);
-                    acc[1 % BT] = fma_f16f16f32(pw[i], h.x >> 16, acc[1 % BT]);
-                    acc[2 % BT] = fma_f16f16f32(pw[i], h.y, acc[2 % BT]);
-                    acc[3 % BT] = fma_f16f16f32(pw[i], h.y >> 16, acc[3 % BT]);
+                    uint2 h[GS];
+#pragma unroll
+                    for (int j = 0; j < GS; ++j)
+                        if (i0 + j < NP) h[j] = *reinterpret_cast<const uint2*>(hs + (pw[i0 + j] >> 16));
+#pragma unroll
+                    for (int j = 0; j < GS; ++j) {
+                        if (i0 + j < NP) {
+                            const uint32_t wv = pw[i0 + j];
+                            acc[0] = fma_f16f16f32(wv, h[j].x, acc[0]);
+                            acc[1 % BT] = fma_f16f16f32(wv, h[j].x >> 16, acc[1 % BT]);
+                            acc[2 % BT] = fma_f16f16f32(wv, h[j].y, acc[2 % BT]);
+                            acc[3 % BT] = fma_f16f16f32(wv, h[j].y >> 16, acc[3 % BT]);
+                        }
+                    }
                 } else if (BT == 2) {
-                    const uint32_t h = *reinterpret_cast<const uint32_t*>(hs + o);
-                    acc[0] = fma_f16f16f32(pw[i], h, acc[0]);
-                    acc[1 % BT] = fma_f16f16f32(pw[i], h >> 16, acc[1 % BT]);
+                    uint32_t h[GS];
+#pragma unroll
+                    for (int j = 0; j < GS; ++j)
+                        if (i0 + j < NP) h[j] = *reinterpret_cast<const uint32_t*>(hs + (pw[i0 + j] >> 16));
+#pragma unroll
+                    for (int j = 0; j < GS; ++j) {
+                        if (i0 + j < NP) {
+                            acc[0] = fma_f16f16f32(pw[i0 + j], h[j], acc[0]);
+                            acc[1 % BT] = fma_f16f16f32(pw[i0 + j], h[j] >> 16, acc[1 % BT]);
+                        }
+                    }
                 } else {
-                    const uint32_t h = *reinterpret_cast<const unsigned short*>(hs + o);
-                    acc[0] = fma_f16f16f32(pw[i], h, acc[0]);
+                    uint32_t h[GS];
+#pragma unroll
+                    for (int j = 0; j < GS; ++j)
+                        if (i0 + j < NP) h[j] = *reinterpret_cast<const unsigned short*>(hs + (pw[i0 + j] >> 16));
+#pragma unroll
+                    for (int j = 0; j < GS; ++j)
+                        if (i0 + j < NP) acc[0] = fma_f16f16f32(pw[i0 + j], h[j], acc[0]);
                 }
             }
         }
@@ -487,9 +538,12 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                 W.operate(acc, hs, n_w);
                 if (n_w > NP) operate_smem_tier<BT, F16>(acc, hs, ws, NP, n_w, nt);
                 if (prof) prof[4] = clock64();
-                for (int m = L >> 1; m >= 1; m >>= 1) {
 #pragma unroll
-                    for (int b = 0; b < BT; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], m);
+                for (int m = 16; m >= 1; m >>= 1) {
+                    if (m < L) {  // warp-uniform
+#pragma unroll
+                        for (int b = 0; b < BT; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], m);
+                    }
                 }
                 if (prof) prof[5] = clock64();
                 if (row_leader) {
