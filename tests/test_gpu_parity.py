@@ -261,3 +261,32 @@ def test_capacity_large_hidden_on_chip(cuda_device, H, d):
     prob = inputs.make_problem(H, 64, 1, 6, d, act="tanh", h0="random")
     g, o, err = check(prob, "fp16")
     print(H, d, g["info"])
+
+
+def test_C5_shape_sampled_and_partition(cuda_device):
+    """C5 layer (H=5760, d=10%, B=64, fp16): the shared-memory weight tier and 16
+    batch tiles; samples 0 and 63 checked against the oracle (sampled outputs,
+    T shortened to 24 for the CPU side), and the 8-way batch partition of the
+    same plan is bit-identical to the full batch."""
+    import torch
+    from paper_1804_10223_b200.multigpu import shard
+    cfg = {k: v for k, v in inputs.CONFIGS["C5"].items() if k != "prec"}
+    cfg["T"] = 24
+    prob = inputs.make_problem(**cfg)
+    m = from_problem(prob, prec="fp16")
+    x = torch.from_numpy(prob["x"]).cuda()
+    y, _ = m.forward(x)
+    torch.cuda.synchronize()
+    m.status()
+    for b in (0, 63):
+        q = dict(prob)
+        q["x"] = prob["x"][:, b:b + 1]
+        q["B"] = 1
+        o = oracle.forward(q)
+        assert np.abs(y[:, b].cpu().numpy() - o["y"][:, 0]).max() <= TOL["fp16"]
+    parts = []
+    for r in range(8):
+        s0, c = shard(64, 8, r)
+        parts.append(m.forward(x[:, s0:s0 + c].contiguous())[0])
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts, 1), y)
