@@ -1,0 +1,122 @@
+"""C3 sweep (BASELINE.json configs[2]; the paper's Fig. 2/3 axes):
+hidden x density x batch at T = 256, our persistent kernel vs the per-step
+dense cuBLAS loop (CUDA graph) and the per-step cuSPARSE SpMM loop (eager),
+plus the largest on-chip points.  Writes one JSON line per point.
+
+usage: python scripts/sweep.py [--quick] > gpurun_out/sweep.jsonl
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_1804_10223_b200 import SrnnError, from_problem, inputs  # noqa: E402
+
+
+def t_events(fn, reps=5):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(reps):
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts)
+
+
+def dense_graph_us(H, B, T):
+    W = (torch.rand(H, H, device="cuda") - 0.5).half()
+    bp = torch.rand(T, H, B, device="cuda")
+    h = torch.zeros(H, B, device="cuda", dtype=torch.float16)
+    z = torch.empty(H, B, device="cuda", dtype=torch.float16)
+
+    def loop():
+        hh = h
+        for t in range(T):
+            torch.mm(W, hh, out=z)
+            hh = torch.relu(z.float() + bp[t]).half()
+    loop()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        loop()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        loop()
+    return 1000 * t_events(g.replay) / T
+
+
+def cusparse_us(prob, B, T):
+    H = prob["H"]
+    crow = torch.from_numpy(prob["rowptr"]).long()
+    col = torch.from_numpy(prob["col"]).long()
+    val = torch.from_numpy(prob["val"])
+    W = torch.sparse_csr_tensor(crow, col, val, (H, H)).cuda()
+    bp = torch.rand(T, H, B, device="cuda")
+    h = torch.zeros(H, B, device="cuda")
+
+    def loop():
+        hh = h
+        for t in range(T):
+            hh = torch.relu(torch.sparse.mm(W, hh) + bp[t])
+    loop()
+    return 1000 * t_events(loop, reps=3) / T
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    a = ap.parse_args()
+    T = 256
+    Hs = [1152, 1792, 2304, 4096, 5760] if not a.quick else [1792, 2304]
+    ds = [0.01, 0.05, 0.10, 0.30]
+    Bs = [1, 4, 16] if not a.quick else [4]
+    dense_cache = {}
+    for H in Hs:
+        for B in Bs:
+            for d in ds:
+                rec = {"H": H, "B": B, "density": d, "T": T}
+                try:
+                    t0 = time.time()
+                    prob = inputs.make_problem(H, H, B, T, d)
+                    m = from_problem(prob, prec="fp16")
+                    rec["plan_s"] = round(time.time() - t0, 2)
+                    x = torch.from_numpy(prob["x"]).cuda()
+                    bp = m.input_projection(x)
+                    y = torch.empty(T, B, H, device="cuda")
+                    m.recurrence(bp, y=y)
+                    torch.cuda.synchronize()
+                    ms = t_events(lambda: m.recurrence(bp, y=y))
+                    m.status()
+                    inf = m.info()
+                    rec["ours_us_per_step"] = 1000 * ms / T
+                    rec["ours_eff_gflops"] = 2 * prob["nnz"] * B * T / (ms * 1e-3) / 1e9
+                    rec["plan"] = {k: inf[k] for k in ("num_ctas", "threads_per_cta", "lanes_per_row", "pairs_per_lane",
+                                                       "image_slots_per_lane", "batch_tile", "num_batch_tiles")}
+                    m.close()
+                except SrnnError as e:
+                    rec["ours"] = f"not on chip / unsupported: {e}"
+                try:
+                    key = (H, B)
+                    if key not in dense_cache:
+                        dense_cache[key] = dense_graph_us(H, B, T)
+                    rec["cublas_dense_graph_us_per_step"] = dense_cache[key]
+                    rec["cusparse_us_per_step"] = cusparse_us(prob, B, T)
+                except Exception as e:  # noqa: BLE001
+                    rec["baseline_error"] = str(e)[:200]
+                if "ours_us_per_step" in rec and "cublas_dense_graph_us_per_step" in rec:
+                    rec["speedup_vs_dense_graph"] = rec["cublas_dense_graph_us_per_step"] / rec["ours_us_per_step"]
+                    if "cusparse_us_per_step" in rec:
+                        rec["speedup_vs_cusparse"] = rec["cusparse_us_per_step"] / rec["ours_us_per_step"]
+                print(json.dumps(rec), flush=True)
+
+
+if __name__ == "__main__":
+    main()
