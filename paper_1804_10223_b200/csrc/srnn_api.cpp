@@ -147,7 +147,7 @@ double cost_model(const Layout& lay, int bt, int H, int n_tiles, bool f16) {
     int lg = 0;
     while ((1 << lg) < lay.lanes_per_row) ++lg;
     const double reduce = lg * (30.0 + 2.0 * bt);
-    const double words_per_unit = f16 ? (bt == 4 ? 2.0 : 1.0) : bt;
+    const double words_per_unit = f16 ? (bt >= 2 ? bt / 2.0 : 1.0) : bt;
     const double chunks = static_cast<double>(H) * words_per_unit / 2.0;
     const double k = f16 ? 8.0 : 4.0;
     const double groups = std::ceil(chunks / (lay.threads * k));
@@ -192,7 +192,8 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
         (c.lanes_per_row < 1 || c.lanes_per_row > 32 || (c.lanes_per_row & (c.lanes_per_row - 1)) != 0))
         return SRNN_ERR_INVALID_VALUE;
     if (c.num_ctas < 0) return SRNN_ERR_INVALID_VALUE;
-    if (c.batch_tile != 0 && c.batch_tile != 1 && c.batch_tile != 2 && c.batch_tile != 4) return SRNN_ERR_INVALID_VALUE;
+    if (c.batch_tile != 0 && c.batch_tile != 1 && c.batch_tile != 2 && c.batch_tile != 4 && c.batch_tile != 8)
+        return SRNN_ERR_INVALID_VALUE;
 
     srnn_plan* p = new (std::nothrow) srnn_plan();
     if (!p) return SRNN_ERR_INVALID_VALUE;
@@ -225,10 +226,12 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     p->f16 = c.prec == SRNN_PREC_FP16W_FP32ACC && (c.flags & SRNN_FLAG_FP32_STAGING) == 0;
     // Batch tile: the paper's wide load interleaves 4 samples.
     int bt = c.batch >= 4 ? 4 : (c.batch >= 2 ? 2 : 1);
-    if (c.batch_tile == 1 || c.batch_tile == 2 || c.batch_tile == 4) bt = c.batch_tile;
+    if (p->f16 && c.batch >= 8) bt = 8;  // fp16: 8 samples per LDS.128 (one exchange round for B = 8)
+    if (c.batch_tile == 1 || c.batch_tile == 2 || c.batch_tile == 4 || (c.batch_tile == 8 && p->f16))
+        bt = c.batch_tile;
     if (const char* e = std::getenv("SRNN_BT")) {  // experiment override: batch tile width
         const int v = std::atoi(e);
-        if (v == 1 || v == 2 || v == 4) bt = v;
+        if (v == 1 || v == 2 || v == 4 || (v == 8 && p->f16)) bt = v;
     }
     while (bt > 1 && bt > c.batch) bt /= 2;
     // fp16 register pairs carry the hs byte offset in 16 bits: H * E <= 65536
@@ -249,14 +252,16 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     // Register budget for the expected pairs: two registers per pair in the
     // hoisted format, at most ~75% of each SM's 64K registers.
     const double exp_pairs = static_cast<double>(c.density) * p->G * c.hidden * static_cast<double>(c.hidden);
-    const double reg_capacity_pairs = 0.75 * 65536.0 * p->sm_count / (p->f16 ? 1.0 : 2.0);
+    // plus the shared-memory weight tier (up to ~60% of shared memory)
+    const double reg_capacity_pairs =
+        (0.75 * 65536.0 / (p->f16 ? 1.0 : 2.0) + 0.6 * p->smem_optin / (p->f16 ? 4.0 : 8.0)) * p->sm_count;
     if (exp_pairs > reg_capacity_pairs) {
         delete p;
         return SRNN_ERR_NOT_ON_CHIP;
     }
     if (!p->host_only) {
         DeviceGuard g(c.device);
-        const int wpr = p->f16 ? (bt == 4 ? 2 : 1) : bt;  // tagged words per unit
+        const int wpr = p->f16 ? (bt >= 2 ? bt / 2 : 1) : bt;  // tagged words per unit
         const size_t tile_stride = (static_cast<size_t>(c.hidden) * wpr + 1) & ~static_cast<size_t>(1);
         p->xbuf_words = 2 * static_cast<size_t>(p->n_tiles_max) * tile_stride;
         const size_t bp_elems = static_cast<size_t>(std::max(1, c.max_steps)) * c.batch * p->G * c.hidden;

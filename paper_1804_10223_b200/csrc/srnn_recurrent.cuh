@@ -109,7 +109,7 @@ __device__ __forceinline__ bool watchdog_tick(Watchdog& wd, int32_t* status, uns
 // ---------------------------------------------------------------------------
 template <bool F16, int BT>
 struct Fmt {
-    static constexpr int WPR = F16 ? (BT == 4 ? 2 : 1) : BT;   // words per unit
+    static constexpr int WPR = F16 ? (BT >= 2 ? BT / 2 : 1) : BT;  // words per unit
     static constexpr int E = F16 ? 2 * BT : 4 * BT;            // hs bytes per unit
     static constexpr int CHUNK_HS = (F16 && BT == 1) ? 4 : 8;  // hs bytes per 16-byte chunk
 
@@ -272,7 +272,7 @@ struct Weights<NP, BT, false> {
 
 template <int NP, int BT>
 struct Weights<NP, BT, true> {
-    static constexpr int GS = BT == 4 ? 4 : 8;
+    static constexpr int GS = BT >= 4 ? 4 : 8;
     uint32_t pw[NP];
     __device__ __forceinline__ void load(const RecParams& p, size_t img0, int n_w) {
 #pragma unroll
@@ -282,7 +282,26 @@ struct Weights<NP, BT, true> {
 #pragma unroll
         for (int i0 = 0; i0 < NP; i0 += GS) {
             if (i0 < n_w) {
-                if (BT == 4) {
+                if (BT == 8) {
+                    uint4 h[GS];
+#pragma unroll
+                    for (int j = 0; j < GS; ++j)
+                        if (i0 + j < NP) h[j] = *reinterpret_cast<const uint4*>(hs + (pw[i0 + j] >> 16));
+#pragma unroll
+                    for (int j = 0; j < GS; ++j) {
+                        if (i0 + j < NP) {
+                            const uint32_t wv = pw[i0 + j];
+                            acc[0] = fma_f16f16f32(wv, h[j].x, acc[0]);
+                            acc[1 % BT] = fma_f16f16f32(wv, h[j].x >> 16, acc[1 % BT]);
+                            acc[2 % BT] = fma_f16f16f32(wv, h[j].y, acc[2 % BT]);
+                            acc[3 % BT] = fma_f16f16f32(wv, h[j].y >> 16, acc[3 % BT]);
+                            acc[4 % BT] = fma_f16f16f32(wv, h[j].z, acc[4 % BT]);
+                            acc[5 % BT] = fma_f16f16f32(wv, h[j].z >> 16, acc[5 % BT]);
+                            acc[6 % BT] = fma_f16f16f32(wv, h[j].w, acc[6 % BT]);
+                            acc[7 % BT] = fma_f16f16f32(wv, h[j].w >> 16, acc[7 % BT]);
+                        }
+                    }
+                } else if (BT == 4) {
                     uint2 h[GS];
 #pragma unroll
                     for (int j = 0; j < GS; ++j)
@@ -337,7 +356,22 @@ __device__ __forceinline__ void operate_smem_tier(float (&acc)[BT], const unsign
             uint32_t wv[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) wv[j] = w32[j * nt];
-            if (BT == 4) {
+            if (BT == 8) {
+                uint4 h[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) h[j] = *reinterpret_cast<const uint4*>(hs + (wv[j] >> 16));
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    acc[0] = fma_f16f16f32(wv[j], h[j].x, acc[0]);
+                    acc[1 % BT] = fma_f16f16f32(wv[j], h[j].x >> 16, acc[1 % BT]);
+                    acc[2 % BT] = fma_f16f16f32(wv[j], h[j].y, acc[2 % BT]);
+                    acc[3 % BT] = fma_f16f16f32(wv[j], h[j].y >> 16, acc[3 % BT]);
+                    acc[4 % BT] = fma_f16f16f32(wv[j], h[j].z, acc[4 % BT]);
+                    acc[5 % BT] = fma_f16f16f32(wv[j], h[j].z >> 16, acc[5 % BT]);
+                    acc[6 % BT] = fma_f16f16f32(wv[j], h[j].w, acc[6 % BT]);
+                    acc[7 % BT] = fma_f16f16f32(wv[j], h[j].w >> 16, acc[7 % BT]);
+                }
+            } else if (BT == 4) {
                 uint2 h[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) h[j] = *reinterpret_cast<const uint2*>(hs + (wv[j] >> 16));
@@ -538,15 +572,42 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                 W.operate(acc, hs, n_w);
                 if (n_w > NP) operate_smem_tier<BT, F16>(acc, hs, ws, NP, n_w, nt);
                 if (prof) prof[4] = clock64();
+                // ---- reduce over the row's L lanes, fixed order ----
+                // L >= BT: log2(BT) halving levels (each lane keeps half of its
+                // samples and receives the partner's sums for them: BT-1
+                // shuffles instead of BT*log2(BT)), then plain levels; lane j of
+                // the row then holds the sum of sample bitrev(j mod BT).
+                // L < BT: plain xor butterfly, the row leader holds all samples.
+                int sbase = 0;
+                if (L >= BT) {
 #pragma unroll
-                for (int m = 16; m >= 1; m >>= 1) {
-                    if (m < L) {  // warp-uniform
+                    for (int lvl = 0, half = BT / 2; half >= 1; ++lvl, half /= 2) {
+                        const int m = 1 << lvl;
+                        const bool upper = (lane & m) != 0;
 #pragma unroll
-                        for (int b = 0; b < BT; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], m);
+                        for (int i = 0; i < half; ++i) {
+                            const float keep = upper ? acc[(i + half) % BT] : acc[i];
+                            const float send = upper ? acc[i] : acc[(i + half) % BT];
+                            acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                        }
+                        if (upper) sbase += half;
+                    }
+#pragma unroll
+                    for (int m = BT; m <= 16; m <<= 1)
+                        if (m < L) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], m);
+                } else {
+#pragma unroll
+                    for (int m = 16; m >= 1; m >>= 1) {
+                        if (m < L) {  // warp-uniform
+#pragma unroll
+                            for (int b = 0; b < BT; ++b) acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], m);
+                        }
                     }
                 }
                 if (prof) prof[5] = clock64();
-                if (row_leader) {
+                if (L >= BT) {
+                    if ((lane % L) < BT && krow < G * U) zs[krow * BT + sbase] = acc[0];
+                } else if (row_leader) {
 #pragma unroll
                     for (int b = 0; b < BT; ++b) zs[krow * BT + b] = acc[b];
                 }
@@ -633,6 +694,10 @@ int launch_np(int bt, int g, const RecParams& p, int num_ctas, size_t smem, void
     SRNN_CASE(1, 4)
     SRNN_CASE(2, 4)
     SRNN_CASE(4, 4)
+    if constexpr (F16) {
+        SRNN_CASE(8, 1)
+        SRNN_CASE(8, 4)
+    }
 #undef SRNN_CASE
     return static_cast<int>(cudaErrorInvalidValue);
 }

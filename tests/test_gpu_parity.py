@@ -54,6 +54,9 @@ def check(prob, prec, flags=0, **kw):
     (1152, 4, 24, 0.10, "relu"),     # Table 1 shape, short T
     (513, 6, 9, 0.02, "identity"),   # two batch tiles, ragged
     (64, 2, 30, 0.50, "tanh"),
+    (700, 8, 10, 0.05, "tanh"),      # fp16: one batch tile of 8 (LDS.128)
+    (333, 16, 7, 0.10, "relu"),      # two tiles of 8
+    (129, 13, 6, 0.20, "tanh"),      # ragged last tile
 ])
 def test_rnn_parity_small(cuda_device, prec, H, B, T, d, act):
     prob = inputs.make_problem(H, H, B, T, d, act=act, h0="random", seed_offset=H)
@@ -65,6 +68,7 @@ def test_rnn_parity_small(cuda_device, prec, H, B, T, d, act):
     (128, 4, 10, 0.125, "row_balanced"),
     (257, 1, 12, 0.12, "unstructured"),
     (96, 5, 7, 0.3, "unstructured"),
+    (200, 8, 6, 0.1, "row_balanced"),
 ])
 def test_lstm_parity_small(cuda_device, prec, H, B, T, d, pattern):
     prob = inputs.make_problem(H, H, B, T, d, cell="lstm", pattern=pattern, h0="random", c0="random",
@@ -118,10 +122,12 @@ def test_naive_layout_parity(cuda_device):
     check(prob, "fp32", flags=FLAG_NAIVE_LAYOUT)
 
 
-@pytest.mark.parametrize("prec", ["fp32", "fp16"])
+@pytest.mark.parametrize("prec,B", [("fp32", 4), ("fp16", 4), ("fp16", 8), ("fp32", 1), ("fp16", 2)])
 @pytest.mark.parametrize("L", [1, 2, 4, 8, 16, 32])
-def test_every_lane_mapping(cuda_device, L, prec):
-    prob = inputs.make_problem(512, 512, 4, 8, 0.05, act="tanh", h0="random")
+def test_every_lane_mapping(cuda_device, L, prec, B):
+    """Every lanes-per-row mapping x batch tile: the halving butterfly (L >= BT)
+    and the plain butterfly (L < BT) both reduce to the oracle."""
+    prob = inputs.make_problem(512, 512, B, 8, 0.05, act="tanh", h0="random")
     check(prob, prec, lanes_per_row=L)
 
 
