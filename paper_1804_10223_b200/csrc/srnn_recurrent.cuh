@@ -132,9 +132,11 @@ struct Fmt {
 };
 
 // Stage h_{s-1} (one batch tile) into shared memory.  Every thread owns up
-// to K 16-byte chunks per group; all of them are in flight at once, and
-// chunks whose tags are stale are re-polled together (one round trip per
-// round, not per chunk).  Tag mode spins; grid-sync mode checks once.
+// to K 16-byte chunks per group (chunk c = thread + j * blockDim); all of them
+// are in flight at once, and chunks whose tags are stale are re-polled
+// together (one round trip per round, not per chunk).  The producers always
+// write whole chunks (an odd word count gets a tagged pad word), so a chunk is
+// valid iff both tags match.  Tag mode spins; grid-sync mode checks once.
 template <bool F16, int BT, int K>
 __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, unsigned char* hs, int n_words,
                                           uint32_t want, bool spin, int32_t* status,
@@ -144,24 +146,22 @@ __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, un
     Watchdog wd{0ull, 0u};
     bool ok = true;
     for (int base = threadIdx.x; base < n_chunks; base += K * nt) {
+        const ulonglong2* ptr = src + base;
         ulonglong2 v[K];
         uint32_t pend = 0u;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-            const int idx = base + j * nt;
-            if (idx < n_chunks) {
-                v[j] = ld_relaxed_v2(src + idx);
+            if (base + j * nt < n_chunks) {
+                v[j] = ld_relaxed_v2(ptr + j * nt);
                 pend |= 1u << j;
             }
         }
         while (true) {
 #pragma unroll
             for (int j = 0; j < K; ++j) {
-                if (pend & (1u << j)) {
-                    const int idx = base + j * nt;
-                    const bool has1 = 2 * idx + 1 < n_words;
-                    if (tag_of(v[j].x) == want && (!has1 || tag_of(v[j].y) == want)) {
-                        Fmt<F16, BT>::store(hs, idx, v[j].x, v[j].y, has1);
+                if ((pend >> j) & 1u) {
+                    if ((tag_of(v[j].x) == want) & (tag_of(v[j].y) == want)) {
+                        Fmt<F16, BT>::store(hs, base + j * nt, v[j].x, v[j].y, true);
                         pend &= ~(1u << j);
                     }
                 }
@@ -177,7 +177,7 @@ __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, un
             }
 #pragma unroll
             for (int j = 0; j < K; ++j)
-                if (pend & (1u << j)) v[j] = ld_relaxed_v2(src + base + j * nt);
+                if ((pend >> j) & 1u) v[j] = ld_relaxed_v2(ptr + j * nt);
         }
         if (!ok) break;
     }
@@ -501,6 +501,8 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     auto publish = [&](int s, int k, int e, bool ok, float h) {
         unsigned long long* dst = p.xbuf + static_cast<size_t>((s & 1) * p.n_tiles + k) * tile_stride;
         const uint32_t tag = p.epoch + static_cast<uint32_t>(s);
+        if ((n_words & 1) && cta == 0 && e == 0)  // keep every 16-byte chunk whole: tagged pad word
+            st_relaxed_u64(dst + n_words, static_cast<unsigned long long>(tag) << 32);
         const int unit = u0 + e / BT, eb = e % BT;
         if (!F16) {
             if (ok) st_relaxed_u64(dst + unit * BT + eb, pack_tagged(h, tag));
