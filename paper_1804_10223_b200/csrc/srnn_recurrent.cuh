@@ -492,7 +492,6 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
         }
     }
 
-    const int act = p.act;
     const int krow = warp * (32 / L) + lane / L;  // local row of this lane
     const bool row_leader = (lane % L) == 0 && krow < G * U;
     if (tid == 0) *s_abort = 0;
@@ -543,17 +542,14 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                                   : nullptr;
             if (prof) prof[0] = clock64();
             // b'_s of this tile -> shared memory, asynchronously (in flight while we spin)
-            const size_t row0 = static_cast<size_t>(s - 1) * p.B + static_cast<size_t>(k) * BT;  // (step, first sample)
-            const float* bp_tile = p.bprime + row0 * GH + u0;
-            const int nb = min(BT, p.B - k * BT);  // real samples in this tile
             for (int j = 0; j < item_rounds; ++j) {
                 const int e = tid + j * nt;
                 if (e < n_items) {
-                    const int eu = e / BT, eb = e - (e / BT) * BT;
+                    const int unit = u0 + e / BT, bg = k * BT + e % BT;
 #pragma unroll
                     for (int q = 0; q < G; ++q) {
-                        if (eb < nb)
-                            cp_async_f32(&bps[e * G + q], bp_tile + eb * GH + q * H + eu);
+                        if (bg < p.B)
+                            cp_async_f32(&bps[e * G + q], p.bprime + (static_cast<size_t>(s - 1) * p.B + bg) * GH + q * H + unit);
                         else
                             bps[e * G + q] = 0.0f;
                     }
@@ -628,16 +624,14 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                 const uint32_t r = (static_cast<uint32_t>(cta) * 2654435761u) ^ (static_cast<uint32_t>(s * 40503 + k));
                 __nanosleep((r >> 7) & 2047u);
             }
-            float* y_tile = p.y != nullptr ? p.y + row0 * H + u0 : nullptr;
             for (int j = 0; j < item_rounds; ++j) {
                 const int e = tid + j * nt;
                 const bool ok = e < n_items;
                 float h = 0.0f;
                 if (ok) {
-                    const int eu = e / BT, eb = e - (e / BT) * BT;
-                    const int unit = u0 + eu, bg = k * BT + eb;
+                    const int unit = u0 + e / BT, bg = k * BT + e % BT;
                     if (G == 1) {
-                        h = activation(act, zs[e] + bps[e]);
+                        h = activation(p.act, zs[e] + bps[e]);
                     } else {
                         const int ub = U * BT;
                         const float zi = zs[0 * ub + e] + bps[e * G + 0];
@@ -650,8 +644,8 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                         h = sigmoidf_acc(zo) * tanhf(c);
                         if (s == p.T && p.cT != nullptr && bg < p.B) p.cT[static_cast<size_t>(bg) * H + unit] = c;
                     }
-                    if (eb < nb) {
-                        if (y_tile != nullptr) y_tile[eb * H + eu] = h;
+                    if (bg < p.B) {
+                        if (p.y != nullptr) p.y[(static_cast<size_t>(s - 1) * p.B + bg) * H + unit] = h;
                         if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + unit] = h;
                     }
                 }
