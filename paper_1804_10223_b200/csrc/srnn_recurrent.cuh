@@ -140,30 +140,23 @@ struct Fmt {
 template <bool F16, int BT, int K>
 __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, unsigned char* hs, int n_words,
                                           uint32_t want, bool spin, int32_t* status,
-                                          unsigned long long timeout_ns, bool early_barrier) {
+                                          unsigned long long timeout_ns) {
     const int n_chunks = (n_words + 1) >> 1;
     const int nt = blockDim.x;
     Watchdog wd{0ull, 0u};
     bool ok = true;
-    int base = threadIdx.x;
-    ulonglong2 v[K];
-    uint32_t pend = 0u;
-    auto issue = [&]() {
-        pend = 0u;
+    for (int base = threadIdx.x; base < n_chunks; base += K * nt) {
+        const ulonglong2* ptr = src + base;
+        ulonglong2 v[K];
+        uint32_t pend = 0u;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
             if (base + j * nt < n_chunks) {
-                v[j] = ld_relaxed_v2(src + base + j * nt);
+                v[j] = ld_relaxed_v2(ptr + j * nt);
                 pend |= 1u << j;
             }
         }
-    };
-    issue();
-    // hs is still being read by slower warps of the previous tile when the
-    // epilogue has no barrier of its own: wait here, while the loads fly.
-    if (early_barrier) __syncthreads();
-    while (true) {
-        while (pend != 0u) {
+        while (true) {
 #pragma unroll
             for (int j = 0; j < K; ++j) {
                 if ((pend >> j) & 1u) {
@@ -176,7 +169,6 @@ __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, un
             if (pend == 0u) break;
             if (!spin) {
                 atomicCAS(status, 0, -4 /* protocol violation -> SRNN_ERR_STATE */);
-                pend = 0u;
                 break;
             }
             if (watchdog_tick(wd, status, timeout_ns)) {
@@ -185,11 +177,9 @@ __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, un
             }
 #pragma unroll
             for (int j = 0; j < K; ++j)
-                if ((pend >> j) & 1u) v[j] = ld_relaxed_v2(src + base + j * nt);
+                if ((pend >> j) & 1u) v[j] = ld_relaxed_v2(ptr + j * nt);
         }
-        base += K * nt;
-        if (!ok || base >= n_chunks) break;
-        issue();
+        if (!ok) break;
     }
     return ok;
 }
@@ -502,15 +492,8 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
         }
     }
 
-    const int act = p.act;
     const int krow = warp * (32 / L) + lane / L;  // local row of this lane
     const bool row_leader = (lane % L) == 0 && krow < G * U;
-    // Direct epilogue (RNN with L >= BT): after the halving butterfly, lane
-    // j < BT of a row holds sample j's sum and finishes that sample itself
-    // (b', g, y, tagged publish): no shared-memory round trip, no barrier.
-    const bool direct = (G == 1) && (L >= BT);
-    const int dsample = lane & (L - 1);                     // sample of this lane (direct path)
-    const bool dactive = direct && dsample < BT && krow < U;  // lane owns (unit krow, sample dsample)
     if (tid == 0) *s_abort = 0;
 
     // Publish item e's h of (step s, tile k) as tagged words.  Called by all
@@ -559,7 +542,7 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                                   : nullptr;
             if (prof) prof[0] = clock64();
             // b'_s of this tile -> shared memory, asynchronously (in flight while we spin)
-            for (int j = 0; j < (direct ? 0 : item_rounds); ++j) {
+            for (int j = 0; j < item_rounds; ++j) {
                 const int e = tid + j * nt;
                 if (e < n_items) {
                     const int unit = u0 + e / BT, bg = k * BT + e % BT;
@@ -576,11 +559,8 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
             // ---- load: h_{s-1} tile k -> hs ----
             const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
                 p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
-            float bpd = 0.0f;  // direct path: this lane's b'_s (lands during the load)
-            if (dactive && k * BT + dsample < p.B)
-                bpd = __ldg(p.bprime + (static_cast<size_t>(s - 1) * p.B + k * BT + dsample) * GH + u0 + krow);
             if (!load_tile<F16, BT, LoadK<NP, F16>::value>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
-                                                            !grid_sync, p.status, p.timeout_ns, direct))
+                                                            !grid_sync, p.status, p.timeout_ns))
                 *s_abort = 1;
             __syncthreads();
             if (prof) prof[1] = clock64();
@@ -602,20 +582,18 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                 // L < BT: plain xor butterfly, the row leader holds all samples.
                 int sbase = 0;
                 if (L >= BT) {
-                    // split by the lowest sample bit first: lane j of the row
-                    // ends with sample j mod BT (natural order)
 #pragma unroll
-                    for (int lvl = 0, nv = BT; nv > 1; ++lvl, nv /= 2) {
+                    for (int lvl = 0, half = BT / 2; half >= 1; ++lvl, half /= 2) {
                         const int m = 1 << lvl;
                         const bool upper = (lane & m) != 0;
 #pragma unroll
-                        for (int i = 0; i < nv / 2; ++i) {
-                            const float keep = upper ? acc[(2 * i + 1) % BT] : acc[(2 * i) % BT];
-                            const float send = upper ? acc[(2 * i) % BT] : acc[(2 * i + 1) % BT];
+                        for (int i = 0; i < half; ++i) {
+                            const float keep = upper ? acc[(i + half) % BT] : acc[i];
+                            const float send = upper ? acc[i] : acc[(i + half) % BT];
                             acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
                         }
+                        if (upper) sbase += half;
                     }
-                    sbase = lane & (BT - 1);
 #pragma unroll
                     for (int m = BT; m <= 16; m <<= 1)
                         if (m < L) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], m);
@@ -629,33 +607,6 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                     }
                 }
                 if (prof) prof[5] = clock64();
-                if (direct) {
-                    // ---- direct epilogue: z + b', g, y, tagged publish ----
-                    const int b = dsample, bg = k * BT + b, unit = u0 + krow;
-                    const float h = activation(act, acc[0] + bpd);
-                    if (dactive && bg < p.B) {
-                        if (p.y != nullptr) p.y[(static_cast<size_t>(s - 1) * p.B + bg) * H + unit] = h;
-                        if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + unit] = h;
-                    }
-                    if ((p.flags & kFlagJitter) && tid == 0) {
-                        const uint32_t r = (static_cast<uint32_t>(cta) * 2654435761u) ^ (static_cast<uint32_t>(s * 40503 + k));
-                        __nanosleep((r >> 7) & 2047u);
-                    }
-                    unsigned long long* dst = p.xbuf + static_cast<size_t>((s & 1) * p.n_tiles + k) * tile_stride;
-                    const unsigned long long tag = static_cast<unsigned long long>(p.epoch + static_cast<uint32_t>(s)) << 32;
-                    if ((n_words & 1) && cta == 0 && tid == 0) st_relaxed_u64(dst + n_words, tag);  // pad word
-                    if (!F16) {
-                        if (dactive) st_relaxed_u64(dst + unit * BT + b, tag | __float_as_uint(h));
-                    } else {
-                        const uint32_t hb = __half_as_ushort(__float2half_rn(h));
-                        const uint32_t nb2 = __shfl_down_sync(0xffffffffu, hb, 1);
-                        if (dactive && (BT == 1 || (b & 1) == 0))
-                            st_relaxed_u64(dst + unit * F::WPR + (b >> 1), tag | (BT == 1 ? hb : (hb | (nb2 << 16))));
-                    }
-                    if (prof) prof[3] = clock64();
-                    if (grid_sync) cg::this_grid().sync();
-                    continue;
-                }
                 if (L >= BT) {
                     if ((lane % L) < BT && krow < G * U) zs[krow * BT + sbase] = acc[0];
                 } else if (row_leader) {
