@@ -653,6 +653,9 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
             }
             if (prof) prof[3] = clock64();
             if (grid_sync) cg::this_grid().sync();
+#ifdef SRNN_BARRIER_AFTER_PUBLISH
+            __syncthreads();  // experiment: start polling only after this CTA has published
+#endif
         }
     }
 done:
