@@ -27,9 +27,12 @@ def main():
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--bt", type=int, default=0, help="SRNN_BT override (batch tile)")
+    ap.add_argument("--delay", type=int, default=-1, help="SRNN_POLL_DELAY_NS")
     a = ap.parse_args()
     if a.bt:
         os.environ["SRNN_BT"] = str(a.bt)
+    if a.delay >= 0:
+        os.environ["SRNN_POLL_DELAY_NS"] = str(a.delay)
     prob = inputs.make_problem(a.H, a.H, a.B, a.T, a.d, cell=a.cell)
     m = from_problem(prob, prec=a.prec, flags=a.flags, num_ctas=a.C, lanes_per_row=a.L)
     x = torch.from_numpy(prob["x"]).cuda()
