@@ -41,7 +41,8 @@ struct RecParams {
     unsigned long long* xbuf;  // tagged exchange words [2][n_tiles][H][BT]
     int32_t* status;      // device status word (srnn_status_t)
     unsigned long long timeout_ns;
-    uint32_t poll_delay_ns;  // sleep before the first poll of a tile (tuning knob, SRNN_POLL_DELAY_NS)
+    uint32_t poll_delay_ns;    // sleep before the first poll of a tile (tuning knob, SRNN_POLL_DELAY_NS)
+    uint32_t poll_backoff_ns;  // sleep between stale poll rounds (tuning knob, SRNN_POLL_BACKOFF_NS)
     long long* profile;   // SRNN_FLAG_PROFILE: [cta][T][n_tiles][4] clock64 stamps or null
 };
 

@@ -140,7 +140,7 @@ struct Fmt {
 template <bool F16, int BT, int K>
 __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, unsigned char* hs, int n_words,
                                           uint32_t want, bool spin, int32_t* status,
-                                          unsigned long long timeout_ns) {
+                                          unsigned long long timeout_ns, uint32_t backoff_ns = 0) {
     const int n_chunks = (n_words + 1) >> 1;
     const int nt = blockDim.x;
     Watchdog wd{0ull, 0u};
@@ -175,6 +175,7 @@ __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, un
                 ok = false;
                 break;
             }
+            if (backoff_ns) __nanosleep(backoff_ns);
 #pragma unroll
             for (int j = 0; j < K; ++j)
                 if ((pend >> j) & 1u) v[j] = ld_relaxed_v2(ptr + j * nt);
@@ -560,7 +561,7 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
             const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
                 p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
             if (!load_tile<F16, BT, LoadK<NP, F16>::value>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
-                                                            !grid_sync, p.status, p.timeout_ns))
+                                                            !grid_sync, p.status, p.timeout_ns, p.poll_backoff_ns))
                 *s_abort = 1;
             __syncthreads();
             if (prof) prof[1] = clock64();
