@@ -622,6 +622,7 @@ srnn_status_t srnn_recurrence(srnn_plan_t p, int32_t T, int32_t B, const float* 
     rp.timeout_ns = p->timeout_ns;
     if (const char* d = std::getenv("SRNN_POLL_DELAY_NS")) rp.poll_delay_ns = static_cast<uint32_t>(std::atoi(d));
     if (const char* d = std::getenv("SRNN_POLL_BACKOFF_NS")) rp.poll_backoff_ns = static_cast<uint32_t>(std::atoi(d));
+    if (const char* d = std::getenv("SRNN_LOADER_THREADS")) rp.loader_threads = std::atoi(d);
     if (p->cfg.flags & SRNN_FLAG_PROFILE) {
         const int64_t need = static_cast<int64_t>(p->lay.num_ctas) * T * rp.n_tiles * 8;
         if (need > p->prof_elems) {

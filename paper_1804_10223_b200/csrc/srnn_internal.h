@@ -43,6 +43,7 @@ struct RecParams {
     unsigned long long timeout_ns;
     uint32_t poll_delay_ns;    // sleep before the first poll of a tile (tuning knob, SRNN_POLL_DELAY_NS)
     uint32_t poll_backoff_ns;  // sleep between stale poll rounds (tuning knob, SRNN_POLL_BACKOFF_NS)
+    int32_t loader_threads;    // threads that poll/stage h (0 = all; tuning knob, SRNN_LOADER_THREADS)
     long long* profile;   // SRNN_FLAG_PROFILE: [cta][T][n_tiles][4] clock64 stamps or null
 };
 

@@ -140,9 +140,10 @@ struct Fmt {
 template <bool F16, int BT, int K>
 __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, unsigned char* hs, int n_words,
                                           uint32_t want, bool spin, int32_t* status,
-                                          unsigned long long timeout_ns, uint32_t backoff_ns = 0) {
+                                          unsigned long long timeout_ns, uint32_t backoff_ns = 0,
+                                          int loaders = 0) {
     const int n_chunks = (n_words + 1) >> 1;
-    const int nt = blockDim.x;
+    const int nt = loaders > 0 ? min(loaders, static_cast<int>(blockDim.x)) : static_cast<int>(blockDim.x);
     Watchdog wd{0ull, 0u};
     bool ok = true;
     for (int base = threadIdx.x; base < n_chunks; base += K * nt) {
@@ -561,7 +562,8 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
             const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
                 p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
             if (!load_tile<F16, BT, LoadK<NP, F16>::value>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
-                                                            !grid_sync, p.status, p.timeout_ns, p.poll_backoff_ns))
+                                                            !grid_sync, p.status, p.timeout_ns, p.poll_backoff_ns,
+                                                            p.loader_threads))
                 *s_abort = 1;
             __syncthreads();
             if (prof) prof[1] = clock64();
