@@ -87,7 +87,7 @@ int elem_bytes(bool f16, int bt) { return f16 ? 2 * bt : 4 * bt; }
 
 size_t smem_for(const srnn_plan* p, int units_max, int bt, int n_tiles) {
     size_t s = (static_cast<size_t>(p->cfg.hidden) * elem_bytes(p->f16, bt) + 15) & ~static_cast<size_t>(15);
-    s += 2 * static_cast<size_t>(p->G) * units_max * bt * 4;  // zs + b' staging
+    s += 3 * static_cast<size_t>(p->G) * units_max * bt * 4;  // zs + double-buffered b' staging
     if (p->G == 4) s += static_cast<size_t>(n_tiles) * units_max * bt * 4;
     return s + 16;
 }

@@ -466,8 +466,8 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     // shared memory: hs [H][BT] at offset 0 (E bytes per unit), then fp32 areas
     unsigned char* hs = smem;
     float* zs = reinterpret_cast<float*>(smem + ((static_cast<size_t>(H) * F::E + 15) & ~static_cast<size_t>(15)));
-    float* bps = zs + G * umax_bt;                           // b'_s of this tile: [item][G]
-    float* cs = bps + G * umax_bt;                           // LSTM c: [n_tiles][item]
+    float* bpsb = zs + G * umax_bt;                          // b' double buffer: [2][item][G]
+    float* cs = bpsb + 2 * G * umax_bt;                      // LSTM c: [n_tiles][item]
     int* s_abort = reinterpret_cast<int*>(cs + (G == 4 ? p.n_tiles * umax_bt : 0));
     unsigned char* ws = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(s_abort + 1) + 15) & ~static_cast<uintptr_t>(15));  // smem weight tier
@@ -537,27 +537,41 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     if (grid_sync) cg::this_grid().sync();
     __syncthreads();
 
+    auto issue_bprime = [&](int s, int k, int b) {
+        float* dstb = bpsb + b * G * umax_bt;
+        for (int j = 0; j < item_rounds; ++j) {
+            const int e = tid + j * nt;
+            if (e < n_items) {
+                const int unit = u0 + e / BT, bg = k * BT + e % BT;
+#pragma unroll
+                for (int q = 0; q < G; ++q) {
+                    if (bg < p.B)
+                        cp_async_f32(&dstb[e * G + q], p.bprime + (static_cast<size_t>(s - 1) * p.B + bg) * GH + q * H + unit);
+                    else
+                        dstb[e * G + q] = 0.0f;
+                }
+            }
+        }
+    };
+    int buf = 0;
+    if (p.T >= 1) issue_bprime(1, 0, 0);
+    cp_async_commit();
+
     for (int s = 1; s <= p.T; ++s) {
         for (int k = 0; k < p.n_tiles; ++k) {
             long long* prof = (p.flags & kFlagProfile) && p.profile != nullptr && tid == 0
                                   ? p.profile + ((static_cast<size_t>(cta) * p.T + (s - 1)) * p.n_tiles + k) * 8
                                   : nullptr;
             if (prof) prof[0] = clock64();
-            // b'_s of this tile -> shared memory, asynchronously (in flight while we spin)
-            for (int j = 0; j < item_rounds; ++j) {
-                const int e = tid + j * nt;
-                if (e < n_items) {
-                    const int unit = u0 + e / BT, bg = k * BT + e % BT;
-#pragma unroll
-                    for (int q = 0; q < G; ++q) {
-                        if (bg < p.B)
-                            cp_async_f32(&bps[e * G + q], p.bprime + (static_cast<size_t>(s - 1) * p.B + bg) * GH + q * H + unit);
-                        else
-                            bps[e * G + q] = 0.0f;
-                    }
-                }
+            // b' of the NEXT tile -> shared memory (cp.async, double-buffered):
+            // it lands during this whole tile; this tile's b' was issued one
+            // tile earlier.
+            {
+                const int ns = k + 1 < p.n_tiles ? s : s + 1, nk = k + 1 < p.n_tiles ? k + 1 : 0;
+                if (ns <= p.T) issue_bprime(ns, nk, buf ^ 1);
+                cp_async_commit();
             }
-            cp_async_commit();
+            float* bps = bpsb + buf * G * umax_bt;
             // ---- load: h_{s-1} tile k -> hs ----
             const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
                 p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
@@ -617,7 +631,7 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                     for (int b = 0; b < BT; ++b) zs[krow * BT + b] = acc[b];
                 }
             }
-            cp_async_wait_all();
+            asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's b' (the newest group may pend)
             if (prof) prof[6] = clock64();
             __syncthreads();
             if (prof) prof[2] = clock64();
@@ -661,6 +675,7 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
             // epilogue warps for the LSU (measured: -6..10% step time).
             __syncthreads();
             if (p.poll_delay_ns) __nanosleep(p.poll_delay_ns);
+            buf ^= 1;
         }
     }
 done:
