@@ -494,7 +494,13 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
         }
     }
 
+    const int act = p.act;
     const int krow = warp * (32 / L) + lane / L;  // local row of this lane
+    // epilogue fast path (one item per thread): item e1 = tid -> (unit, sample)
+    const int e1 = tid, e1_b = tid % BT, e1_unit = u0 + tid / BT;
+    const bool e1_ok = tid < n_items;
+    const float* zs_e1 = zs + e1;
+    float* const y_e1 = (p.y != nullptr && e1_ok) ? p.y + static_cast<size_t>(e1_b) * H + e1_unit : nullptr;
     const bool row_leader = (lane % L) == 0 && krow < G * U;
     if (tid == 0) *s_abort = 0;
 
@@ -641,6 +647,19 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                 const uint32_t r = (static_cast<uint32_t>(cta) * 2654435761u) ^ (static_cast<uint32_t>(s * 40503 + k));
                 __nanosleep((r >> 7) & 2047u);
             }
+            if (G == 1 && item_rounds == 1) {
+                // fast path (one item per thread, RNN): addresses hoisted out of the time loop
+                float h = 0.0f;
+                if (e1_ok) {
+                    h = activation(act, zs_e1[0] + bps[e1]);
+                    const int bg = k * BT + e1_b;
+                    if (bg < p.B) {
+                        if (y_e1 != nullptr) y_e1[(static_cast<size_t>(s - 1) * p.B + k * BT) * H] = h;
+                        if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + e1_unit] = h;
+                    }
+                }
+                publish(s, k, e1, e1_ok, h);
+            } else
             for (int j = 0; j < item_rounds; ++j) {
                 const int e = tid + j * nt;
                 const bool ok = e < n_items;
