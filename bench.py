@@ -365,6 +365,39 @@ def main():
                              "peak_tflops": 1663.3 if prec == "fp16" else None,
                              "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; fp16 has the same dense rate)",
                              "frac": (gemm_flops / t_gemm / 1e12) / 1663.3 if prec == "fp16" else None}
+        # Latency roofline of the recurrent kernel: the measured exchange/sync floor (same
+        # H, B, plan shape, density 0: no pairs, everything else identical) plus the
+        # shared-memory time of the packer's predicted wavefronts (busiest CTA, per step).
+        try:
+            zprob = dict(prob)
+            zprob["rowptr"] = np.zeros_like(prob["rowptr"])
+            zprob["col"] = np.zeros(0, np.int32)
+            zprob["val"] = np.zeros(0, np.float32)
+            zm = from_problem(zprob, prec=prec, device=local, flags=args.flags, num_ctas=info["num_ctas"],
+                              lanes_per_row=info["lanes_per_row"])
+            zm.recurrence(bp, y=y, hT=hT)
+            torch.cuda.synchronize()
+            ze = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            zts = []
+            for _ in range(5):
+                ze[0].record(stream)
+                zm.recurrence(bp, y=y, hT=hT)
+                ze[1].record(stream)
+                torch.cuda.synchronize()
+                zts.append(ze[0].elapsed_time(ze[1]))
+            zm.status()
+            zm.close()
+            f_hz = (clocks.get("sm_mhz") or 1965.0) * 1e6
+            floor_us = statistics.median(zts) * 1000 / T
+            smem_us = info["wavefronts_per_step_max"] * info["num_batch_tiles"] / f_hz * 1e6
+            out["roofline_latency"] = {
+                "sync_floor_us_per_step": floor_us, "smem_us_per_step": smem_us,
+                "t_roof_us_per_step": floor_us + smem_us, "t_us_per_step": t_rec * 1e6 / T,
+                "frac": (floor_us + smem_us) / (t_rec * 1e6 / T),
+                "note": "sync floor = same plan shape at density 0 (exchange + barriers + epilogue, no "
+                        "pairs), measured here; smem = predicted wavefronts of the busiest CTA / SM clock"}
+        except Exception as ex:  # noqa: BLE001
+            out["roofline_latency"] = {"error": str(ex)[:200]}
         if not args.no_cublas and world == 1:
             cb = cublas_dense_baseline(H, B, T, dev)
             cb["speedup_vs_graph"] = cb["graph_us_per_timestep"] / (t_rec * 1e6 / T)
