@@ -84,6 +84,10 @@ typedef enum { SRNN_PREC_FP32 = 0, SRNN_PREC_FP16W_FP32ACC = 1 } srnn_prec_t;
                                               register pairs (ablation; default fp16 staging and
                                               one register per pair)        */
 #define SRNN_FLAG_PROFILE        (1u << 6) /* record per-CTA phase timestamps (srnn_plan_debug_timeline) */
+#define SRNN_FLAG_RESERVE_SMS    (1u << 7) /* leave 4 SMs free so srnn_forward_host can pipeline: x
+                                              chunks are copied and projected (GEMM on the free SMs)
+                                              while the persistent kernel runs, y chunks are copied
+                                              back as the kernel reports progress               */
 
 typedef struct {
     int32_t hidden;     /* H >= 1, <= 65536 (u16 column index)                          */
@@ -177,9 +181,14 @@ srnn_status_t srnn_recurrence(srnn_plan_t plan, int32_t T, int32_t B, const floa
                               void *stream);
 
 /* End-to-end call on HOST buffers (same layouts as srnn_forward): copies x
- * (and h0/c0) host->device, runs srnn_forward, copies y (and hT/cT) back, and
- * synchronises the plan's internal stream before returning.  Any output
- * pointer may be NULL.  Pageable or pinned host memory is accepted. */
+ * (and h0/c0) host->device, runs the input projection and the recurrence,
+ * copies y (and hT/cT) back, and synchronises before returning.  Any output
+ * pointer may be NULL.  Pageable or pinned host memory is accepted (pinned
+ * overlaps).  If the plan leaves SMs free (SRNN_FLAG_RESERVE_SMS) the call is
+ * pipelined: x arrives and is projected in chunks of steps while the
+ * persistent kernel already runs (it waits per step for its b' rows), and y
+ * leaves in chunks as the kernel reports progress (stream memory operations,
+ * cuStreamWaitValue32 / cuStreamWriteValue32). */
 srnn_status_t srnn_forward_host(srnn_plan_t plan, int32_t T, int32_t B, const float *x_host,
                                 const float *h0_host, const float *c0_host, float *y_host,
                                 float *hT_host, float *cT_host);

@@ -28,6 +28,7 @@ FLAG_SIMT_GEMM = 1 << 3
 FLAG_DEBUG_JITTER = 1 << 4
 FLAG_FP32_STAGING = 1 << 5
 FLAG_PROFILE = 1 << 6
+FLAG_RESERVE_SMS = 1 << 7
 
 EXPORTED = ["srnn_plan_create", "srnn_plan_query", "srnn_load_weights", "srnn_forward", "srnn_input_projection",
             "srnn_recurrence", "srnn_forward_host", "srnn_plan_status", "srnn_plan_export_layout",

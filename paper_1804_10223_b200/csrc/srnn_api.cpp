@@ -60,6 +60,12 @@ struct srnn_plan {
     unsigned long long timeout_ns = 2000000000ull;
     long long* d_prof = nullptr;
     int64_t prof_elems = 0;
+    // pipelined srnn_forward_host
+    uint32_t* d_ready = nullptr;     // b' rows ready (monotone counter)
+    uint32_t* d_progress = nullptr;  // per-CTA progress increments (monotone counter)
+    uint32_t ready_base = 0, progress_base = 0;
+    cudaStream_t s_rec = nullptr, s_out = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_rec = nullptr;
 };
 
 namespace {
@@ -110,6 +116,12 @@ void free_device(srnn_plan* p) {
     cudaFree(p->d_hT);
     cudaFree(p->d_cT);
     cudaFree(p->d_prof);
+    cudaFree(p->d_ready);
+    cudaFree(p->d_progress);
+    if (p->s_rec) cudaStreamDestroy(p->s_rec);
+    if (p->s_out) cudaStreamDestroy(p->s_out);
+    if (p->ev_in) cudaEventDestroy(p->ev_in);
+    if (p->ev_rec) cudaEventDestroy(p->ev_rec);
     if (p->stream) cudaStreamDestroy(p->stream);
     p->d_img = nullptr;
 }
@@ -348,7 +360,7 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
     if (p->cfg.num_ctas > 0) {
         cands_c.push_back(p->cfg.num_ctas);
     } else {
-        const int cmax = std::min(p->sm_count, H);
+        const int cmax = std::min(p->sm_count - ((p->cfg.flags & SRNN_FLAG_RESERVE_SMS) ? 4 : 0), H);
         cands_c.push_back(cmax);
         for (int cc = cmax / 2; cc >= 1; cc /= 2) cands_c.push_back(cc);
     }
@@ -542,6 +554,30 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
     return SRNN_OK;
 }
 
+// b' rows [r0, r0 + M) from x rows [r0, r0 + M) (x, bprime: full device buffers).
+static srnn_status_t project_rows(srnn_plan_t p, int64_t r0, int64_t M, const float* x, float* bprime, void* stream) {
+    const int I = p->cfg.input, N = p->G * p->cfg.hidden;
+    if (M <= 0) return SRNN_OK;
+    if (p->tc_gemm) {
+        void* x16 = static_cast<char*>(p->d_x16) + static_cast<size_t>(r0) * p->k_pad * 2;
+        int e = I == p->k_pad ? launch_f32_to_f16(x + r0 * I, x16, M * I, stream)
+                              : launch_f32_to_f16_padded(x + r0 * I, x16, M, I, p->k_pad, stream);
+        if (e == 0)
+            e = launch_gemm_tc(&p->map_x16, &p->map_wx16, p->d_bias, bprime, static_cast<int>(M), N, p->k_pad, stream,
+                               static_cast<int>(r0));
+        return e == 0 ? SRNN_OK : SRNN_ERR_CUDA;
+    }
+    GemmParams gp;
+    gp.M = M;
+    gp.N = N;
+    gp.K = I;
+    gp.A = x + r0 * I;
+    gp.W = p->d_wx;
+    gp.bias = p->d_bias;
+    gp.C = bprime + r0 * N;
+    return launch_gemm_f32(gp, stream) == 0 ? SRNN_OK : SRNN_ERR_CUDA;
+}
+
 srnn_status_t srnn_input_projection(srnn_plan_t p, int32_t T, int32_t B, const float* x, float* bprime, void* stream) {
     if (!p) return SRNN_ERR_INVALID_VALUE;
     if (!p->loaded || p->host_only) return SRNN_ERR_STATE;
@@ -549,29 +585,29 @@ srnn_status_t srnn_input_projection(srnn_plan_t p, int32_t T, int32_t B, const f
         return SRNN_ERR_INVALID_VALUE;
     if (T == 0) return SRNN_OK;
     DeviceGuard g(p->cfg.device);
-    if (p->tc_gemm) {
-        const int64_t M = static_cast<int64_t>(T) * B;
-        const int I = p->cfg.input;
-        int e = I == p->k_pad ? launch_f32_to_f16(x, p->d_x16, M * I, stream)
-                              : launch_f32_to_f16_padded(x, p->d_x16, M, I, p->k_pad, stream);
-        if (e == 0)
-            e = launch_gemm_tc(&p->map_x16, &p->map_wx16, p->d_bias, bprime, static_cast<int>(M), p->G * p->cfg.hidden,
-                               p->k_pad, stream);
-        return e == 0 ? SRNN_OK : SRNN_ERR_CUDA;
-    }
-    GemmParams gp;
-    gp.M = static_cast<int64_t>(T) * B;
-    gp.N = p->G * p->cfg.hidden;
-    gp.K = p->cfg.input;
-    gp.A = x;
-    gp.W = p->d_wx;
-    gp.bias = p->d_bias;
-    gp.C = bprime;
-    return launch_gemm_f32(gp, stream) == 0 ? SRNN_OK : SRNN_ERR_CUDA;
+    return project_rows(p, 0, static_cast<int64_t>(T) * B, x, bprime, stream);
 }
+
+struct PipeArgs {
+    const uint32_t* bp_ready = nullptr;
+    uint32_t bp_ready_base = 0;
+    uint32_t* progress = nullptr;
+    int every = 0;
+};
+static srnn_status_t recurrence_impl(srnn_plan_t p, int32_t T, int32_t B, const float* bprime, const float* h0,
+                                     const float* c0, float* y, float* hT, float* cT, void* stream,
+                                     const PipeArgs& pa);
 
 srnn_status_t srnn_recurrence(srnn_plan_t p, int32_t T, int32_t B, const float* bprime, const float* h0,
                               const float* c0, float* y, float* hT, float* cT, void* stream) {
+    return recurrence_impl(p, T, B, bprime, h0, c0, y, hT, cT, stream, PipeArgs());
+}
+
+}  // extern "C"
+
+static srnn_status_t recurrence_impl(srnn_plan_t p, int32_t T, int32_t B, const float* bprime, const float* h0,
+                                     const float* c0, float* y, float* hT, float* cT, void* stream,
+                                     const PipeArgs& pa) {
     if (!p) return SRNN_ERR_INVALID_VALUE;
     if (!p->loaded || p->host_only) return SRNN_ERR_STATE;
     if (T < 0 || T > p->cfg.max_steps || B < 1 || B > p->cfg.batch || (T > 0 && !bprime)) return SRNN_ERR_INVALID_VALUE;
@@ -633,12 +669,18 @@ srnn_status_t srnn_recurrence(srnn_plan_t p, int32_t T, int32_t B, const float* 
         p->prof_elems = need;
         rp.profile = p->d_prof;
     }
+    rp.bp_ready = pa.bp_ready;
+    rp.bp_ready_base = pa.bp_ready_base;
+    rp.progress = pa.progress;
+    rp.progress_every = pa.every > 0 ? pa.every : 1;
     int e = launch_recurrent(p->np_inst, p->BT, p->G, p->f16 ? 1 : 0, rp, p->lay.num_ctas, p->smem_bytes, stream,
                              false, nullptr, nullptr);
     if (e != 0) return SRNN_ERR_CUDA;
     p->epoch += static_cast<uint32_t>(T) + 1;
     return SRNN_OK;
 }
+
+extern "C" {
 
 srnn_status_t srnn_forward(srnn_plan_t p, int32_t T, int32_t B, const float* x, const float* h0, const float* c0,
                            float* y, float* hT, float* cT, void* stream) {
@@ -652,36 +694,119 @@ srnn_status_t srnn_forward(srnn_plan_t p, int32_t T, int32_t B, const float* x, 
     return srnn_recurrence(p, T, B, p->d_bprime, h0, c0, y, hT, cT, stream);
 }
 
+// Driver stream-memory operations (cuStreamWaitValue32 / cuStreamWriteValue32)
+// through the runtime's driver entry point (no -lcuda).
+namespace {
+typedef CUresult (*PFN_wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_wait32 g_wait32 = nullptr;
+PFN_write32 g_write32 = nullptr;
+bool stream_mem_ops() {
+    if (g_wait32 && g_write32) return true;
+    void* f1 = nullptr;
+    void* f2 = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f1, cudaEnableDefault, &q) != cudaSuccess || !f1) return false;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f2, cudaEnableDefault, &q) != cudaSuccess || !f2) return false;
+    g_wait32 = reinterpret_cast<PFN_wait32>(f1);
+    g_write32 = reinterpret_cast<PFN_write32>(f2);
+    return true;
+}
+}  // namespace
+
 srnn_status_t srnn_forward_host(srnn_plan_t p, int32_t T, int32_t B, const float* x_host, const float* h0_host,
                                 const float* c0_host, float* y_host, float* hT_host, float* cT_host) {
     if (!p) return SRNN_ERR_INVALID_VALUE;
     if (!p->loaded || p->host_only) return SRNN_ERR_STATE;
     if (T < 0 || T > p->cfg.max_steps || B < 1 || B > p->cfg.batch || (T > 0 && !x_host)) return SRNN_ERR_INVALID_VALUE;
     DeviceGuard g(p->cfg.device);
-    const int H = p->cfg.hidden, I = p->cfg.input;
+    const int H = p->cfg.hidden, I = p->cfg.input, GH = p->G * H;
     const size_t xs = static_cast<size_t>(std::max(1, p->cfg.max_steps)) * p->cfg.batch * I * 4;
     const size_t ys = static_cast<size_t>(std::max(1, p->cfg.max_steps)) * p->cfg.batch * H * 4;
     const size_t hs = static_cast<size_t>(p->cfg.batch) * H * 4;
     if (!p->d_x) {
         if (cudaMalloc(&p->d_x, xs) != cudaSuccess || cudaMalloc(&p->d_y, ys) != cudaSuccess ||
             cudaMalloc(&p->d_h0, hs) != cudaSuccess || cudaMalloc(&p->d_c0, hs) != cudaSuccess ||
-            cudaMalloc(&p->d_hT, hs) != cudaSuccess || cudaMalloc(&p->d_cT, hs) != cudaSuccess)
+            cudaMalloc(&p->d_hT, hs) != cudaSuccess || cudaMalloc(&p->d_cT, hs) != cudaSuccess ||
+            cudaMalloc(&p->d_ready, 4) != cudaSuccess || cudaMalloc(&p->d_progress, 4) != cudaSuccess ||
+            cudaMemset(p->d_ready, 0, 4) != cudaSuccess || cudaMemset(p->d_progress, 0, 4) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&p->s_rec, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->ev_rec, cudaEventDisableTiming) != cudaSuccess)
             return SRNN_ERR_CUDA;
     }
     cudaStream_t st = p->stream;
-    const size_t xb = static_cast<size_t>(T) * B * I * 4, yb = static_cast<size_t>(T) * B * H * 4,
-                 hb = static_cast<size_t>(B) * H * 4;
+    const size_t hb = static_cast<size_t>(B) * H * 4;
     cudaError_t e = cudaSuccess;
-    if (T > 0) e = cudaMemcpyAsync(p->d_x, x_host, xb, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess && h0_host) e = cudaMemcpyAsync(p->d_h0, h0_host, hb, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess && c0_host && p->G == 4) e = cudaMemcpyAsync(p->d_c0, c0_host, hb, cudaMemcpyHostToDevice, st);
+    const bool pipelined = T >= 2 && p->lay.num_ctas < p->sm_count && stream_mem_ops();
+    if (!pipelined) {  // plain: H2D, forward, D2H on one stream
+        const size_t xb = static_cast<size_t>(T) * B * I * 4, yb = static_cast<size_t>(T) * B * H * 4;
+        if (T > 0) e = cudaMemcpyAsync(p->d_x, x_host, xb, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess && h0_host) e = cudaMemcpyAsync(p->d_h0, h0_host, hb, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess && c0_host && p->G == 4) e = cudaMemcpyAsync(p->d_c0, c0_host, hb, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return SRNN_ERR_CUDA;
+        srnn_status_t s = srnn_forward(p, T, B, p->d_x, h0_host ? p->d_h0 : nullptr, c0_host ? p->d_c0 : nullptr,
+                                       y_host ? p->d_y : nullptr, p->d_hT, p->G == 4 ? p->d_cT : nullptr, st);
+        if (s != SRNN_OK) return s;
+        if (y_host && T > 0) e = cudaMemcpyAsync(y_host, p->d_y, yb, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess && hT_host) e = cudaMemcpyAsync(hT_host, p->d_hT, hb, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess && cT_host && p->G == 4) e = cudaMemcpyAsync(cT_host, p->d_cT, hb, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return SRNN_ERR_CUDA;
+        return srnn_plan_status(p);
+    }
+    // ---- pipelined: stream `st` copies + projects x chunk by chunk on the free SMs and
+    // bumps d_ready; s_rec runs the persistent kernel, which waits per step for its b'
+    // rows; s_out copies y chunks back as the kernel's progress counter passes them ----
+    const int n_chunks = std::min(8, T);
+    const int every = (T + n_chunks - 1) / n_chunks;  // steps per chunk (input and output)
+    const uint32_t ready_base = p->ready_base, prog_base = p->progress_base;
+    if (h0_host) e = cudaMemcpyAsync(p->d_h0, h0_host, hb, cudaMemcpyHostToDevice, p->s_rec);
+    if (e == cudaSuccess && c0_host && p->G == 4) e = cudaMemcpyAsync(p->d_c0, c0_host, hb, cudaMemcpyHostToDevice, p->s_rec);
     if (e != cudaSuccess) return SRNN_ERR_CUDA;
-    srnn_status_t s = srnn_forward(p, T, B, p->d_x, h0_host ? p->d_h0 : nullptr, c0_host ? p->d_c0 : nullptr,
-                                   y_host ? p->d_y : nullptr, p->d_hT, p->G == 4 ? p->d_cT : nullptr, st);
+    PipeArgs pa;
+    pa.bp_ready = p->d_ready;
+    pa.bp_ready_base = ready_base;
+    pa.progress = y_host ? p->d_progress : nullptr;
+    pa.every = every;
+    srnn_status_t s = recurrence_impl(p, T, B, p->d_bprime, h0_host ? p->d_h0 : nullptr,
+                                      c0_host ? p->d_c0 : nullptr, y_host ? p->d_y : nullptr, p->d_hT,
+                                      p->G == 4 ? p->d_cT : nullptr, p->s_rec, pa);
     if (s != SRNN_OK) return s;
-    if (y_host && T > 0) e = cudaMemcpyAsync(y_host, p->d_y, yb, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess && hT_host) e = cudaMemcpyAsync(hT_host, p->d_hT, hb, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess && cT_host && p->G == 4) e = cudaMemcpyAsync(cT_host, p->d_cT, hb, cudaMemcpyDeviceToHost, st);
+    if (cudaEventRecord(p->ev_rec, p->s_rec) != cudaSuccess) return SRNN_ERR_CUDA;
+    for (int c = 0; c < n_chunks; ++c) {
+        const int s0 = c * every, s1 = std::min(T, s0 + every);
+        if (s0 >= s1) break;
+        const int64_t r0 = static_cast<int64_t>(s0) * B, nr = static_cast<int64_t>(s1 - s0) * B;
+        e = cudaMemcpyAsync(p->d_x + r0 * I, x_host + r0 * I, static_cast<size_t>(nr) * I * 4, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return SRNN_ERR_CUDA;
+        s = project_rows(p, r0, nr, p->d_x, p->d_bprime, st);
+        if (s != SRNN_OK) return s;
+        if (g_write32(st, reinterpret_cast<CUdeviceptr>(p->d_ready), ready_base + static_cast<uint32_t>(s1),
+                      CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+            return SRNN_ERR_CUDA;
+    }
+    (void)GH;
+    if (y_host) {
+        const uint32_t C = static_cast<uint32_t>(p->lay.num_ctas);
+        for (int c = 0; c < n_chunks; ++c) {
+            const int s0 = c * every, s1 = std::min(T, s0 + every);
+            if (s0 >= s1) break;
+            if (g_wait32(p->s_out, reinterpret_cast<CUdeviceptr>(p->d_progress), prog_base + C * static_cast<uint32_t>(c + 1),
+                         CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                return SRNN_ERR_CUDA;
+            const size_t r0 = static_cast<size_t>(s0) * B, nr = static_cast<size_t>(s1 - s0) * B;
+            e = cudaMemcpyAsync(y_host + r0 * H, p->d_y + r0 * H, nr * H * 4, cudaMemcpyDeviceToHost, p->s_out);
+            if (e != cudaSuccess) return SRNN_ERR_CUDA;
+        }
+        p->progress_base = prog_base + C * static_cast<uint32_t>((T + every - 1) / every);
+    }
+    p->ready_base = ready_base + static_cast<uint32_t>(T) + 1;
+    e = cudaStreamWaitEvent(p->s_out, p->ev_rec, 0);
+    if (e == cudaSuccess && hT_host) e = cudaMemcpyAsync(hT_host, p->d_hT, hb, cudaMemcpyDeviceToHost, p->s_out);
+    if (e == cudaSuccess && cT_host && p->G == 4) e = cudaMemcpyAsync(cT_host, p->d_cT, hb, cudaMemcpyDeviceToHost, p->s_out);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->s_out);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return SRNN_ERR_CUDA;
     return srnn_plan_status(p);

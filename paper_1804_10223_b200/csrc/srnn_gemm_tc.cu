@@ -63,7 +63,7 @@ constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | ((TC_BN >> 3) <
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_f16_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                       const float* __restrict__ bias, float* __restrict__ C, int M, int N, int K) {
+                       const float* __restrict__ bias, float* __restrict__ C, int M, int N, int K, int m_off) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for the 128B-swizzled operand tiles
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * TC_BN;
+    const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * TC_BN;  // rows relative to m_off
     const int nk = (K + TC_BK - 1) / TC_BK;
 
     if (threadIdx.x == 0) {
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int s = kb % TC_STAGES;
             if (kb >= TC_STAGES) mbar_wait(&empty[s], ((kb / TC_STAGES) - 1) & 1);
             mbar_expect_tx(&full[s], 2 * TC_TILE_BYTES);
-            tma_load_2d(sA + s * TC_TILE_BYTES, &map_a, &full[s], kb * TC_BK, m0);
+            tma_load_2d(sA + s * TC_TILE_BYTES, &map_a, &full[s], kb * TC_BK, m_off + m0);
             tma_load_2d(sB + s * TC_TILE_BYTES, &map_b, &full[s], kb * TC_BK, n0);
         }
     } else if (warp == 1 && lane == 0) {
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 : "r"(taddr));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             if (row < M) {
-                float* crow = C + static_cast<size_t>(row) * N + n0 + c;
+                float* crow = C + static_cast<size_t>(m_off + row) * N + n0 + c;
                 const int nvalid = min(32, N - (n0 + c));
                 if (nvalid == 32 && (N & 3) == 0) {
 #pragma unroll
@@ -228,7 +228,7 @@ int launch_f32_to_f16(const float* in, void* out, int64_t n, void* stream) {
 }
 
 int launch_gemm_tc(const void* map_a, const void* map_b, const float* bias, float* C, int M, int N, int K,
-                   void* stream) {
+                   void* stream, int m_off) {
     if (M <= 0 || N <= 0) return 0;
     static bool attr_set = false;
     const size_t smem = gemm_tc_smem_bytes();
@@ -240,7 +240,7 @@ int launch_gemm_tc(const void* map_a, const void* map_b, const float* bias, floa
     }
     dim3 grid((N + TC_BN - 1) / TC_BN, (M + TC_BM - 1) / TC_BM);
     gemm_tc_f16_kernel<<<grid, TC_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(
-        *static_cast<const CUtensorMap*>(map_a), *static_cast<const CUtensorMap*>(map_b), bias, C, M, N, K);
+        *static_cast<const CUtensorMap*>(map_a), *static_cast<const CUtensorMap*>(map_b), bias, C, M, N, K, m_off);
     return static_cast<int>(cudaGetLastError());
 }
 

@@ -44,7 +44,13 @@ struct RecParams {
     uint32_t poll_delay_ns;    // sleep before the first poll of a tile (tuning knob, SRNN_POLL_DELAY_NS)
     uint32_t poll_backoff_ns;  // sleep between stale poll rounds (tuning knob, SRNN_POLL_BACKOFF_NS)
     int32_t loader_threads;    // threads that poll/stage h (0 = all; tuning knob, SRNN_LOADER_THREADS)
-    long long* profile;   // SRNN_FLAG_PROFILE: [cta][T][n_tiles][4] clock64 stamps or null
+    long long* profile;   // SRNN_FLAG_PROFILE: [cta][T][n_tiles][8] clock64 stamps or null
+    // host-pipelined forward (srnn_forward_host): b' arrives in chunks while the
+    // kernel runs; y leaves in chunks while it runs
+    const uint32_t* bp_ready;  // b' rows of steps <= *bp_ready - bp_ready_base are written (or null)
+    uint32_t bp_ready_base;
+    uint32_t* progress;        // +1 per CTA every progress_every steps (after y is stored), or null
+    int32_t progress_every;
 };
 
 struct GemmParams {
@@ -64,7 +70,7 @@ int launch_recurrent(int np, int bt, int g, int f16, const RecParams& p, int num
 int launch_gemm_f32(const GemmParams& p, void* stream);
 // fp16 tensor-core input GEMM (srnn_gemm_tc.cu); maps are CUtensorMap*.
 int launch_gemm_tc(const void* map_a, const void* map_b, const float* bias, float* C, int M, int N, int K,
-                   void* stream);
+                   void* stream, int m_off = 0);  // rows [m_off, m_off + M) of A and C
 int launch_f32_to_f16(const float* in, void* out, int64_t n, void* stream);
 int launch_f32_to_f16_padded(const float* in, void* out, int64_t rows, int cols, int ld_out, void* stream);
 

@@ -57,6 +57,11 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
     asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
     return r;
 }
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+    uint32_t r;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+    return r;
+}
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -545,6 +550,11 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
 
     auto issue_bprime = [&](int s, int k, int b) {
         float* dstb = bpsb + b * G * umax_bt;
+        if (p.bp_ready != nullptr && tid < n_items) {  // pipelined host forward: wait for this step's b'
+            Watchdog wdb{0ull, 0u};
+            while (static_cast<int32_t>(ld_acquire_u32(p.bp_ready) - p.bp_ready_base) < s)
+                if (watchdog_tick(wdb, p.status, p.timeout_ns)) break;
+        }
         for (int j = 0; j < item_rounds; ++j) {
             const int e = tid + j * nt;
             if (e < n_items) {
@@ -695,6 +705,11 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
             __syncthreads();
             if (p.poll_delay_ns) __nanosleep(p.poll_delay_ns);
             buf ^= 1;
+            if (p.progress != nullptr && tid == 0 && k == p.n_tiles - 1 &&
+                (s % p.progress_every == 0 || s == p.T)) {
+                __threadfence();  // this CTA's y of steps <= s (ordered by the barrier above) before the count
+                atomicAdd(p.progress, 1u);
+            }
         }
     }
 done:

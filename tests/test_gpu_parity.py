@@ -9,7 +9,7 @@ import pytest
 
 import oracle
 from paper_1804_10223_b200 import (FLAG_DEBUG_JITTER, FLAG_FP32_STAGING, FLAG_GRID_SYNC, FLAG_NAIVE_LAYOUT,
-                                   from_problem, inputs)
+                                   FLAG_RESERVE_SMS, from_problem, inputs)
 
 pytestmark = pytest.mark.gpu
 
@@ -296,3 +296,26 @@ def test_C5_shape_sampled_and_partition(cuda_device):
         parts.append(m.forward(x[:, s0:s0 + c].contiguous())[0])
     torch.cuda.synchronize()
     assert torch.equal(torch.cat(parts, 1), y)
+
+
+@pytest.mark.parametrize("prec,cell,B,T", [("fp16", "rnn", 4, 37), ("fp32", "rnn", 3, 16), ("fp16", "lstm", 2, 9),
+                                           ("fp16", "rnn", 4, 1)])
+def test_forward_host_pipelined(cuda_device, prec, cell, B, T):
+    """SRNN_FLAG_RESERVE_SMS: srnn_forward_host projects x chunks on the free SMs while
+    the persistent kernel runs and copies y back by progress -- same bits as the
+    plain device forward of the same plan, over repeated calls (monotone counters)."""
+    import torch
+    prob = inputs.make_problem(640, 320, B, T, 0.1, cell=cell, act="tanh", h0="random", c0="random")
+    m = from_problem(prob, prec=prec, flags=FLAG_RESERVE_SMS)
+    assert m.info()["num_ctas"] <= m.info()["sm_count"] - 4
+    xh = torch.from_numpy(prob["x"]).pin_memory().numpy()
+    for _ in range(3):
+        outs = m.forward_host(xh, prob["h0"], prob["c0"])
+        m.status()
+    dev = m.forward(torch.from_numpy(prob["x"]).cuda(), torch.from_numpy(prob["h0"]).cuda(),
+                    torch.from_numpy(prob["c0"]).cuda() if cell == "lstm" else None)
+    torch.cuda.synchronize()
+    assert np.array_equal(outs[0], dev[0].cpu().numpy())
+    assert np.array_equal(outs[1], dev[1].cpu().numpy())
+    o = oracle.forward(prob)
+    assert np.abs(outs[0].astype(np.float64) - o["y"]).max() <= TOL[prec]
