@@ -282,7 +282,8 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
             cudaMalloc(&p->d_bprime, bp_elems * sizeof(float)) != cudaSuccess ||
             cudaMemset(p->d_xbuf, 0, p->xbuf_words * 8) != cudaSuccess ||
             cudaMemset(p->d_status, 0, sizeof(int32_t)) != cudaSuccess ||
-            cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaDeviceSynchronize() != cudaSuccess) {  // memsets complete before any non-blocking stream
             free_device(p);
             delete p;
             return SRNN_ERR_CUDA;
@@ -549,6 +550,8 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
         if (le != 0) return SRNN_ERR_CUDA;
         p->regs = regs;
         if (maxb < 1) return SRNN_ERR_NOT_ON_CHIP;
+        if (preload_projection_kernels() != 0 || preload_gemm_f32() != 0) return SRNN_ERR_CUDA;
+        if (cudaDeviceSynchronize() != cudaSuccess) return SRNN_ERR_CUDA;  // uploads visible to every stream
     }
     p->loaded = true;
     return SRNN_OK;
@@ -735,6 +738,8 @@ srnn_status_t srnn_forward_host(srnn_plan_t p, int32_t T, int32_t B, const float
             cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&p->ev_rec, cudaEventDisableTiming) != cudaSuccess)
             return SRNN_ERR_CUDA;
+        // the memsets above run on the legacy stream; the non-blocking streams below must see them
+        if (cudaDeviceSynchronize() != cudaSuccess) return SRNN_ERR_CUDA;
     }
     cudaStream_t st = p->stream;
     const size_t hb = static_cast<size_t>(B) * H * 4;

@@ -217,6 +217,17 @@ int launch_f32_to_f16_padded(const float* in, void* out, int64_t rows, int cols,
     return static_cast<int>(cudaGetLastError());
 }
 
+// Force module loading of the projection kernels (CUDA lazy loading would
+// otherwise load them at first launch, which can stall behind a running
+// persistent kernel that is waiting for their output).
+int preload_projection_kernels() {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, f32_to_f16_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, f32_to_f16_padded_kernel);
+    return static_cast<int>(e);
+}
+
 size_t gemm_tc_smem_bytes() { return 2 * TC_STAGES * TC_TILE_BYTES + 1024 /* align */ + 256 /* barriers */; }
 
 int launch_f32_to_f16(const float* in, void* out, int64_t n, void* stream) {

@@ -72,6 +72,8 @@ int launch_gemm_f32(const GemmParams& p, void* stream);
 int launch_gemm_tc(const void* map_a, const void* map_b, const float* bias, float* C, int M, int N, int K,
                    void* stream, int m_off = 0);  // rows [m_off, m_off + M) of A and C
 int launch_f32_to_f16(const float* in, void* out, int64_t n, void* stream);
+int preload_projection_kernels();
+int preload_gemm_f32();
 int launch_f32_to_f16_padded(const float* in, void* out, int64_t rows, int cols, int ld_out, void* stream);
 
 // Compiled register-slot instances (pairs per lane); 96 exists only for the
