@@ -53,6 +53,19 @@ def dense_graph_us(H, B, T):
     return 1000 * t_events(g.replay) / T
 
 
+def cudnn_rnn_us(H, B, T):
+    """torch.nn.RNN (cuDNN, fp16, ReLU, dense): the library's per-layer RNN, which may use
+    cuDNN's persistent kernels -- the paper's 'dense persistent' comparator (PAPER.md:138)."""
+    rnn = torch.nn.RNN(H, H, nonlinearity="relu").cuda().half()
+    x = torch.rand(T, B, H, device="cuda", dtype=torch.float16)
+    with torch.no_grad():
+        rnn(x)
+        ms = t_events(lambda: rnn(x), reps=3)
+    # the layer includes the input projection: report it separately-timed GEMM-free estimate is not
+    # possible through the module, so this is the whole layer (an upper bound for its recurrence)
+    return 1000 * ms / T
+
+
 def cusparse_us(prob, B, T):
     H = prob["H"]
     crow = torch.from_numpy(prob["rowptr"]).long()
@@ -73,19 +86,28 @@ def cusparse_us(prob, B, T):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--experiment", default="c3", choices=["c3", "e4", "e5"],
+                    help="c3: hidden x batch x density grid; e4: constant nnz 1.32M (PAPER.md:161); "
+                         "e5: load-balanced vs unbalanced pruning at 2304 @ 25% (PAPER.md:188)")
     a = ap.parse_args()
     T = 256
-    Hs = [1152, 1792, 2304, 4096, 5760] if not a.quick else [1792, 2304]
-    ds = [0.01, 0.05, 0.10, 0.30]
-    Bs = [1, 4, 16] if not a.quick else [4]
+    if a.experiment == "c3":
+        Hs = [1152, 1792, 2304, 4096, 5760] if not a.quick else [1792, 2304]
+        ds = [0.01, 0.05, 0.10, 0.30]
+        Bs = [1, 4, 16] if not a.quick else [4]
+        points = [(H, B, d, "unstructured") for H in Hs for B in Bs for d in ds]
+    elif a.experiment == "e4":  # constant nnz = 2304^2 * 0.25 = 11520^2 * 0.01 = 1,327,104
+        points = [(H, 4, 1327104 / (H * H), "unstructured") for H in (2304, 3072, 4096, 5760, 7168, 9216, 11520)]
+    else:  # E5: row-balanced vs unbalanced at 2304 @ 25%, B = 4
+        points = [(2304, 4, 0.25, "unstructured"), (2304, 4, 0.25, "row_balanced"),
+                  (1024, 4, 0.125, "unstructured"), (1024, 4, 0.125, "row_balanced")]
     dense_cache = {}
-    for H in Hs:
-        for B in Bs:
-            for d in ds:
-                rec = {"H": H, "B": B, "density": d, "T": T}
+    cudnn_cache = {}
+    for H, B, d, pattern in points:
+                rec = {"H": H, "B": B, "density": d, "T": T, "pattern": pattern, "experiment": a.experiment}
                 try:
                     t0 = time.time()
-                    prob = inputs.make_problem(H, H, B, T, d)
+                    prob = inputs.make_problem(H, H, B, T, d, pattern=pattern)
                     m = from_problem(prob, prec="fp16")
                     rec["plan_s"] = round(time.time() - t0, 2)
                     x = torch.from_numpy(prob["x"]).cuda()
@@ -108,6 +130,12 @@ def main():
                     if key not in dense_cache:
                         dense_cache[key] = dense_graph_us(H, B, T)
                     rec["cublas_dense_graph_us_per_step"] = dense_cache[key]
+                    if key not in cudnn_cache:
+                        try:
+                            cudnn_cache[key] = cudnn_rnn_us(H, B, T)
+                        except Exception as e:  # noqa: BLE001
+                            cudnn_cache[key] = None
+                    rec["cudnn_rnn_layer_us_per_step"] = cudnn_cache[key]
                     rec["cusparse_us_per_step"] = cusparse_us(prob, B, T)
                 except Exception as e:  # noqa: BLE001
                     rec["baseline_error"] = str(e)[:200]
