@@ -129,6 +129,7 @@ typedef struct {
     int64_t conflict_wavefronts;       /* extra wavefronts from bank conflicts in that CTA (L)        */
     int64_t smem_weight_bytes_per_cta; /* shared-memory weight tier (pairs beyond the register slots) (L) */
     int64_t image_slots_per_lane;      /* register + shared-memory slots per lane in the image (L)     */
+    int64_t model_cycles_per_step;     /* planner's cost-model estimate of one timestep, SM cycles (L) */
 } srnn_plan_info_t;
 
 /* Create a plan for the layer described by *cfg.

@@ -57,7 +57,7 @@ class PlanInfo(ctypes.Structure):
                [(n, ctypes.c_int64) for n in
                 ("nnz", "slots_total", "smem_bytes_per_cta", "weight_image_bytes", "wavefronts_per_step_max",
                  "wavefronts_per_step_ideal", "conflict_wavefronts", "smem_weight_bytes_per_cta",
-                 "image_slots_per_lane")]
+                 "image_slots_per_lane", "model_cycles_per_step")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

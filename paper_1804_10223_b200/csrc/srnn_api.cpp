@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -32,6 +33,7 @@ struct srnn_plan {
     // layout decisions
     Layout lay;
     int np_inst = 0;   // register slots per lane (compiled instance)
+    double model_cost = 0;  // planner cost-model estimate of one timestep (SM cycles)
     int ns_slots = 0;  // shared-memory tier slots per lane
     int regs = 0;
     size_t smem_bytes = 0;
@@ -151,7 +153,7 @@ bool encode_fp16_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint6
 //              warp's dependent LDS->FMA chain)
 //   load     = poll rounds (one round trip each) + tagged-word ingress bytes
 //   reduce   = xor-butterfly latency, epilogue per item round, exchange RTT.
-double cost_model(const Layout& lay, int bt, int H, int n_tiles, bool f16) {
+double cost_model(const Layout& lay, int bt, int H, int n_tiles, bool f16, int inst) {
     const double wf = static_cast<double>(lay.wavefronts_max_cta);
     const double instr_per_slot = f16 ? (3.0 + bt) : (2.0 + bt);
     const double issue = static_cast<double>(lay.issue_max_cta) * instr_per_slot / 4.0;
@@ -161,13 +163,17 @@ double cost_model(const Layout& lay, int bt, int H, int n_tiles, bool f16) {
     const double reduce = lg * (30.0 + 2.0 * bt);
     const double words_per_unit = f16 ? (bt >= 2 ? bt / 2.0 : 1.0) : bt;
     const double chunks = static_cast<double>(H) * words_per_unit / 2.0;
-    const double k = f16 ? 8.0 : 4.0;
+    const double k = (f16 && inst <= 48) ? 8.0 : 4.0;  // LoadK<NP, F16> in srnn_recurrent.cuh
     const double groups = std::ceil(chunks / (lay.threads * k));
     const double load = groups * 900.0 + chunks * 16.0 / 48.0;
     int umax = 0;
     for (int c = 0; c < lay.num_ctas; ++c) umax = std::max(umax, lay.cta_unit0[c + 1] - lay.cta_unit0[c]);
     const double epi = std::ceil(static_cast<double>(umax) * bt / lay.threads) * 300.0;
     const double sync = lay.num_ctas > 1 ? 1200.0 : 600.0;
+    if (std::getenv("SRNN_PLAN_LOG") != nullptr)
+        std::fprintf(stderr, "srnn cost: C=%d L=%d threads=%d inst=%d wf=%.0f issue=%.0f chain=%.0f groups=%.0f "
+                     "chunks=%.0f reduce=%.0f epi=%.0f sync=%.0f tiles=%d\n", lay.num_ctas, lay.lanes_per_row,
+                     lay.threads, inst, wf, issue, chain, groups, chunks, reduce, epi, sync, n_tiles);
     return n_tiles * (std::max(std::max(wf, issue), chain) + load + reduce + epi + sync);
 }
 
@@ -317,6 +323,7 @@ srnn_status_t srnn_plan_query(srnn_plan_t p, srnn_plan_info_t* out) {
         out->smem_bytes_per_cta = static_cast<int64_t>(p->smem_bytes);
         out->smem_weight_bytes_per_cta = static_cast<int64_t>(p->ns_slots) * l.threads * (p->f16 ? 4 : 8);
         out->image_slots_per_lane = p->np_inst + p->ns_slots;
+        out->model_cycles_per_step = static_cast<int64_t>(p->model_cost);
         out->weight_image_bytes = static_cast<int64_t>(l.num_ctas) * (p->np_inst + p->ns_slots) * l.threads *
                                   (p->f16 ? 4 : 8);
         out->wavefronts_per_step_max = l.wavefronts_max_cta;
@@ -376,6 +383,7 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
     bool any = false;
     const int pair_bytes = p->f16 ? 4 : 8;
     const int P = p->E >= 4 ? 128 / p->E : 32;  // lanes per shared-memory phase
+    const bool plan_log = std::getenv("SRNN_PLAN_LOG") != nullptr;  // diagnostics: every candidate to stderr
     // Evaluate one (CTAs, lanes per row, slot budget) candidate.
     auto try_layout = [&](int C, int L, int np, int reg_cap, int64_t ns_cap) {
         Layout lay;
@@ -388,8 +396,13 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
             ns = ((su - reg_cap) + 3) & ~3;
             if (ns > ns_cap) return;
         }
-        double cst = cost_model(lay, p->BT, H, p->n_tiles_max, p->f16);
+        double cst = cost_model(lay, p->BT, H, p->n_tiles_max, p->f16, inst);
         if (ns > 0) cst += static_cast<double>(ns) * lay.warps * 2.0;  // weight LDS + issue per smem slot
+        cst += 2.0 * inst;  // tie-break toward the smaller register instance (code size)
+        if (plan_log)
+            std::fprintf(stderr, "srnn plan: C=%d L=%d np=%d slots=%d inst=%d ns=%d threads=%d wf=%lld issue=%lld cost=%.0f\n",
+                         C, L, np, su, inst, ns, lay.threads, static_cast<long long>(lay.wavefronts_max_cta),
+                         static_cast<long long>(lay.issue_max_cta), cst);
         if (cst < best_cost) {
             best_cost = cst;
             best = std::move(lay);
@@ -472,6 +485,7 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
     p->smem_bytes = smem_for(p, umax, p->BT, p->n_tiles_max) + 16 +
                     static_cast<size_t>(best_ns) * fin.threads * pair_bytes;
     p->np_inst = best_inst;
+    p->model_cost = best_cost;
     p->ns_slots = best_ns;
     p->lay = std::move(fin);
     p->nnz = nnz;
