@@ -12,6 +12,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/srnn.h"
@@ -66,8 +68,10 @@ struct srnn_plan {
     uint32_t* d_ready = nullptr;     // b' rows ready (monotone counter)
     uint32_t* d_progress = nullptr;  // per-CTA progress increments (monotone counter)
     uint32_t ready_base = 0, progress_base = 0;
-    cudaStream_t s_rec = nullptr, s_out = nullptr;
+    cudaStream_t s_rec = nullptr, s_out = nullptr, s_copy = nullptr;
     cudaEvent_t ev_in = nullptr, ev_rec = nullptr;
+    cudaEvent_t ev_chunk[10] = {};  // x chunk c resident (s_copy -> projection stream)
+    int32_t* h_status = nullptr;     // pinned: status read back on s_out at the end of a call
 };
 
 namespace {
@@ -122,6 +126,11 @@ void free_device(srnn_plan* p) {
     cudaFree(p->d_progress);
     if (p->s_rec) cudaStreamDestroy(p->s_rec);
     if (p->s_out) cudaStreamDestroy(p->s_out);
+    if (p->s_copy) cudaStreamDestroy(p->s_copy);
+    if (p->h_status) cudaFreeHost(p->h_status);
+    p->h_status = nullptr;
+    for (cudaEvent_t& ev : p->ev_chunk)
+        if (ev) cudaEventDestroy(ev);
     if (p->ev_in) cudaEventDestroy(p->ev_in);
     if (p->ev_rec) cudaEventDestroy(p->ev_rec);
     if (p->stream) cudaStreamDestroy(p->stream);
@@ -129,7 +138,7 @@ void free_device(srnn_plan* p) {
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
-bool encode_fp16_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k_pad) {
+bool encode_fp16_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k_pad, uint32_t box_rows) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         void* fn = nullptr;
@@ -140,7 +149,7 @@ bool encode_fp16_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint6
     }
     cuuint64_t dims[2] = {k_pad, rows};
     cuuint64_t strides[1] = {k_pad * 2};
-    cuuint32_t box[2] = {64, 128};  // 64 fp16 = one 128-byte swizzle row, 128 rows (srnn_gemm_tc.cu)
+    cuuint32_t box[2] = {64, box_rows};  // 64 fp16 = one 128-byte swizzle row (srnn_gemm_tc.cu)
     cuuint32_t estr[2] = {1, 1};
     return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -368,7 +377,12 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
     if (p->cfg.num_ctas > 0) {
         cands_c.push_back(p->cfg.num_ctas);
     } else {
-        const int cmax = std::min(p->sm_count - ((p->cfg.flags & SRNN_FLAG_RESERVE_SMS) ? 4 : 0), H);
+        int reserve = 0;
+        if (p->cfg.flags & SRNN_FLAG_RESERVE_SMS) {
+            reserve = 4;
+            if (const char* r = std::getenv("SRNN_RESERVE_SMS")) reserve = std::max(1, std::min(p->sm_count / 2, std::atoi(r)));
+        }
+        const int cmax = std::max(1, std::min(p->sm_count - reserve, H));
         cands_c.push_back(cmax);
         for (int cc = cmax / 2; cc >= 1; cc /= 2) cands_c.push_back(cc);
     }
@@ -543,8 +557,9 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
             e = cudaMalloc(&p->d_wx16, w16.size() * 2);
             if (e == cudaSuccess) e = cudaMemcpy(p->d_wx16, w16.data(), w16.size() * 2, cudaMemcpyHostToDevice);
             if (e == cudaSuccess) e = cudaMalloc(&p->d_x16, xrows * p->k_pad * 2);
-            if (e == cudaSuccess && (!encode_fp16_kmajor(&p->map_wx16, p->d_wx16, R, p->k_pad) ||
-                                     !encode_fp16_kmajor(&p->map_x16, p->d_x16, xrows, p->k_pad)))
+            // A (x) in 128-row boxes, B (W_x) in 64-row boxes (tile widths 128 / 192 / 256)
+            if (e == cudaSuccess && (!encode_fp16_kmajor(&p->map_wx16, p->d_wx16, R, p->k_pad, 64) ||
+                                     !encode_fp16_kmajor(&p->map_x16, p->d_x16, xrows, p->k_pad, 128)))
                 return SRNN_ERR_CUDA;
         }
         if (e == cudaSuccess) e = cudaMalloc(&p->d_bias, static_cast<size_t>(R) * 4);
@@ -572,7 +587,9 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
 }
 
 // b' rows [r0, r0 + M) from x rows [r0, r0 + M) (x, bprime: full device buffers).
-static srnn_status_t project_rows(srnn_plan_t p, int64_t r0, int64_t M, const float* x, float* bprime, void* stream) {
+// `sms`: SMs the projection can use (all of them, or the few the pipelined forward leaves free)
+static srnn_status_t project_rows(srnn_plan_t p, int64_t r0, int64_t M, const float* x, float* bprime, void* stream,
+                                  int sms) {
     const int I = p->cfg.input, N = p->G * p->cfg.hidden;
     if (M <= 0) return SRNN_OK;
     if (p->tc_gemm) {
@@ -581,7 +598,7 @@ static srnn_status_t project_rows(srnn_plan_t p, int64_t r0, int64_t M, const fl
                               : launch_f32_to_f16_padded(x + r0 * I, x16, M, I, p->k_pad, stream);
         if (e == 0)
             e = launch_gemm_tc(&p->map_x16, &p->map_wx16, p->d_bias, bprime, static_cast<int>(M), N, p->k_pad, stream,
-                               static_cast<int>(r0));
+                               static_cast<int>(r0), 0, sms);
         return e == 0 ? SRNN_OK : SRNN_ERR_CUDA;
     }
     GemmParams gp;
@@ -602,7 +619,7 @@ srnn_status_t srnn_input_projection(srnn_plan_t p, int32_t T, int32_t B, const f
         return SRNN_ERR_INVALID_VALUE;
     if (T == 0) return SRNN_OK;
     DeviceGuard g(p->cfg.device);
-    return project_rows(p, 0, static_cast<int64_t>(T) * B, x, bprime, stream);
+    return project_rows(p, 0, static_cast<int64_t>(T) * B, x, bprime, stream, p->sm_count);
 }
 
 struct PipeArgs {
@@ -750,8 +767,12 @@ srnn_status_t srnn_forward_host(srnn_plan_t p, int32_t T, int32_t B, const float
             cudaStreamCreateWithFlags(&p->s_rec, cudaStreamNonBlocking) != cudaSuccess ||
             cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&p->ev_rec, cudaEventDisableTiming) != cudaSuccess)
+            cudaEventCreateWithFlags(&p->ev_rec, cudaEventDisableTiming) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&p->s_copy, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaMallocHost(&p->h_status, sizeof(int32_t)) != cudaSuccess)
             return SRNN_ERR_CUDA;
+        for (cudaEvent_t& ev : p->ev_chunk)
+            if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return SRNN_ERR_CUDA;
         // the memsets above run on the legacy stream; the non-blocking streams below must see them
         if (cudaDeviceSynchronize() != cudaSuccess) return SRNN_ERR_CUDA;
     }
@@ -778,57 +799,122 @@ srnn_status_t srnn_forward_host(srnn_plan_t p, int32_t T, int32_t B, const float
     // ---- pipelined: stream `st` copies + projects x chunk by chunk on the free SMs and
     // bumps d_ready; s_rec runs the persistent kernel, which waits per step for its b'
     // rows; s_out copies y chunks back as the kernel's progress counter passes them ----
-    const int n_chunks = std::min(8, T);
-    const int every = (T + n_chunks - 1) / n_chunks;  // steps per chunk (input and output)
+    // input chunks: up to 8, each a whole number of 128-row GEMM tiles where the
+    // batch allows (a partial tile costs the projection as much as a full one)
+    int in_b[10] = {0};
+    int n_chunks = 0;
+    {
+        const int q = std::max(1, 128 / B);  // steps per 128 rows
+        int per = (T + 7) / 8;
+        per = ((per + q - 1) / q) * q;
+        for (int s0 = 0; s0 < T && n_chunks < 8; s0 += per) in_b[++n_chunks] = std::min(T, s0 + per);
+        in_b[n_chunks] = T;
+    }
+    // output chunks: 16 even ones (the last one's copy is the exposed tail)
+    const int every = (T + std::min(16, T) - 1) / std::min(16, T);
+    const int n_out = (T + every - 1) / every;
     const uint32_t ready_base = p->ready_base, prog_base = p->progress_base;
     if (h0_host) e = cudaMemcpyAsync(p->d_h0, h0_host, hb, cudaMemcpyHostToDevice, p->s_rec);
     if (e == cudaSuccess && c0_host && p->G == 4) e = cudaMemcpyAsync(p->d_c0, c0_host, hb, cudaMemcpyHostToDevice, p->s_rec);
     if (e != cudaSuccess) return SRNN_ERR_CUDA;
+    // SRNN_PIPE_TRACE: timing events at every stage, printed to stderr (diagnostics)
+    static const bool trace = std::getenv("SRNN_PIPE_TRACE") != nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> tr;
+    auto mark = [&](const std::string& label, cudaStream_t where) {
+        if (!trace) return;
+        cudaEvent_t ev;
+        cudaEventCreate(&ev);
+        cudaEventRecord(ev, where);
+        tr.emplace_back(label, ev);
+    };
+    mark("start", p->s_copy);
+    // x chunks stream in on their own copy stream (one event each), so the copy
+    // engine runs ahead of the projections instead of alternating with them.
+    // Chunk 0 is enqueued first: the host's enqueue time is on the critical path.
+    auto copy_chunk = [&](int c) -> srnn_status_t {
+        const int s0 = in_b[c], s1 = in_b[c + 1];
+        const int64_t r0 = static_cast<int64_t>(s0) * B, nr = static_cast<int64_t>(s1 - s0) * B;
+        if (cudaMemcpyAsync(p->d_x + r0 * I, x_host + r0 * I, static_cast<size_t>(nr) * I * 4, cudaMemcpyHostToDevice,
+                            p->s_copy) != cudaSuccess ||
+            cudaEventRecord(p->ev_chunk[c], p->s_copy) != cudaSuccess)
+            return SRNN_ERR_CUDA;
+        mark("x" + std::to_string(c) + " in", p->s_copy);
+        return SRNN_OK;
+    };
+    // chunk c: projection once its x rows are resident, then d_ready = base + (its last step + 1)
+    auto feed_chunk = [&](int c, int sms) -> srnn_status_t {
+        const int s0 = in_b[c], s1 = in_b[c + 1];
+        const int64_t r0 = static_cast<int64_t>(s0) * B, nr = static_cast<int64_t>(s1 - s0) * B;
+        if (cudaStreamWaitEvent(st, p->ev_chunk[c], 0) != cudaSuccess) return SRNN_ERR_CUDA;
+        srnn_status_t fs = project_rows(p, r0, nr, p->d_x, p->d_bprime, st, sms);
+        if (fs != SRNN_OK) return fs;
+        mark("b'" + std::to_string(c) + " ready", st);
+        if (g_write32(st, reinterpret_cast<CUdeviceptr>(p->d_ready), ready_base + static_cast<uint32_t>(s1),
+                      CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+            return SRNN_ERR_CUDA;
+        return SRNN_OK;
+    };
+    // The first chunk is projected on every SM before the persistent kernel
+    // starts; the others on the SMs it leaves free, while it runs.
+    srnn_status_t s = copy_chunk(0);
+    if (s == SRNN_OK) s = feed_chunk(0, p->sm_count);
+    if (s != SRNN_OK) return s;
+    if (cudaEventRecord(p->ev_in, st) != cudaSuccess || cudaStreamWaitEvent(p->s_rec, p->ev_in, 0) != cudaSuccess)
+        return SRNN_ERR_CUDA;
     PipeArgs pa;
     pa.bp_ready = p->d_ready;
     pa.bp_ready_base = ready_base;
     pa.progress = y_host ? p->d_progress : nullptr;
     pa.every = every;
-    srnn_status_t s = recurrence_impl(p, T, B, p->d_bprime, h0_host ? p->d_h0 : nullptr,
-                                      c0_host ? p->d_c0 : nullptr, y_host ? p->d_y : nullptr, p->d_hT,
-                                      p->G == 4 ? p->d_cT : nullptr, p->s_rec, pa);
+    mark("kernel launch", p->s_rec);
+    s = recurrence_impl(p, T, B, p->d_bprime, h0_host ? p->d_h0 : nullptr, c0_host ? p->d_c0 : nullptr,
+                        y_host ? p->d_y : nullptr, p->d_hT, p->G == 4 ? p->d_cT : nullptr, p->s_rec, pa);
     if (s != SRNN_OK) return s;
+    mark("kernel done", p->s_rec);
     if (cudaEventRecord(p->ev_rec, p->s_rec) != cudaSuccess) return SRNN_ERR_CUDA;
-    for (int c = 0; c < n_chunks; ++c) {
-        const int s0 = c * every, s1 = std::min(T, s0 + every);
-        if (s0 >= s1) break;
-        const int64_t r0 = static_cast<int64_t>(s0) * B, nr = static_cast<int64_t>(s1 - s0) * B;
-        e = cudaMemcpyAsync(p->d_x + r0 * I, x_host + r0 * I, static_cast<size_t>(nr) * I * 4, cudaMemcpyHostToDevice, st);
-        if (e != cudaSuccess) return SRNN_ERR_CUDA;
-        s = project_rows(p, r0, nr, p->d_x, p->d_bprime, st);
+    for (int c = 1; c < n_chunks; ++c) {
+        s = copy_chunk(c);
         if (s != SRNN_OK) return s;
-        if (g_write32(st, reinterpret_cast<CUdeviceptr>(p->d_ready), ready_base + static_cast<uint32_t>(s1),
-                      CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
-            return SRNN_ERR_CUDA;
+    }
+    for (int c = 1; c < n_chunks; ++c) {
+        s = feed_chunk(c, p->sm_count - p->lay.num_ctas);
+        if (s != SRNN_OK) return s;
     }
     (void)GH;
     if (y_host) {
         const uint32_t C = static_cast<uint32_t>(p->lay.num_ctas);
-        for (int c = 0; c < n_chunks; ++c) {
+        for (int c = 0; c < n_out; ++c) {
             const int s0 = c * every, s1 = std::min(T, s0 + every);
-            if (s0 >= s1) break;
             if (g_wait32(p->s_out, reinterpret_cast<CUdeviceptr>(p->d_progress), prog_base + C * static_cast<uint32_t>(c + 1),
                          CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
                 return SRNN_ERR_CUDA;
             const size_t r0 = static_cast<size_t>(s0) * B, nr = static_cast<size_t>(s1 - s0) * B;
             e = cudaMemcpyAsync(y_host + r0 * H, p->d_y + r0 * H, nr * H * 4, cudaMemcpyDeviceToHost, p->s_out);
             if (e != cudaSuccess) return SRNN_ERR_CUDA;
+            mark("y" + std::to_string(c) + " out", p->s_out);
         }
-        p->progress_base = prog_base + C * static_cast<uint32_t>((T + every - 1) / every);
+        p->progress_base = prog_base + C * static_cast<uint32_t>(n_out);
     }
     p->ready_base = ready_base + static_cast<uint32_t>(T) + 1;
     e = cudaStreamWaitEvent(p->s_out, p->ev_rec, 0);
     if (e == cudaSuccess && hT_host) e = cudaMemcpyAsync(hT_host, p->d_hT, hb, cudaMemcpyDeviceToHost, p->s_out);
     if (e == cudaSuccess && cT_host && p->G == 4) e = cudaMemcpyAsync(cT_host, p->d_cT, hb, cudaMemcpyDeviceToHost, p->s_out);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(p->h_status, p->d_status, 4, cudaMemcpyDeviceToHost, p->s_out);
     if (e == cudaSuccess) e = cudaStreamSynchronize(p->s_out);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return SRNN_ERR_CUDA;
-    return srnn_plan_status(p);
+    mark("end", p->s_out);
+    if (trace) {
+        cudaDeviceSynchronize();
+        for (auto& t : tr) {
+            float ms = 0.0f;
+            cudaEventElapsedTime(&ms, tr[0].second, t.second);
+            std::fprintf(stderr, "srnn pipe: %8.1f us  %s\n", 1000.0 * ms, t.first.c_str());
+        }
+        for (auto& t : tr) cudaEventDestroy(t.second);
+    }
+    if (*p->h_status != 0) return srnn_plan_status(p);  // reads and clears it
+    return SRNN_OK;
 }
 
 srnn_status_t srnn_plan_status(srnn_plan_t p) {

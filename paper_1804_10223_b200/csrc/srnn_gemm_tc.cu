@@ -7,11 +7,17 @@
 //     b'[m][n] = bias[n] + sum_k x16[m][k] * Wx16[n][k]     (fp16 in, fp32 accumulate)
 //
 // x (fp32, [T*B][I]) is first rounded to fp16 (RNE) by a small kernel; W_x is
-// rounded once at srnn_load_weights.  One CTA computes a 128 x 128 output
-// tile with tcgen05.mma (cta_group::1, kind::f16, M=128 N=128 K=16) from
-// shared-memory operands staged by TMA (cp.async.bulk.tensor, 128-byte
-// swizzle, 4-stage mbarrier pipeline); the accumulator lives in TMEM and is
-// read back by four epilogue warps with tcgen05.ld, + bias, stored as fp32.
+// rounded once at srnn_load_weights.  One CTA computes a 128 x BN output
+// tile (BN = 128 or 256) with tcgen05.mma (cta_group::1, kind::f16, M=128
+// N=BN K=16) from shared-memory operands staged by TMA (cp.async.bulk.tensor,
+// 128-byte swizzle, mbarrier ring of 192 KB: 6 stages at BN = 128, 4 at 256);
+// the accumulator lives in TMEM and is read back by four epilogue warps with
+// tcgen05.ld, + bias, stored as fp32.  The kernel is persistent over tiles
+// (grid = min(tiles, SMs it may use)) with two TMEM accumulators, so the
+// epilogue of one tile overlaps the loads and MMAs of the next.  BN = 256 halves the re-reads of the x tile and carries 1.5x
+// the bytes in flight per SM: it is used when the 128 x 128 grid would not fill
+// the SMs anyway (e.g. the per-chunk projections of the pipelined
+// srnn_forward_host, which run on the few SMs the persistent kernel leaves free).
 //
 //   warp 0: TMA producer (one elected lane)    warp 1: TMEM alloc + MMA issuer
 //   warps 2-5: epilogue (TMEM lane quarter = warp % 4)
@@ -19,14 +25,16 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "srnn_internal.h"
 
 namespace srnn {
 namespace {
 
-constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 64, TC_STAGES = 4, TC_THREADS = 192;
-constexpr uint32_t TC_TILE_BYTES = TC_BM * TC_BK * 2;  // 16 KB per operand tile
-constexpr uint32_t TC_TMEM_COLS = 128;
+constexpr int TC_BM = 128, TC_BK = 64, TC_STAGES = 4, TC_THREADS = 192;
+constexpr uint32_t TC_TILE_BYTES = TC_BM * TC_BK * 2;  // 16 KB: one 128-row operand box
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -58,39 +66,64 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
            ((1024ull >> 4) << 32) /* SBO */ | (1ull << 46) /* sm100 descriptor version */ |
            (2ull << 61) /* SWIZZLE_128B */;
 }
-// Instruction descriptor, kind::f16: D f32, A/B f16, both K-major, M = 128, N = 128.
-constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | ((TC_BN >> 3) << 17) | ((TC_BM >> 4) << 24);
+// Instruction descriptor, kind::f16: D f32, A/B f16, both K-major, M = 128, N = BN.
+template <int BN>
+__host__ __device__ constexpr uint32_t idesc_f16() {
+    return (1u << 4) | (0u << 7) | (0u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+           (static_cast<uint32_t>(TC_BM >> 4) << 24);
+}
 
+template <int BN>
+struct TcCfg {
+    static constexpr uint32_t B_BYTES = BN * TC_BK * 2;  // BN/64 boxes of 64 rows, 8-row groups 1 KB apart
+    static constexpr int STAGES = static_cast<int>((200u * 1024u) / (TC_TILE_BYTES + B_BYTES));  // ~200 KB in flight
+    static constexpr uint32_t STAGE_BYTES = TC_TILE_BYTES + B_BYTES;
+    static constexpr uint32_t TMEM_COLS = BN == 128 ? 256 : 512;  // two accumulators (power-of-2 allocation)
+    static constexpr size_t SMEM = STAGES * STAGE_BYTES + 1024 /* align */ + 256 /* barriers */;
+};
+
+// Persistent over output tiles: CTA b takes tiles b, b + gridDim.x, ... (n-fastest).
+// The producer and the MMA issuer run ahead into the next tile while the
+// epilogue warps drain the other TMEM accumulator.
+template <int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_f16_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                        const float* __restrict__ bias, float* __restrict__ C, int M, int N, int K, int m_off) {
+    using Cfg = TcCfg<BN>;
+    constexpr int STAGES = Cfg::STAGES;
+    constexpr uint32_t kIdesc = idesc_f16<BN>();
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for the 128B-swizzled operand tiles
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* sA = smem;
-    unsigned char* sB = smem + TC_STAGES * TC_TILE_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * TC_STAGES * TC_TILE_BYTES);
-    uint64_t* empty = full + TC_STAGES;
-    uint64_t* tmem_full = empty + TC_STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    unsigned char* sB = smem + STAGES * TC_TILE_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;  // [2] accumulator ready for the epilogue
+    uint64_t* tempty = tfull + 2;      // [2] accumulator drained by the 4 epilogue warps
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * TC_BN;  // rows relative to m_off
     const int nk = (K + TC_BK - 1) / TC_BK;
+    const int tiles_n = (N + BN - 1) / BN;
+    const int n_tiles = tiles_n * ((M + TC_BM - 1) / TC_BM);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < TC_STAGES; ++s) {
+        for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
     }
     if (warp == 1) {  // TMEM allocation (whole warp)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
-                     "r"(TC_TMEM_COLS)
+                     "r"(Cfg::TMEM_COLS)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
@@ -101,76 +134,101 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
     if (warp == 0 && lane == 0) {
         // ---- TMA producer ----
-        for (int kb = 0; kb < nk; ++kb) {
-            const int s = kb % TC_STAGES;
-            if (kb >= TC_STAGES) mbar_wait(&empty[s], ((kb / TC_STAGES) - 1) & 1);
-            mbar_expect_tx(&full[s], 2 * TC_TILE_BYTES);
-            tma_load_2d(sA + s * TC_TILE_BYTES, &map_a, &full[s], kb * TC_BK, m_off + m0);
-            tma_load_2d(sB + s * TC_TILE_BYTES, &map_b, &full[s], kb * TC_BK, n0);
+        int it = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            const int m0 = (t / tiles_n) * TC_BM, n0 = (t % tiles_n) * BN;
+            for (int kb = 0; kb < nk; ++kb, ++it) {
+                const int s = it % STAGES;
+                if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+                mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
+                tma_load_2d(sA + s * TC_TILE_BYTES, &map_a, &full[s], kb * TC_BK, m_off + m0);
+#pragma unroll
+                for (int j = 0; j < BN / 64; ++j)  // rows past N are zero-filled by TMA
+                    tma_load_2d(sB + s * Cfg::B_BYTES + j * (TC_TILE_BYTES / 2), &map_b, &full[s], kb * TC_BK,
+                                n0 + 64 * j);
+            }
         }
     } else if (warp == 1 && lane == 0) {
-        // ---- MMA issuer: D[tmem] (+)= A[smem] * B[smem]^T ----
-        for (int kb = 0; kb < nk; ++kb) {
-            const int s = kb % TC_STAGES;
-            mbar_wait(&full[s], (kb / TC_STAGES) & 1);
+        // ---- MMA issuer: D[tmem acc] (+)= A[smem] * B[smem]^T ----
+        int it = 0, lt = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+            const int acc = lt & 1;
+            if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint64_t da = smem_desc_sw128(sA + s * TC_TILE_BYTES);
-            const uint64_t db = smem_desc_sw128(sB + s * TC_TILE_BYTES);
+            const uint32_t d_tmem = tmem + static_cast<uint32_t>(acc * BN);
+            for (int kb = 0; kb < nk; ++kb, ++it) {
+                const int s = it % STAGES;
+                mbar_wait(&full[s], (it / STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint64_t da = smem_desc_sw128(sA + s * TC_TILE_BYTES);
+                const uint64_t db = smem_desc_sw128(sB + s * Cfg::B_BYTES);
 #pragma unroll
-            for (int k = 0; k < TC_BK / 16; ++k) {
-                const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
-                // advance 16 fp16 (32 bytes) along K inside the swizzled row: +2 in the >>4 address field
-                asm volatile(
-                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                    "l"(da + 2ull * k), "l"(db + 2ull * k), "r"(kIdesc), "r"(accum)
-                    : "memory");
+                for (int k = 0; k < TC_BK / 16; ++k) {
+                    const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
+                    // advance 16 fp16 (32 bytes) along K inside the swizzled row: +2 in the >>4 address field
+                    asm volatile(
+                        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+                        "l"(da + 2ull * k), "l"(db + 2ull * k), "r"(kIdesc), "r"(accum)
+                        : "memory");
+                }
+                // free the smem stage once these MMAs have read it
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 su32(&empty[s]))
+                             : "memory");
             }
-            // free the smem stage once these MMAs have read it
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             su32(&empty[s]))
+                             su32(&tfull[acc]))
                          : "memory");
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         su32(tmem_full))
-                     : "memory");
     } else if (warp >= 2) {
         // ---- epilogue: TMEM -> registers -> + bias -> global ----
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
-        const int row = m0 + quarter * 32 + lane;
-        mbar_wait(tmem_full, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        int lt = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+            const int acc = lt & 1;
+            const int m0 = (t / tiles_n) * TC_BM, n0 = (t % tiles_n) * BN;
+            const int row = m0 + quarter * 32 + lane;
+            mbar_wait(&tfull[acc], (lt >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
-        for (int c = 0; c < TC_BN; c += 32) {
-            uint32_t v[32];
-            const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(c);
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (row < M) {
-                float* crow = C + static_cast<size_t>(m_off + row) * N + n0 + c;
-                const int nvalid = min(32, N - (n0 + c));
-                if (nvalid == 32 && (N & 3) == 0) {
+            for (int c = 0; c < BN; c += 32) {
+                uint32_t v[32];
+                const uint32_t taddr =
+                    tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN + c);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (c + 32 >= BN) {  // last chunk read: hand the accumulator back to the MMA issuer
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&tempty[acc])) : "memory");
+                }
+                if (row < M) {
+                    float* crow = C + static_cast<size_t>(m_off + row) * N + n0 + c;
+                    const int nvalid = min(32, N - (n0 + c));
+                    if (nvalid == 32 && (N & 3) == 0) {
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        float4 o;
-                        o.x = __uint_as_float(v[j + 0]) + (bias ? __ldg(bias + n0 + c + j + 0) : 0.0f);
-                        o.y = __uint_as_float(v[j + 1]) + (bias ? __ldg(bias + n0 + c + j + 1) : 0.0f);
-                        o.z = __uint_as_float(v[j + 2]) + (bias ? __ldg(bias + n0 + c + j + 2) : 0.0f);
-                        o.w = __uint_as_float(v[j + 3]) + (bias ? __ldg(bias + n0 + c + j + 3) : 0.0f);
-                        *reinterpret_cast<float4*>(crow + j) = o;
+                        for (int j = 0; j < 32; j += 4) {
+                            float4 o;
+                            o.x = __uint_as_float(v[j + 0]) + (bias ? __ldg(bias + n0 + c + j + 0) : 0.0f);
+                            o.y = __uint_as_float(v[j + 1]) + (bias ? __ldg(bias + n0 + c + j + 1) : 0.0f);
+                            o.z = __uint_as_float(v[j + 2]) + (bias ? __ldg(bias + n0 + c + j + 2) : 0.0f);
+                            o.w = __uint_as_float(v[j + 3]) + (bias ? __ldg(bias + n0 + c + j + 3) : 0.0f);
+                            *reinterpret_cast<float4*>(crow + j) = o;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (j < nvalid) crow[j] = __uint_as_float(v[j]) + (bias ? __ldg(bias + n0 + c + j) : 0.0f);
                     }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (j < nvalid) crow[j] = __uint_as_float(v[j]) + (bias ? __ldg(bias + n0 + c + j) : 0.0f);
                 }
             }
         }
@@ -179,7 +237,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::TMEM_COLS)
                      : "memory");
     }
 }
@@ -222,13 +280,13 @@ int launch_f32_to_f16_padded(const float* in, void* out, int64_t rows, int cols,
 // persistent kernel that is waiting for their output).
 int preload_projection_kernels() {
     cudaFuncAttributes a;
-    cudaError_t e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel);
+    cudaError_t e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel<128>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel<192>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel<256>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, f32_to_f16_kernel);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, f32_to_f16_padded_kernel);
     return static_cast<int>(e);
 }
-
-size_t gemm_tc_smem_bytes() { return 2 * TC_STAGES * TC_TILE_BYTES + 1024 /* align */ + 256 /* barriers */; }
 
 int launch_f32_to_f16(const float* in, void* out, int64_t n, void* stream) {
     if (n <= 0) return 0;
@@ -238,21 +296,53 @@ int launch_f32_to_f16(const float* in, void* out, int64_t n, void* stream) {
     return static_cast<int>(cudaGetLastError());
 }
 
-int launch_gemm_tc(const void* map_a, const void* map_b, const float* bias, float* C, int M, int N, int K,
-                   void* stream, int m_off) {
-    if (M <= 0 || N <= 0) return 0;
+template <int BN>
+static int launch_gemm_tc_bn(const void* map_a, const void* map_b, const float* bias, float* C, int M, int N, int K,
+                             cudaStream_t stream, int m_off, int sms) {
     static bool attr_set = false;
-    const size_t smem = gemm_tc_smem_bytes();
+    const size_t smem = TcCfg<BN>::SMEM;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_tc_f16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(gemm_tc_f16_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return static_cast<int>(e);
         attr_set = true;
     }
-    dim3 grid((N + TC_BN - 1) / TC_BN, (M + TC_BM - 1) / TC_BM);
-    gemm_tc_f16_kernel<<<grid, TC_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(
-        *static_cast<const CUtensorMap*>(map_a), *static_cast<const CUtensorMap*>(map_b), bias, C, M, N, K, m_off);
+    const int64_t tiles = static_cast<int64_t>((N + BN - 1) / BN) * ((M + TC_BM - 1) / TC_BM);
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
+    gemm_tc_f16_kernel<BN><<<grid, TC_THREADS, smem, stream>>>(*static_cast<const CUtensorMap*>(map_a),
+                                                               *static_cast<const CUtensorMap*>(map_b), bias, C, M, N,
+                                                               K, m_off);
     return static_cast<int>(cudaGetLastError());
+}
+
+// bn = 128, 192 or 256; 0 picks the width that minimises the operand bytes of
+// the busiest CTA: ceil(tiles / sms) x (128 + bn) rows of K -- 128 when the
+// 128-wide grid fits in one wave, wider when the launch has few SMs (the
+// pipelined projections on the SMs the persistent kernel leaves free).
+int launch_gemm_tc(const void* map_a, const void* map_b, const float* bias, float* C, int M, int N, int K,
+                   void* stream, int m_off, int bn, int sms) {
+    if (M <= 0 || N <= 0) return 0;
+    if (const char* e = std::getenv("SRNN_GEMM_SMS")) sms = std::atoi(e);  // experiment: cap the grid
+    sms = std::max(1, sms);
+    if (bn == 0) {
+        const int64_t tm = (M + TC_BM - 1) / TC_BM;
+        int64_t best = -1;
+        for (int w : {128, 192, 256}) {
+            const int64_t tiles = tm * ((N + w - 1) / w);
+            const int64_t cost = ((tiles + sms - 1) / sms) * (128 + w);
+            if (best < 0 || cost < best) {
+                best = cost;
+                bn = w;
+            }
+        }
+        if (const char* e = std::getenv("SRNN_GEMM_BN")) bn = std::atoi(e);
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch (bn) {
+        case 192: return launch_gemm_tc_bn<192>(map_a, map_b, bias, C, M, N, K, st, m_off, sms);
+        case 256: return launch_gemm_tc_bn<256>(map_a, map_b, bias, C, M, N, K, st, m_off, sms);
+        default: return launch_gemm_tc_bn<128>(map_a, map_b, bias, C, M, N, K, st, m_off, sms);
+    }
 }
 
 }  // namespace srnn

@@ -70,7 +70,8 @@ int launch_recurrent(int np, int bt, int g, int f16, const RecParams& p, int num
 int launch_gemm_f32(const GemmParams& p, void* stream);
 // fp16 tensor-core input GEMM (srnn_gemm_tc.cu); maps are CUtensorMap*.
 int launch_gemm_tc(const void* map_a, const void* map_b, const float* bias, float* C, int M, int N, int K,
-                   void* stream, int m_off = 0);  // rows [m_off, m_off + M) of A and C
+                   void* stream, int m_off = 0, int bn = 0, int sms = 148);
+// rows [m_off, m_off + M) of A and C; bn = tile width (0: pick from the grid size vs `sms`, the SMs it may use)
 int launch_f32_to_f16(const float* in, void* out, int64_t n, void* stream);
 int preload_projection_kernels();
 int preload_gemm_f32();

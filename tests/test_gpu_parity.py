@@ -177,11 +177,15 @@ def test_input_projection_alone(cuda_device):
 
 @pytest.mark.parametrize("H,I,B,T,cell", [(384, 200, 3, 7, "rnn"), (200, 100, 3, 5, "rnn"), (2304, 2304, 4, 256, "rnn"),
                                         (130, 64, 2, 9, "lstm"), (1024, 1024, 4, 100, "lstm")])
-def test_input_projection_tensor_cores(cuda_device, H, I, B, T, cell):
+@pytest.mark.parametrize("bn", ["auto", "128", "192", "256"])
+def test_input_projection_tensor_cores(cuda_device, monkeypatch, H, I, B, T, cell, bn):
     """fp16 mode: tcgen05 GEMM on fp16-rounded x and W_x, fp32 accumulate.
     Against the oracle fed the same fp16-rounded operands (fp32 vs fp64
-    accumulation only) and against the unquantised oracle (fp16 rounding)."""
+    accumulation only) and against the unquantised oracle (fp16 rounding).
+    bn: output tile width 128 / 192 / 256 forced (ragged N: TMA zero-fills rows past N)."""
     import torch
+    if bn != "auto":
+        monkeypatch.setenv("SRNN_GEMM_BN", bn)
     prob = inputs.make_problem(H, I, B, T, 0.05, cell=cell)
     m = from_problem(prob, prec="fp16")
     bp = m.input_projection(torch.from_numpy(prob["x"]).cuda())
@@ -299,7 +303,8 @@ def test_C5_shape_sampled_and_partition(cuda_device):
 
 
 @pytest.mark.parametrize("prec,cell,B,T", [("fp16", "rnn", 4, 37), ("fp32", "rnn", 3, 16), ("fp16", "lstm", 2, 9),
-                                           ("fp16", "rnn", 4, 1)])
+                                           ("fp16", "rnn", 4, 1), ("fp16", "rnn", 4, 2), ("fp16", "rnn", 4, 256),
+                                           ("fp32", "lstm", 3, 33)])
 def test_forward_host_pipelined(cuda_device, prec, cell, B, T):
     """SRNN_FLAG_RESERVE_SMS: srnn_forward_host projects x chunks on the free SMs while
     the persistent kernel runs and copies y back by progress -- same bits as the
