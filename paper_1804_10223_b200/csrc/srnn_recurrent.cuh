@@ -77,12 +77,29 @@ __device__ __forceinline__ float val_of(unsigned long long w) {
 
 // g(.) of Eq. 1/2. Accurate libdevice transcendentals (no
 // fast-math: the fp32 parity bound is 1e-5).
+// Transcendentals.  FAST (the fp16-staged path) uses the SFU's tanh.approx.f32
+// (relative error ~2^-11, the same order as the fp16 rounding every h goes
+// through before the exchange) and sigma(z) = 0.5 + 0.5 tanh(z / 2); the fp32
+// path keeps the accurate libm forms (reading R14).
+__device__ __forceinline__ float tanh_approx(float z) {
+    float r;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(z));
+    return r;
+}
+template <bool FAST>
+__device__ __forceinline__ float tanh_g(float z) {
+    return FAST ? tanh_approx(z) : tanhf(z);
+}
+template <bool FAST>
+__device__ __forceinline__ float sigmoid_g(float z) {
+    return FAST ? fmaf(0.5f, tanh_approx(0.5f * z), 0.5f) : 1.0f / (1.0f + expf(-z));
+}
+template <bool FAST>
 __device__ __forceinline__ float activation(int act, float z) {
     if (act == 0) return fmaxf(z, 0.0f);
-    if (act == 1) return tanhf(z);
+    if (act == 1) return tanh_g<FAST>(z);
     return z;
 }
-__device__ __forceinline__ float sigmoidf_acc(float z) { return 1.0f / (1.0f + expf(-z)); }
 
 // Spin-wait bookkeeping of one loader thread.
 struct Watchdog {
@@ -661,7 +678,7 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                 // fast path (one item per thread, RNN): addresses hoisted out of the time loop
                 float h = 0.0f;
                 if (e1_ok) {
-                    h = activation(act, zs_e1[0] + bps[e1]);
+                    h = activation<F16>(act, zs_e1[0] + bps[e1]);
                     const int bg = k * BT + e1_b;
                     if (bg < p.B) {
                         if (y_e1 != nullptr) y_e1[(static_cast<size_t>(s - 1) * p.B + k * BT) * H] = h;
@@ -677,7 +694,7 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                 if (ok) {
                     const int unit = u0 + e / BT, bg = k * BT + e % BT;
                     if (G == 1) {
-                        h = activation(p.act, zs[e] + bps[e]);
+                        h = activation<F16>(p.act, zs[e] + bps[e]);
                     } else {
                         const int ub = U * BT;
                         const float zi = zs[0 * ub + e] + bps[e * G + 0];
@@ -685,9 +702,9 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                         const float zg = zs[2 * ub + e] + bps[e * G + 2 % G];
                         const float zo = zs[3 * ub + e] + bps[e * G + 3 % G];
                         float* cp = &cs[k * umax_bt + e];
-                        const float c = sigmoidf_acc(zf) * (*cp) + sigmoidf_acc(zi) * tanhf(zg);
+                        const float c = sigmoid_g<F16>(zf) * (*cp) + sigmoid_g<F16>(zi) * tanh_g<F16>(zg);
                         *cp = c;
-                        h = sigmoidf_acc(zo) * tanhf(c);
+                        h = sigmoid_g<F16>(zo) * tanh_g<F16>(c);
                         if (s == p.T && p.cT != nullptr && bg < p.B) p.cT[static_cast<size_t>(bg) * H + unit] = c;
                     }
                     if (bg < p.B) {

@@ -10,6 +10,10 @@
 //   a2a_sent      poll one sentinel word per producer, then one bulk read
 //   a2a_relacq    raw data + st.release flag per producer; ld.acquire flag,
 //                 then plain bulk read of the raw data (half the bytes)
+//   a2a_cluster<CS>  thread-block clusters of CS CTAs: each CTA polls 1/CS of
+//                 the chunks from L2 and forwards them into every cluster
+//                 peer's shared memory (DSMEM, double-buffered), then one
+//                 cluster barrier -- L2 polling traffic / CS
 //
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mb scripts/microbench_exchange.cu
 // run:   ./mb [units_per_cta=16] [words_per_unit=2] [steps=2000]
@@ -182,6 +186,102 @@ __global__ void k_a2a_relacq(Args a) {
     if (acc == 12345) sink = acc;
 }
 
+// cluster forwarding: CTA r of a CS-cluster polls chunks c with c % CS == r, writes each fresh
+// chunk into hs[(s & 1)] of all CS CTAs (DSMEM), then barrier.cluster (release/acquire).
+template <int CS>
+__global__ void k_a2a_cluster(Args a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    namespace cgx = cooperative_groups;
+    cgx::cluster_group cl = cgx::this_cluster();
+    const int rank = static_cast<int>(cl.block_rank());
+    const int n = gridDim.x;
+    const int per = a.upc * a.wpu;
+    const int total = n * per;
+    const int chunks = total / 2;
+    ulonglong2* hs0 = reinterpret_cast<ulonglong2*>(smem);
+    ulonglong2* peer[CS];
+    for (int r = 0; r < CS; ++r) peer[r] = cl.map_shared_rank(hs0, r);
+    unsigned long long acc = 0;
+    for (int s = 1; s <= a.steps; ++s) {
+        unsigned long long* dst = a.words + static_cast<size_t>(s & 1) * total;
+        for (int i = threadIdx.x; i < per; i += blockDim.x)
+            st_relaxed(dst + blockIdx.x * per + i, (static_cast<unsigned long long>(s) << 32) | i);
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(dst);
+        const int boff = (s & 1) * chunks;
+        const int mine = (chunks - rank + CS - 1) / CS;  // chunks rank, rank + CS, ...
+        for (int base = threadIdx.x; base < mine; base += 8 * blockDim.x) {
+            ulonglong2 v[8];
+            unsigned pend = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                int idx = base + j * blockDim.x;
+                if (idx < mine) {
+                    v[j] = ld_relaxed_v2(src + idx * CS + rank);
+                    pend |= 1u << j;
+                }
+            }
+            while (pend) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if ((pend >> j & 1) && (v[j].x >> 32) == static_cast<unsigned long long>(s) &&
+                        (v[j].y >> 32) == static_cast<unsigned long long>(s)) {
+                        const int c = (base + j * blockDim.x) * CS + rank;
+#pragma unroll
+                        for (int r = 0; r < CS; ++r) peer[r][boff + c] = v[j];
+                        pend &= ~(1u << j);
+                    }
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (pend >> j & 1) v[j] = ld_relaxed_v2(src + (base + j * blockDim.x) * CS + rank);
+            }
+        }
+        cl.sync();
+        acc += hs0[boff + threadIdx.x].x;
+    }
+    if (acc == 12345) a.out[1] = acc;
+}
+
+static float run_cluster(void* fn, Args a, int grid, int block, int cs, size_t smem) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (cs > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg);
+    if (ncl * cs < grid) {
+        printf(", \"cluster%d_max_active_clusters\": %d", cs, ncl);
+        return -1.0f;
+    }
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    void* args[] = {&a};
+    for (int rep = 0; rep < 2; ++rep) {
+        cudaMemset(a.words, 0, static_cast<size_t>(2) * 148 * 64 * 8 * 8);
+        cudaDeviceSynchronize();
+        cudaEventRecord(e0);
+        cudaError_t err = cudaLaunchKernelExC(&cfg, fn, args);
+        cudaEventRecord(e1);
+        if (err == cudaSuccess) err = cudaDeviceSynchronize();
+        if (err != cudaSuccess) {
+            printf(", \"cluster%d_error\": \"%s\"", cs, cudaGetErrorString(err));
+            return -1.0f;
+        }
+    }
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    return ms * 1000.0f / a.steps;
+}
+
 static float run(void* fn, Args a, int grid, int block) {
     void* args[] = {&a};
     cudaEvent_t e0, e1;
@@ -228,6 +328,18 @@ int main(int argc, char** argv) {
         printf(", \"a2a_bulk_tagged_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_bulk), a, ncta, blk));
         printf(", \"a2a_sentinel_then_bulk_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_sent), a, ncta, blk));
         printf(", \"a2a_release_acquire_raw_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_relacq), a, ncta, blk));
+    }
+    {
+        const size_t smem = static_cast<size_t>(2) * ncta * a.upc * a.wpu * 8;
+        for (int cs : {2, 4, 8}) {
+            const int grid = (ncta / cs) * cs;
+            void* fn = cs == 2 ? reinterpret_cast<void*>(k_a2a_cluster<2>)
+                     : cs == 4 ? reinterpret_cast<void*>(k_a2a_cluster<4>) : reinterpret_cast<void*>(k_a2a_cluster<8>);
+            Args b = a;
+            b.upc = a.upc * ncta / grid + (a.upc * ncta % grid ? 1 : 0);  // same h size on fewer CTAs
+            printf(", \"a2a_cluster%d_ctas\": %d, \"a2a_cluster%d_us\": %.4f", cs, grid, cs,
+                   run_cluster(fn, b, grid, 512, cs, smem + 4096));
+        }
     }
     printf(", \"bytes_tagged_per_cta\": %d, \"bytes_raw_per_cta\": %d}\n", ncta * a.upc * a.wpu * 8, ncta * a.upc * 8);
     return 0;

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--d", type=float, default=0.3)
     ap.add_argument("--T", type=int, default=256)
     ap.add_argument("--cell", default="rnn")
+    ap.add_argument("--pattern", default="unstructured")
     ap.add_argument("--prec", default="fp16")
     ap.add_argument("--L", type=int, default=0)
     ap.add_argument("--C", type=int, default=0)
@@ -33,7 +34,7 @@ def main():
         os.environ["SRNN_BT"] = str(a.bt)
     if a.delay >= 0:
         os.environ["SRNN_POLL_DELAY_NS"] = str(a.delay)
-    prob = inputs.make_problem(a.H, a.H, a.B, a.T, a.d, cell=a.cell)
+    prob = inputs.make_problem(a.H, a.H, a.B, a.T, a.d, cell=a.cell, pattern=a.pattern)
     m = from_problem(prob, prec=a.prec, flags=a.flags, num_ctas=a.C, lanes_per_row=a.L)
     x = torch.from_numpy(prob["x"]).cuda()
     bp = m.input_projection(x)

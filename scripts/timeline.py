@@ -21,6 +21,7 @@ ap.add_argument("--d", type=float, default=0.3)
 ap.add_argument("--T", type=int, default=256)
 ap.add_argument("--prec", default="fp16")
 ap.add_argument("--cell", default="rnn")
+ap.add_argument("--pattern", default="unstructured")
 ap.add_argument("--L", type=int, default=0)
 ap.add_argument("--C", type=int, default=0)
 ap.add_argument("--bt", type=int, default=0)
@@ -28,7 +29,7 @@ ap.add_argument("--flags", type=int, default=0)
 a = ap.parse_args()
 if a.bt:
     os.environ["SRNN_BT"] = str(a.bt)
-prob = inputs.make_problem(a.H, a.H, a.B, a.T, a.d, cell=a.cell)
+prob = inputs.make_problem(a.H, a.H, a.B, a.T, a.d, cell=a.cell, pattern=a.pattern)
 m = from_problem(prob, prec=a.prec, flags=a.flags | FLAG_PROFILE, num_ctas=a.C, lanes_per_row=a.L)
 x = torch.from_numpy(prob["x"]).cuda()
 for _ in range(3):
