@@ -261,14 +261,15 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
         if (v == 1 || v == 2 || v == 4 || (v == 8 && p->f16)) bt = v;
     }
     while (bt > 1 && bt > c.batch) bt /= 2;
-    // fp16 register pairs carry the hs byte offset in 16 bits: H * E <= 65536
-    while (p->f16 && bt > 1 && static_cast<int64_t>(c.hidden) * elem_bytes(true, bt) > 65536) bt /= 2;
-    if (p->f16 && static_cast<int64_t>(c.hidden) * elem_bytes(true, bt) > 65536) {
+    // fp16 register pairs carry the hs offset in 16 bits: bytes for BT <= 4
+    // (H * E <= 65536), 16-byte units for BT = 8 (the column index, any H)
+    const int umax_guess = (c.hidden + p->sm_count - 1) / p->sm_count;
+    while (bt > 1 && smem_for(p, umax_guess, bt, (c.batch + bt - 1) / bt) > static_cast<size_t>(p->smem_optin)) bt /= 2;
+    while (p->f16 && bt > 1 && bt < 8 && static_cast<int64_t>(c.hidden) * elem_bytes(true, bt) > 65536) bt /= 2;
+    if (p->f16 && bt < 8 && static_cast<int64_t>(c.hidden) * elem_bytes(true, bt) > 65536) {
         delete p;
         return SRNN_ERR_UNSUPPORTED;
     }
-    const int umax_guess = (c.hidden + p->sm_count - 1) / p->sm_count;
-    while (bt > 1 && smem_for(p, umax_guess, bt, (c.batch + bt - 1) / bt) > static_cast<size_t>(p->smem_optin)) bt /= 2;
     p->BT = bt;
     p->E = elem_bytes(p->f16, bt);
     p->n_tiles_max = (c.batch + bt - 1) / bt;
@@ -521,7 +522,8 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
         if (p->f16) {
             std::vector<uint32_t> img(n);
             for (size_t i = 0; i < n; ++i)
-                img[i] = (static_cast<uint32_t>(l.col[i] * p->E) << 16) | float_to_half_rne(l.val[i]);
+                img[i] = (static_cast<uint32_t>(p->BT >= 8 ? l.col[i] * (p->E / 16) : l.col[i] * p->E) << 16) |
+                         float_to_half_rne(l.val[i]);
             e = cudaMalloc(&p->d_img, n * 4);
             if (e == cudaSuccess) e = cudaMemcpy(p->d_img, img.data(), n * 4, cudaMemcpyHostToDevice);
         } else {

@@ -294,6 +294,9 @@ struct Weights<NP, BT, false> {
     }
 };
 
+// F16 register pair: high 16 bits = hs offset of the column, low 16 bits = fp16
+// weight.  The offset is in bytes for BT <= 4 (E <= 8, H * E <= 64 KB) and in
+// 16-byte units for BT = 8 (E = 16: the column index itself, any H <= 65536).
 template <int NP, int BT>
 struct Weights<NP, BT, true> {
     static constexpr int GS = BT >= 4 ? 4 : 8;
@@ -310,7 +313,7 @@ struct Weights<NP, BT, true> {
                     uint4 h[GS];
 #pragma unroll
                     for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) h[j] = *reinterpret_cast<const uint4*>(hs + (pw[i0 + j] >> 16));
+                        if (i0 + j < NP) h[j] = *reinterpret_cast<const uint4*>(hs + ((pw[i0 + j] >> 12) & 0xffff0u));
 #pragma unroll
                     for (int j = 0; j < GS; ++j) {
                         if (i0 + j < NP) {
@@ -383,7 +386,7 @@ __device__ __forceinline__ void operate_smem_tier(float (&acc)[BT], const unsign
             if (BT == 8) {
                 uint4 h[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) h[j] = *reinterpret_cast<const uint4*>(hs + (wv[j] >> 16));
+                for (int j = 0; j < 4; ++j) h[j] = *reinterpret_cast<const uint4*>(hs + ((wv[j] >> 12) & 0xffff0u));
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     acc[0] = fma_f16f16f32(wv[j], h[j].x, acc[0]);

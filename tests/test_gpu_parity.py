@@ -273,9 +273,18 @@ def test_capacity_large_hidden_on_chip(cuda_device, H, d):
     print(H, d, g["info"])
 
 
+@pytest.mark.parametrize("H,B,d", [(6000, 8, 0.01), (4100, 11, 0.02), (9000, 8, 0.004)])
+def test_bt8_beyond_byte_offsets(cuda_device, H, B, d):
+    """fp16 BT = 8 past H * 16 B > 64 KB: the register pair carries the column in
+    16-byte units (the byte offset would not fit 16 bits); every output checked."""
+    prob = inputs.make_problem(H, 64, B, 5, d, act="tanh", h0="random", seed_offset=H)
+    g, o, err = check(prob, "fp16")
+    assert g["info"]["batch_tile"] == 8
+
+
 def test_C5_shape_sampled_and_partition(cuda_device):
-    """C5 layer (H=5760, d=10%, B=64, fp16): the shared-memory weight tier and 16
-    batch tiles; samples 0 and 63 checked against the oracle (sampled outputs,
+    """C5 layer (H=5760, d=10%, B=64, fp16): the shared-memory weight tier and 8
+    batch tiles of 8; samples 0 and 63 checked against the oracle (sampled outputs,
     T shortened to 24 for the CPU side), and the 8-way batch partition of the
     same plan is bit-identical to the full batch."""
     import torch
