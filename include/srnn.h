@@ -102,7 +102,7 @@ typedef struct {
     uint32_t flags;     /* SRNN_FLAG_* bits                                              */
     int32_t num_ctas;   /* 0 = planner's choice; else force this CTA count (<= SMs)     */
     int32_t lanes_per_row; /* 0 = planner's choice; else 1,2,4,8,16 or 32              */
-    int32_t batch_tile; /* 0 = planner's choice; else 1, 2 or 4 samples staged per h tile */
+    int32_t batch_tile; /* 0 = planner's choice; else 1, 2, 4 (fp32) or 1..16 (fp16) samples per h tile */
 } srnn_config_t;
 
 /* What the planner decided (srnn_plan_query). Fields marked (L) are final
@@ -114,7 +114,7 @@ typedef struct {
     int32_t lanes_per_row;     /* L: lanes cooperating on one row (L)                        */
     int32_t pairs_per_lane;    /* NP: register slots per lane = compiled instance (L)        */
     int32_t slots_used;        /* max slots actually used by any warp (<= NP) (L)            */
-    int32_t batch_tile;        /* BT: samples staged per smem h tile (1, 2 or 4)             */
+    int32_t batch_tile;        /* BT: samples staged per smem h tile (1, 2, 4; fp16 also 8, 16) */
     int32_t num_batch_tiles;   /* ceil(B_max / BT)                                           */
     int32_t units_per_cta_max; /* hidden units owned by the largest CTA (L)                  */
     int32_t regs_per_thread;   /* compiled register count of the chosen kernel instance (L)  */

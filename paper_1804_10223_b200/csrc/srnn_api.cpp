@@ -89,9 +89,9 @@ struct DeviceGuard {
     }
 };
 
-int inst_for(int slots, bool f16) {
+int inst_for(int slots, bool f16, int bt) {
     for (int i = 0; i < kNumNP; ++i)
-        if (kNPList[i] >= slots && kNPList[i] <= max_np(f16)) return kNPList[i];
+        if (kNPList[i] >= slots && kNPList[i] <= max_np(f16, bt)) return kNPList[i];
     return -1;
 }
 
@@ -163,7 +163,7 @@ bool encode_fp16_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint6
 //   load     = poll rounds (one round trip each) + tagged-word ingress bytes
 //   reduce   = xor-butterfly latency, epilogue per item round, exchange RTT.
 double cost_model(const Layout& lay, int bt, int H, int n_tiles, bool f16, int inst) {
-    const double wf = static_cast<double>(lay.wavefronts_max_cta);
+    const double wf = static_cast<double>(lay.wavefronts_max_cta) * (bt == 16 ? 2 : 1);
     const double instr_per_slot = f16 ? (3.0 + bt) : (2.0 + bt);
     const double issue = static_cast<double>(lay.issue_max_cta) * instr_per_slot / 4.0;
     const double chain = lay.slots_used * 11.0;
@@ -219,7 +219,8 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
         (c.lanes_per_row < 1 || c.lanes_per_row > 32 || (c.lanes_per_row & (c.lanes_per_row - 1)) != 0))
         return SRNN_ERR_INVALID_VALUE;
     if (c.num_ctas < 0) return SRNN_ERR_INVALID_VALUE;
-    if (c.batch_tile != 0 && c.batch_tile != 1 && c.batch_tile != 2 && c.batch_tile != 4 && c.batch_tile != 8)
+    if (c.batch_tile != 0 && c.batch_tile != 1 && c.batch_tile != 2 && c.batch_tile != 4 && c.batch_tile != 8 &&
+        c.batch_tile != 16)
         return SRNN_ERR_INVALID_VALUE;
 
     srnn_plan* p = new (std::nothrow) srnn_plan();
@@ -253,12 +254,13 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     p->f16 = c.prec == SRNN_PREC_FP16W_FP32ACC && (c.flags & SRNN_FLAG_FP32_STAGING) == 0;
     // Batch tile: the paper's wide load interleaves 4 samples.
     int bt = c.batch >= 4 ? 4 : (c.batch >= 2 ? 2 : 1);
-    if (p->f16 && c.batch >= 8) bt = 8;  // fp16: 8 samples per LDS.128 (one exchange round for B = 8)
-    if (c.batch_tile == 1 || c.batch_tile == 2 || c.batch_tile == 4 || (c.batch_tile == 8 && p->f16))
+    if (p->f16 && c.batch >= 8) bt = 8;    // fp16: 8 samples per LDS.128 (one exchange round for B = 8)
+    if (p->f16 && c.batch >= 16) bt = 16;  // fp16: two planes of 8 (every extra tile costs a whole exchange)
+    if (c.batch_tile == 1 || c.batch_tile == 2 || c.batch_tile == 4 || ((c.batch_tile == 8 || c.batch_tile == 16) && p->f16))
         bt = c.batch_tile;
     if (const char* e = std::getenv("SRNN_BT")) {  // experiment override: batch tile width
         const int v = std::atoi(e);
-        if (v == 1 || v == 2 || v == 4 || (v == 8 && p->f16)) bt = v;
+        if (v == 1 || v == 2 || v == 4 || ((v == 8 || v == 16) && p->f16)) bt = v;
     }
     while (bt > 1 && bt > c.batch) bt /= 2;
     // fp16 register pairs carry the hs offset in 16 bits: bytes for BT <= 4
@@ -336,9 +338,10 @@ srnn_status_t srnn_plan_query(srnn_plan_t p, srnn_plan_info_t* out) {
         out->model_cycles_per_step = static_cast<int64_t>(p->model_cost);
         out->weight_image_bytes = static_cast<int64_t>(l.num_ctas) * (p->np_inst + p->ns_slots) * l.threads *
                                   (p->f16 ? 4 : 8);
-        out->wavefronts_per_step_max = l.wavefronts_max_cta;
-        out->wavefronts_per_step_ideal = l.wavefronts_ideal_cta;
-        out->conflict_wavefronts = l.conflicts_max_cta;
+        const int planes = p->BT == 16 ? 2 : 1;  // two LDS.128 per pair at BT = 16
+        out->wavefronts_per_step_max = l.wavefronts_max_cta * planes;
+        out->wavefronts_per_step_ideal = l.wavefronts_ideal_cta * planes;
+        out->conflict_wavefronts = l.conflicts_max_cta * planes;
     }
     return SRNN_OK;
 }
@@ -370,10 +373,11 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
     in.col = col;
     in.val = qval.data();
     in.BT = p->BT;
-    in.E = p->E;
+    in.E = p->BT == 16 ? 16 : p->E;  // BT = 16 gathers two 16-byte planes: the bank model of BT = 8, twice
     in.naive = (p->cfg.flags & SRNN_FLAG_NAIVE_LAYOUT) != 0;
 
     // ---- search (num_ctas, lanes_per_row, slot budget) ----
+search_again:
     std::vector<int> cands_c;
     if (p->cfg.num_ctas > 0) {
         cands_c.push_back(p->cfg.num_ctas);
@@ -404,7 +408,7 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
         Layout lay;
         if (!pack_layout(in, C, L, np, &lay)) return;
         const int su = std::max(1, lay.slots_used);
-        int inst = inst_for(su, p->f16);
+        int inst = inst_for(su, p->f16, p->BT);
         int ns = 0;
         if (inst < 0 || inst > reg_cap) {  // registers + shared-memory tier
             inst = reg_cap;
@@ -449,7 +453,7 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
             if (threads > 1024) continue;
             int reg_cap = -1;  // largest register instance whose thread cap admits this CTA size
             for (int i = 0; i < kNumNP; ++i)
-                if (kNPList[i] <= max_np(p->f16) && threads <= max_threads_for(kNPList[i], p->f16)) reg_cap = kNPList[i];
+                if (kNPList[i] <= max_np(p->f16, p->BT) && threads <= max_threads_for(kNPList[i], p->f16, p->BT)) reg_cap = kNPList[i];
             if (reg_cap < 0) continue;
             if (std::getenv("SRNN_FORCE_SMEM_TIER") != nullptr) reg_cap = kNPList[0];  // test hook
             const int64_t ns_cap =
@@ -469,6 +473,15 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
             for (int extra : {1, 2, 4, std::max(1, f.np0 / 8), std::max(2, f.np0 / 4)})
                 try_layout(f.C, f.L, f.np0 + extra, f.reg_cap, f.ns_cap);
         }
+    }
+    if (!any && p->f16 && p->BT == 16 && p->cfg.batch_tile != 16) {
+        // the 16-sample tile's h staging left no room for the weights: 8-sample tiles
+        p->BT = 8;
+        p->E = elem_bytes(true, 8);
+        p->n_tiles_max = (p->cfg.batch + 7) / 8;  // exchange words: ceil(B/8)*4H <= ceil(B/16)*8H, xbuf fits
+        in.BT = 8;
+        in.E = 16;
+        goto search_again;
     }
     if (!any) return SRNN_ERR_NOT_ON_CHIP;
     // Re-pack at the chosen instance width so the image has np_inst slots.
@@ -522,7 +535,7 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
         if (p->f16) {
             std::vector<uint32_t> img(n);
             for (size_t i = 0; i < n; ++i)
-                img[i] = (static_cast<uint32_t>(p->BT >= 8 ? l.col[i] * (p->E / 16) : l.col[i] * p->E) << 16) |
+                img[i] = (static_cast<uint32_t>(p->BT >= 8 ? l.col[i] : l.col[i] * p->E) << 16) |
                          float_to_half_rne(l.val[i]);
             e = cudaMalloc(&p->d_img, n * 4);
             if (e == cudaSuccess) e = cudaMemcpy(p->d_img, img.data(), n * 4, cudaMemcpyHostToDevice);

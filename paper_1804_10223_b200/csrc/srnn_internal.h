@@ -82,8 +82,12 @@ int launch_f32_to_f16_padded(const float* in, void* out, int64_t rows, int cols,
 constexpr int kNumNP = 9;
 constexpr int kNPList[kNumNP] = {4, 8, 12, 16, 24, 32, 48, 64, 96};
 inline int max_np(bool f16) { return f16 ? 96 : 64; }
-// Must match MaxThreads<NP, F16> in srnn_recurrent.cuh.
-inline int max_threads_for(int np, bool f16) {
+// largest register instance compiled with the 16-sample tile (fp16, two hs planes)
+constexpr int kMaxNP16 = 48;
+inline int max_np(bool f16, int bt) { return bt == 16 ? kMaxNP16 : max_np(f16); }
+// Must match MaxThreadsBT<NP, F16, BT> in srnn_recurrent.cuh.
+inline int max_threads_for(int np, bool f16, int bt = 1) {
+    if (f16 && bt == 16) return np <= 4 ? 640 : np <= 8 ? 512 : np <= 16 ? 384 : 256;
     if (f16) return np <= 12 ? 640 : np <= 32 ? 512 : np <= 64 ? 384 : 256;
     return np <= 4 ? 768 : np <= 12 ? 640 : np <= 32 ? 512 : np <= 48 ? 384 : 256;
 }

@@ -135,10 +135,16 @@ struct Fmt {
     static constexpr int E = F16 ? 2 * BT : 4 * BT;            // hs bytes per unit
     static constexpr int CHUNK_HS = (F16 && BT == 1) ? 4 : 8;  // hs bytes per 16-byte chunk
 
-    // store chunk `idx` (words w0, w1; w1 valid iff has1) into hs
+    // store chunk `idx` (words w0, w1; w1 valid iff has1) into hs.  BT = 16 (fp16)
+    // stages two planes of 8 samples, [2][H][8] fp16 (`ps` = plane stride H * 16 B),
+    // so each 16-byte gather stays LDS.128-aligned like BT = 8.
     __device__ __forceinline__ static void store(unsigned char* hs, int idx, unsigned long long w0,
-                                                 unsigned long long w1, bool has1) {
-        if (F16 && BT == 1) {
+                                                 unsigned long long w1, bool has1, int ps = 0) {
+        if (F16 && BT == 16) {
+            const int q = idx & 3;
+            unsigned char* d = hs + (q >> 1) * ps + (idx >> 2) * 16 + (q & 1) * 8;
+            *reinterpret_cast<uint2*>(d) = make_uint2(static_cast<uint32_t>(w0), static_cast<uint32_t>(w1));
+        } else if (F16 && BT == 1) {
             const uint32_t lo = static_cast<uint32_t>(w0) & 0xffffu;
             if (has1)
                 *reinterpret_cast<uint32_t*>(hs + 4 * idx) = lo | (static_cast<uint32_t>(w1) << 16);
@@ -163,7 +169,7 @@ template <bool F16, int BT, int K>
 __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, unsigned char* hs, int n_words,
                                           uint32_t want, bool spin, int32_t* status,
                                           unsigned long long timeout_ns, uint32_t backoff_ns = 0,
-                                          int loaders = 0) {
+                                          int loaders = 0, int ps = 0) {
     const int n_chunks = (n_words + 1) >> 1;
     const int nt = loaders > 0 ? min(loaders, static_cast<int>(blockDim.x)) : static_cast<int>(blockDim.x);
     Watchdog wd{0ull, 0u};
@@ -184,7 +190,7 @@ __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, un
             for (int j = 0; j < K; ++j) {
                 if ((pend >> j) & 1u) {
                     if ((tag_of(v[j].x) == want) & (tag_of(v[j].y) == want)) {
-                        Fmt<F16, BT>::store(hs, base + j * nt, v[j].x, v[j].y, true);
+                        Fmt<F16, BT>::store(hs, base + j * nt, v[j].x, v[j].y, true, ps);
                         pend &= ~(1u << j);
                     }
                 }
@@ -249,7 +255,8 @@ struct Weights<NP, BT, false> {
             }
         }
     }
-    __device__ __forceinline__ void operate(float (&acc)[BT], const unsigned char* hs, int n_w) const {
+    __device__ __forceinline__ void operate(float (&acc)[BT], const unsigned char* hs, int n_w,
+                                            const unsigned char* = nullptr) const {
 #pragma unroll
         for (int i0 = 0; i0 < NP; i0 += GS) {
             if (i0 < n_w) {
@@ -299,17 +306,41 @@ struct Weights<NP, BT, false> {
 // 16-byte units for BT = 8 (E = 16: the column index itself, any H <= 65536).
 template <int NP, int BT>
 struct Weights<NP, BT, true> {
-    static constexpr int GS = BT >= 4 ? 4 : 8;
+    static constexpr int GS = BT == 16 ? 2 : BT >= 4 ? 4 : 8;
     uint32_t pw[NP];
     __device__ __forceinline__ void load(const RecParams& p, size_t img0, int n_w) {
 #pragma unroll
         for (int i = 0; i < NP; ++i) pw[i] = i < n_w ? p.img_f16[img0 + static_cast<size_t>(i) * p.threads] : 0u;
     }
-    __device__ __forceinline__ void operate(float (&acc)[BT], const unsigned char* hs, int n_w) const {
+    // hs2: the second sample plane (BT = 16 only)
+    __device__ __forceinline__ void operate(float (&acc)[BT], const unsigned char* hs, int n_w,
+                                            const unsigned char* hs2 = nullptr) const {
 #pragma unroll
         for (int i0 = 0; i0 < NP; i0 += GS) {
             if (i0 < n_w) {
-                if (BT == 8) {
+                if (BT == 16) {
+                    uint4 ha[GS], hb[GS];
+#pragma unroll
+                    for (int j = 0; j < GS; ++j) {
+                        if (i0 + j < NP) {
+                            const uint32_t o = (pw[i0 + j] >> 12) & 0xffff0u;
+                            ha[j] = *reinterpret_cast<const uint4*>(hs + o);
+                            hb[j] = *reinterpret_cast<const uint4*>(hs2 + o);
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < GS; ++j) {
+                        if (i0 + j < NP) {
+                            const uint32_t wv = pw[i0 + j];
+                            const uint32_t hv[8] = {ha[j].x, ha[j].y, ha[j].z, ha[j].w, hb[j].x, hb[j].y, hb[j].z, hb[j].w};
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                acc[(2 * q) % BT] = fma_f16f16f32(wv, hv[q], acc[(2 * q) % BT]);
+                                acc[(2 * q + 1) % BT] = fma_f16f16f32(wv, hv[q] >> 16, acc[(2 * q + 1) % BT]);
+                            }
+                        }
+                    }
+                } else if (BT == 8) {
                     uint4 h[GS];
 #pragma unroll
                     for (int j = 0; j < GS; ++j)
@@ -376,14 +407,27 @@ struct Weights<NP, BT, true> {
 // not fit the register file ("larger layer sizes").
 template <int BT, bool F16>
 __device__ __forceinline__ void operate_smem_tier(float (&acc)[BT], const unsigned char* hs, const void* ws,
-                                                  int np_reg, int n_w, int nt) {
+                                                  int np_reg, int n_w, int nt, const unsigned char* hs2 = nullptr) {
     for (int i0 = np_reg; i0 < n_w; i0 += 4) {
         if (F16) {
             const uint32_t* w32 = static_cast<const uint32_t*>(ws) + static_cast<size_t>(i0 - np_reg) * nt + threadIdx.x;
             uint32_t wv[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) wv[j] = w32[j * nt];
-            if (BT == 8) {
+            if (BT == 16) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t o = (wv[j] >> 12) & 0xffff0u;
+                    const uint4 ha = *reinterpret_cast<const uint4*>(hs + o);
+                    const uint4 hb = *reinterpret_cast<const uint4*>(hs2 + o);
+                    const uint32_t hv[8] = {ha.x, ha.y, ha.z, ha.w, hb.x, hb.y, hb.z, hb.w};
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        acc[(2 * q) % BT] = fma_f16f16f32(wv[j], hv[q], acc[(2 * q) % BT]);
+                        acc[(2 * q + 1) % BT] = fma_f16f16f32(wv[j], hv[q] >> 16, acc[(2 * q + 1) % BT]);
+                    }
+                }
+            } else if (BT == 8) {
                 uint4 h[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) h[j] = *reinterpret_cast<const uint4*>(hs + ((wv[j] >> 12) & 0xffff0u));
@@ -461,6 +505,13 @@ struct MaxThreads {
     static constexpr int value = F16 ? (NP <= 12 ? 640 : NP <= 32 ? 512 : NP <= 64 ? 384 : 256)
                                      : (NP <= 4 ? 768 : NP <= 12 ? 640 : NP <= 32 ? 512 : NP <= 48 ? 384 : 256);
 };
+// BT = 16 (fp16) holds 16 accumulators and two 16-byte gathers per slot: one
+// register tier more than the other tiles.  Must match max_threads_for().
+template <int NP, bool F16, int BT>
+struct MaxThreadsBT {
+    static constexpr int value =
+        (F16 && BT == 16) ? (NP <= 4 ? 640 : NP <= 8 ? 512 : NP <= 16 ? 384 : 256) : MaxThreads<NP, F16>::value;
+};
 template <int NP, bool F16>
 struct LoadK {
     static constexpr int value = F16 ? (NP <= 48 ? 8 : 4) : 4;
@@ -477,7 +528,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <int NP, int BT, int G, bool F16>
-__global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent_kernel(const RecParams p) {
+__global__ void __launch_bounds__(MaxThreadsBT<NP, F16, BT>::value, 1) srnn_persistent_kernel(const RecParams p) {
     using F = Fmt<F16, BT>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int H = p.H;
@@ -500,6 +551,8 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
     const int L = p.lanes_per_row;
     const int n_w = p.warp_slots[cta * (p.threads >> 5) + warp];
     const int n_words = H * F::WPR;
+    const int ps = H * 16;                      // BT = 16: second hs plane
+    const unsigned char* hs2 = hs + ps;
     const int tile_stride = (n_words + 1) & ~1;
     const int GH = G * H;
 
@@ -613,7 +666,7 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                 p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
             if (!load_tile<F16, BT, LoadK<NP, F16>::value>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
                                                             !grid_sync, p.status, p.timeout_ns, p.poll_backoff_ns,
-                                                            p.loader_threads))
+                                                            p.loader_threads, ps))
                 *s_abort = 1;
             __syncthreads();
             if (prof) prof[1] = clock64();
@@ -624,8 +677,8 @@ __global__ void __launch_bounds__(MaxThreads<NP, F16>::value, 1) srnn_persistent
                 float acc[BT];
 #pragma unroll
                 for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
-                W.operate(acc, hs, n_w);
-                if (n_w > NP) operate_smem_tier<BT, F16>(acc, hs, ws, NP, n_w, nt);
+                W.operate(acc, hs, n_w, hs2);
+                if (n_w > NP) operate_smem_tier<BT, F16>(acc, hs, ws, NP, n_w, nt, hs2);
                 if (prof) prof[4] = clock64();
                 // ---- reduce over the row's L lanes, fixed order ----
                 // L >= BT: log2(BT) halving levels (each lane keeps half of its
@@ -751,7 +804,7 @@ static int launch_one(const RecParams& p, int num_ctas, size_t smem, void* strea
             int nb = 0;
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, p.threads, smem);
             if (e != cudaSuccess) return static_cast<int>(e);
-            *max_blocks_out = p.threads > MaxThreads<NP, F16>::value ? 0 : nb;
+            *max_blocks_out = p.threads > MaxThreadsBT<NP, F16, BT>::value ? 0 : nb;
         }
     }
     if (query_only) return 0;
@@ -776,6 +829,10 @@ int launch_np(int bt, int g, const RecParams& p, int num_ctas, size_t smem, void
     if constexpr (F16) {
         SRNN_CASE(8, 1)
         SRNN_CASE(8, 4)
+        if constexpr (NP <= kMaxNP16) {
+            SRNN_CASE(16, 1)
+            SRNN_CASE(16, 4)
+        }
     }
 #undef SRNN_CASE
     return static_cast<int>(cudaErrorInvalidValue);

@@ -254,7 +254,7 @@ def test_batch_partition_bit_identical(cuda_device, world):
 
 
 @pytest.mark.parametrize("prec", ["fp32", "fp16"])
-@pytest.mark.parametrize("cell,B", [("rnn", 1), ("rnn", 4), ("rnn", 6), ("lstm", 2)])
+@pytest.mark.parametrize("cell,B", [("rnn", 1), ("rnn", 4), ("rnn", 6), ("lstm", 2), ("rnn", 16), ("lstm", 17)])
 def test_smem_weight_tier_forced(cuda_device, monkeypatch, prec, cell, B):
     """Shared-memory weight tier (a10), forced on a small layer: pairs beyond 4
     register slots per lane live in shared memory."""
@@ -271,6 +271,26 @@ def test_capacity_large_hidden_on_chip(cuda_device, H, d):
     prob = inputs.make_problem(H, 64, 1, 6, d, act="tanh", h0="random")
     g, o, err = check(prob, "fp16")
     print(H, d, g["info"])
+
+
+@pytest.mark.parametrize("cell,H,B,T,d,act", [
+    ("rnn", 333, 16, 7, 0.10, "relu"),      # one tile of 16 (two hs planes of 8)
+    ("rnn", 200, 20, 6, 0.10, "tanh"),      # ragged second tile (4 of 16)
+    ("rnn", 150, 32, 5, 0.20, "identity"),  # two full tiles
+    ("rnn", 1500, 16, 4, 0.05, "tanh"),
+    ("lstm", 200, 16, 6, 0.10, "tanh"),
+    ("lstm", 96, 19, 5, 0.30, "tanh"),
+])
+def test_batch_tile_16(cuda_device, cell, H, B, T, d, act):
+    """fp16 tiles of 16 samples (two hs planes of 8): every output against the
+    oracle, and against the same layer forced to tiles of 8 (same weights; the
+    lane-reduction order differs, so within tolerance rather than bitwise)."""
+    prob = inputs.make_problem(H, H, B, T, d, cell=cell, act=act, h0="random", c0="random", seed_offset=H + B)
+    g, o, err = check(prob, "fp16")
+    assert g["info"]["batch_tile"] == 16
+    g8, _, err8 = check(prob, "fp16", batch_tile=8)
+    assert g8["info"]["batch_tile"] == 8
+    assert np.abs(g["y"] - g8["y"]).max() <= 2 * TOL["fp16"]
 
 
 @pytest.mark.parametrize("H,B,d", [(6000, 8, 0.01), (4100, 11, 0.02), (9000, 8, 0.004)])
