@@ -417,6 +417,35 @@ def main():
             cb["speedup_vs_graph"] = cb["graph_us_per_timestep"] / (t_rec * 1e6 / T)
             cb["speedup_vs_eager"] = cb["eager_us_per_timestep"] / (t_rec * 1e6 / T)
             out["baseline_cublas_dense"] = cb
+        if not args.no_cublas and world == 1 and prec == "fp16":
+            # SURVEY.md Sec. 8(f)1 comparator: the dense persistent RNN on tensor cores
+            # (SRNN_FLAG_DENSE_TC: same exchange/epilogue, U_r as mma.sync fragments)
+            try:
+                from paper_1804_10223_b200 import FLAG_DENSE_TC
+                dm = from_problem(prob, prec=prec, device=local, flags=args.flags | FLAG_DENSE_TC)
+                dm.recurrence(bp, y=y, hT=hT)
+                torch.cuda.synchronize()
+                de = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                dts = []
+                for _ in range(10):
+                    flush.fill_(1.0)
+                    de[0].record(stream)
+                    dm.recurrence(bp, y=y, hT=hT)
+                    de[1].record(stream)
+                    torch.cuda.synchronize()
+                    dts.append(de[0].elapsed_time(de[1]))
+                dm.status()
+                dinf = dm.info()
+                dm.close()
+                d_us = statistics.median(dts) * 1000 / T
+                out["baseline_dense_tc_persistent"] = {
+                    "us_per_timestep": d_us, "speedup_sparse_vs_dense_tc": d_us / (t_rec * 1e6 / T),
+                    "plan": {k: dinf[k] for k in ("num_ctas", "batch_tile", "dense_m_tiles",
+                                                  "dense_kblocks_per_warp", "dense_frags_reg", "dense_frags_smem")},
+                    "note": "same library, SRNN_FLAG_DENSE_TC: dense fp16 U_r in mma.sync m16n8k16 fragments, "
+                            "same tagged exchange and epilogue (recurrence only, median of 10)"}
+            except Exception as ex:  # noqa: BLE001
+                out["baseline_dense_tc_persistent"] = {"error": str(ex)[:200]}
         if not args.no_cpu_baseline and world == 1:
             dt, fl = cpu_oracle_run(cfg, B, T)
             out["cpu_baseline"] = {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": 1, "kind": "oracle",

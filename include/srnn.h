@@ -88,6 +88,17 @@ typedef enum { SRNN_PREC_FP32 = 0, SRNN_PREC_FP16W_FP32ACC = 1 } srnn_prec_t;
                                               chunks are copied and projected (GEMM on the free SMs)
                                               while the persistent kernel runs, y chunks are copied
                                               back as the kernel reports progress               */
+#define SRNN_FLAG_DENSE_TC       (1u << 8) /* comparator: the DENSE persistent
+                                              RNN of PAPER.md:51-71 (Sec. 3.2, Diamos et al.)
+                                              re-done for sm_100a tensor cores.  U_r is densified
+                                              (fp16 RNE, zeros kept) into mma.sync m16n8k16
+                                              A fragments held in registers (overflow: shared
+                                              memory); h_{t-1} is staged as [H][8] fp16 rows and
+                                              read with ldmatrix.trans; the exchange, epilogue and
+                                              LSTM gates are those of the sparse kernel.  FP16W
+                                              mode only (else SRNN_ERR_UNSUPPORTED); batch tiles
+                                              of 4 or 8; SRNN_ERR_NOT_ON_CHIP when the dense
+                                              fragments do not fit registers + shared memory  */
 
 typedef struct {
     int32_t hidden;     /* H >= 1, <= 65536 (u16 column index)                          */
@@ -130,6 +141,11 @@ typedef struct {
     int64_t smem_weight_bytes_per_cta; /* shared-memory weight tier (pairs beyond the register slots) (L) */
     int64_t image_slots_per_lane;      /* register + shared-memory slots per lane in the image (L)     */
     int64_t model_cycles_per_step;     /* planner's cost-model estimate of one timestep, SM cycles (L) */
+    /* SRNN_FLAG_DENSE_TC plans only (zero otherwise) (L): */
+    int32_t dense_m_tiles;     /* 16-row mma tiles per CTA                                   */
+    int32_t dense_kblocks_per_warp; /* 16-column k-blocks of U_r per warp                      */
+    int32_t dense_frags_reg;   /* A fragments per lane held in registers (compiled instance) */
+    int32_t dense_frags_smem;  /* A fragments per lane held in shared memory                 */
 } srnn_plan_info_t;
 
 /* Create a plan for the layer described by *cfg.

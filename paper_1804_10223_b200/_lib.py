@@ -29,6 +29,7 @@ FLAG_DEBUG_JITTER = 1 << 4
 FLAG_FP32_STAGING = 1 << 5
 FLAG_PROFILE = 1 << 6
 FLAG_RESERVE_SMS = 1 << 7
+FLAG_DENSE_TC = 1 << 8
 
 EXPORTED = ["srnn_plan_create", "srnn_plan_query", "srnn_load_weights", "srnn_forward", "srnn_input_projection",
             "srnn_recurrence", "srnn_forward_host", "srnn_plan_status", "srnn_plan_export_layout",
@@ -57,7 +58,9 @@ class PlanInfo(ctypes.Structure):
                [(n, ctypes.c_int64) for n in
                 ("nnz", "slots_total", "smem_bytes_per_cta", "weight_image_bytes", "wavefronts_per_step_max",
                  "wavefronts_per_step_ideal", "conflict_wavefronts", "smem_weight_bytes_per_cta",
-                 "image_slots_per_lane", "model_cycles_per_step")]
+                 "image_slots_per_lane", "model_cycles_per_step")] + \
+               [(n, ctypes.c_int32) for n in
+                ("dense_m_tiles", "dense_kblocks_per_warp", "dense_frags_reg", "dense_frags_smem")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -72,6 +72,10 @@ struct srnn_plan {
     cudaEvent_t ev_in = nullptr, ev_rec = nullptr;
     cudaEvent_t ev_chunk[10] = {};  // x chunk c resident (s_copy -> projection stream)
     int32_t* h_status = nullptr;     // pinned: status read back on s_out at the end of a call
+    // SRNN_FLAG_DENSE_TC comparator: dense mma.sync A fragments of U_r
+    bool dense = false;
+    int dense_mt = 0, dense_kpw = 0, dense_nf = 0, dense_inst = 0, hs_rows = 0;
+    std::vector<uint4> dense_img;  // host image [cta][frag][thread] (freed after upload)
 };
 
 namespace {
@@ -188,6 +192,124 @@ double cost_model(const Layout& lay, int bt, int H, int n_tiles, bool f16, int i
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// SRNN_FLAG_DENSE_TC: the dense persistent RNN comparator (SURVEY.md Sec.
+// 8(f)1).  Same exchange, b' staging and epilogue as the
+// sparse plan; U_r densified into mma.sync m16n8k16 A fragments.
+// ---------------------------------------------------------------------------
+size_t dense_smem(const srnn_plan* p, int umax) {
+    size_t s = static_cast<size_t>(p->hs_rows) * 16;
+    s += 3 * static_cast<size_t>(p->G) * umax * p->BT * 4;
+    if (p->G == 4) s += static_cast<size_t>(p->n_tiles_max) * umax * p->BT * 4;
+    s += 16 + 16;  // abort flag, alignment of the fragment tier
+    s += static_cast<size_t>(std::max(0, p->dense_nf - p->dense_inst)) * kDenseThreads * 16;
+    s += static_cast<size_t>(kDenseThreads / 32) * p->dense_mt * 16 * 8 * 4;  // partial tiles
+    return s;
+}
+
+srnn_status_t create_dense(srnn_plan* p, srnn_plan_t* out) {
+    const srnn_config_t& c = p->cfg;
+    if (!p->f16) {
+        delete p;
+        return SRNN_ERR_UNSUPPORTED;  // fp16 fragments and fp16 h staging only
+    }
+    int bt = c.batch > 4 ? 8 : 4;
+    if (c.batch_tile == 4 || c.batch_tile == 8) bt = c.batch_tile;
+    p->BT = bt;
+    p->E = 16;
+    p->n_tiles_max = (c.batch + bt - 1) / bt;
+    const int kpw = ((c.hidden + 15) / 16 + 15) / 16;
+    p->dense_kpw = kpw;
+    p->hs_rows = 256 * kpw;
+    if (!p->host_only) {
+        DeviceGuard g(c.device);
+        const size_t tile_stride = (static_cast<size_t>(c.hidden) * (bt / 2) + 1) & ~static_cast<size_t>(1);
+        p->xbuf_words = 2 * static_cast<size_t>(p->n_tiles_max) * tile_stride;
+        const size_t bp_elems = static_cast<size_t>(std::max(1, c.max_steps)) * c.batch * p->G * c.hidden;
+        if (cudaMalloc(&p->d_xbuf, p->xbuf_words * 8) != cudaSuccess ||
+            cudaMalloc(&p->d_status, sizeof(int32_t)) != cudaSuccess ||
+            cudaMalloc(&p->d_bprime, bp_elems * sizeof(float)) != cudaSuccess ||
+            cudaMemset(p->d_xbuf, 0, p->xbuf_words * 8) != cudaSuccess ||
+            cudaMemset(p->d_status, 0, sizeof(int32_t)) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaDeviceSynchronize() != cudaSuccess) {
+            free_device(p);
+            delete p;
+            return SRNN_ERR_CUDA;
+        }
+    }
+    *out = p;
+    return SRNN_OK;
+}
+
+// Units -> CTAs, row tiles, fragment tiers, and the fragment image.
+// Fragment f of warp w covers k-block kb = w * kpw + f / MT and row tile
+// m = f % MT; lane (gid = lane / 4, tig = lane % 4) holds, as in the PTX ISA
+// m16n8k16 A layout, {A[gid][2tig..+1], A[gid+8][2tig..+1], A[gid][2tig+8..+9],
+// A[gid+8][2tig+8..+9]} (low half = lower column).
+srnn_status_t pack_dense(srnn_plan* p, const int32_t* rowptr, const int32_t* col, const float* qval) {
+    const int H = p->cfg.hidden, G = p->G;
+    int reserve = 0;
+    if (p->cfg.flags & SRNN_FLAG_RESERVE_SMS) {
+        reserve = 4;
+        if (const char* r = std::getenv("SRNN_RESERVE_SMS")) reserve = std::max(1, std::min(p->sm_count / 2, std::atoi(r)));
+    }
+    const int C = p->cfg.num_ctas > 0 ? p->cfg.num_ctas : std::max(1, std::min(p->sm_count - reserve, H));
+    Layout lay;
+    lay.num_ctas = C;
+    lay.threads = kDenseThreads;
+    lay.warps = kDenseThreads / 32;
+    lay.lanes_per_row = 0;
+    lay.cta_unit0.resize(C + 1);
+    int umax = 0;
+    for (int c = 0; c <= C; ++c) lay.cta_unit0[c] = static_cast<int>((static_cast<int64_t>(c) * H) / C);
+    for (int c = 0; c < C; ++c) umax = std::max(umax, lay.cta_unit0[c + 1] - lay.cta_unit0[c]);
+    const int mt = (G * umax + 15) / 16;
+    if (mt > 2) return SRNN_ERR_NOT_ON_CHIP;  // > 32 rows per CTA: compiled for 1 or 2 row tiles
+    const int kpw = p->dense_kpw, nf = mt * kpw;
+    p->dense_mt = mt;
+    p->dense_nf = nf;
+    p->dense_inst = nf <= 8 ? 8 : 12;
+    if (dense_smem(p, umax) > static_cast<size_t>(p->smem_optin)) return SRNN_ERR_NOT_ON_CHIP;
+    const int W = lay.warps, NT = kDenseThreads;
+    p->dense_img.assign(static_cast<size_t>(C) * nf * NT, make_uint4(0u, 0u, 0u, 0u));
+    std::vector<uint16_t> blk;  // dense rows of one CTA: [G*U][kcols] fp16 bits (zero padded)
+    const int kcols = p->hs_rows;
+    for (int c = 0; c < C; ++c) {
+        const int u0 = lay.cta_unit0[c], U = lay.cta_unit0[c + 1] - u0;
+        blk.assign(static_cast<size_t>(mt) * 16 * kcols, 0);
+        for (int q = 0; q < G; ++q)
+            for (int u = 0; u < U; ++u) {
+                const int r = q * U + u, grow = q * H + u0 + u;
+                for (int i = rowptr[grow]; i < rowptr[grow + 1]; ++i)
+                    blk[static_cast<size_t>(r) * kcols + col[i]] = float_to_half_rne(qval[i]);
+            }
+        auto pair = [&](int r, int k) -> uint32_t {
+            return static_cast<uint32_t>(blk[static_cast<size_t>(r) * kcols + k]) |
+                   (static_cast<uint32_t>(blk[static_cast<size_t>(r) * kcols + k + 1]) << 16);
+        };
+        for (int f = 0; f < nf; ++f)
+            for (int w = 0; w < W; ++w)
+                for (int lane = 0; lane < 32; ++lane) {
+                    const int m = f % mt, kb = w * kpw + f / mt, gid = lane >> 2, tig = lane & 3;
+                    const int r0 = m * 16 + gid, k0 = kb * 16 + 2 * tig;
+                    uint4 a;
+                    a.x = pair(r0, k0);
+                    a.y = pair(r0 + 8, k0);
+                    a.z = pair(r0, k0 + 8);
+                    a.w = pair(r0 + 8, k0 + 8);
+                    p->dense_img[(static_cast<size_t>(c) * nf + f) * NT + w * 32 + lane] = a;
+                }
+    }
+    p->smem_bytes = dense_smem(p, umax);
+    p->np_inst = 0;
+    p->ns_slots = 0;
+    p->model_cost = 0;
+    p->regs = 128;  // host-only estimate; replaced by the compiled count
+    p->lay = std::move(lay);
+    return SRNN_OK;
+}
+
 extern "C" {
 
 const char* srnn_status_string(srnn_status_t s) {
@@ -252,6 +374,8 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
         return SRNN_ERR_INVALID_VALUE;
     }
     p->f16 = c.prec == SRNN_PREC_FP16W_FP32ACC && (c.flags & SRNN_FLAG_FP32_STAGING) == 0;
+    p->dense = (c.flags & SRNN_FLAG_DENSE_TC) != 0;
+    if (p->dense) return create_dense(p, out);
     // Batch tile: the paper's wide load interleaves 4 samples.
     int bt = c.batch >= 4 ? 4 : (c.batch >= 2 ? 2 : 1);
     if (p->f16 && c.batch >= 8) bt = 8;    // fp16: 8 samples per LDS.128 (one exchange round for B = 8)
@@ -338,6 +462,16 @@ srnn_status_t srnn_plan_query(srnn_plan_t p, srnn_plan_info_t* out) {
         out->model_cycles_per_step = static_cast<int64_t>(p->model_cost);
         out->weight_image_bytes = static_cast<int64_t>(l.num_ctas) * (p->np_inst + p->ns_slots) * l.threads *
                                   (p->f16 ? 4 : 8);
+        if (p->dense) {
+            out->packed_registers = 0;
+            out->dense_m_tiles = p->dense_mt;
+            out->dense_kblocks_per_warp = p->dense_kpw;
+            out->dense_frags_reg = std::min(p->dense_inst, p->dense_nf);
+            out->dense_frags_smem = std::max(0, p->dense_nf - p->dense_inst);
+            out->weight_image_bytes = static_cast<int64_t>(l.num_ctas) * p->dense_nf * l.threads * 16;
+            out->smem_weight_bytes_per_cta = static_cast<int64_t>(out->dense_frags_smem) * l.threads * 16;
+            out->image_slots_per_lane = 0;
+        }
         const int planes = p->BT == 16 ? 2 : 1;  // two LDS.128 per pair at BT = 16
         out->wavefronts_per_step_max = l.wavefronts_max_cta * planes;
         out->wavefronts_per_step_ideal = l.wavefronts_ideal_cta * planes;
@@ -376,6 +510,11 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
     in.E = p->BT == 16 ? 16 : p->E;  // BT = 16 gathers two 16-byte planes: the bank model of BT = 8, twice
     in.naive = (p->cfg.flags & SRNN_FLAG_NAIVE_LAYOUT) != 0;
 
+    if (p->dense) {
+        const srnn_status_t st = pack_dense(p, rowptr, col, qval.data());
+        if (st != SRNN_OK) return st;
+        p->nnz = nnz;
+    } else {
     // ---- search (num_ctas, lanes_per_row, slot budget) ----
 search_again:
     std::vector<int> cands_c;
@@ -518,6 +657,7 @@ search_again:
     p->lay = std::move(fin);
     p->nnz = nnz;
     p->regs = (p->f16 ? 1 : 2) * best_inst + 60;  // host-only estimate; replaced by the compiled count below
+    }  // sparse search
 
     if (!p->host_only) {
         DeviceGuard g(p->cfg.device);
@@ -532,7 +672,12 @@ search_again:
         p->d_unit0 = p->d_wslots = nullptr;
         p->d_wx = p->d_bias = nullptr;
         cudaError_t e = cudaSuccess;
-        if (p->f16) {
+        if (p->dense) {
+            const size_t nb = p->dense_img.size() * sizeof(uint4);
+            e = cudaMalloc(&p->d_img, nb);
+            if (e == cudaSuccess) e = cudaMemcpy(p->d_img, p->dense_img.data(), nb, cudaMemcpyHostToDevice);
+            std::vector<uint4>().swap(p->dense_img);
+        } else if (p->f16) {
             std::vector<uint32_t> img(n);
             for (size_t i = 0; i < n; ++i)
                 img[i] = (static_cast<uint32_t>(p->BT >= 8 ? l.col[i] : l.col[i] * p->E) << 16) |
@@ -589,8 +734,10 @@ search_again:
         RecParams rp{};
         rp.threads = l.threads;
         int regs = 0, maxb = 0;
-        int le = launch_recurrent(p->np_inst, p->BT, G, p->f16 ? 1 : 0, rp, l.num_ctas, p->smem_bytes, nullptr, true,
-                                  &regs, &maxb);
+        int le = p->dense ? launch_dense(p->dense_inst, p->dense_mt, p->BT, G, rp, l.num_ctas, p->smem_bytes, nullptr,
+                                         true, &regs, &maxb)
+                          : launch_recurrent(p->np_inst, p->BT, G, p->f16 ? 1 : 0, rp, l.num_ctas, p->smem_bytes,
+                                             nullptr, true, &regs, &maxb);
         if (le != 0) return SRNN_ERR_CUDA;
         p->regs = regs;
         if (maxb < 1) return SRNN_ERR_NOT_ON_CHIP;
@@ -722,8 +869,19 @@ static srnn_status_t recurrence_impl(srnn_plan_t p, int32_t T, int32_t B, const 
     rp.bp_ready_base = pa.bp_ready_base;
     rp.progress = pa.progress;
     rp.progress_every = pa.every > 0 ? pa.every : 1;
-    int e = launch_recurrent(p->np_inst, p->BT, p->G, p->f16 ? 1 : 0, rp, p->lay.num_ctas, p->smem_bytes, stream,
+    int e;
+    if (p->dense) {
+        rp.img_dense = static_cast<const uint4*>(p->d_img);
+        rp.img_f16 = nullptr;
+        rp.dense_kpw = p->dense_kpw;
+        rp.dense_nf = p->dense_nf;
+        rp.hs_rows = p->hs_rows;
+        e = launch_dense(p->dense_inst, p->dense_mt, p->BT, p->G, rp, p->lay.num_ctas, p->smem_bytes, stream, false,
+                         nullptr, nullptr);
+    } else {
+        e = launch_recurrent(p->np_inst, p->BT, p->G, p->f16 ? 1 : 0, rp, p->lay.num_ctas, p->smem_bytes, stream,
                              false, nullptr, nullptr);
+    }
     if (e != 0) return SRNN_ERR_CUDA;
     p->epoch += static_cast<uint32_t>(T) + 1;
     return SRNN_OK;

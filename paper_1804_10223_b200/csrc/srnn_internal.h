@@ -51,6 +51,11 @@ struct RecParams {
     uint32_t bp_ready_base;
     uint32_t* progress;        // +1 per CTA every progress_every steps (after y is stored), or null
     int32_t progress_every;
+    // SRNN_FLAG_DENSE_TC comparator (dense U_r as mma.sync A fragments)
+    const uint4* img_dense;    // [cta][frag][thread] A fragments (4 x 2 fp16), frag = kk * MT + m
+    int32_t dense_kpw;         // k-blocks (16 columns) per warp
+    int32_t dense_nf;          // fragments per lane in the image (= MT * dense_kpw)
+    int32_t hs_rows;           // staged h rows (>= H, = 16 warps * 16 * dense_kpw), 16 bytes each
 };
 
 struct GemmParams {
@@ -67,6 +72,11 @@ struct GemmParams {
 int launch_recurrent(int np, int bt, int g, int f16, const RecParams& p, int num_ctas,
                      size_t smem_bytes, void* stream, bool query_only, int* regs_out,
                      int* max_blocks_per_sm_out);
+// Dense tensor-core comparator (srnn_rec_dense.cu): nf = register fragments
+// per lane (8 or 12), mt = 16-row tiles per CTA (1 or 2), bt = 4 or 8.
+constexpr int kDenseThreads = 512;
+int launch_dense(int nf, int mt, int bt, int g, const RecParams& p, int num_ctas, size_t smem_bytes, void* stream,
+                 bool query_only, int* regs_out, int* max_blocks_per_sm_out);
 int launch_gemm_f32(const GemmParams& p, void* stream);
 // fp16 tensor-core input GEMM (srnn_gemm_tc.cu); maps are CUtensorMap*.
 int launch_gemm_tc(const void* map_a, const void* map_b, const float* bias, float* C, int M, int N, int K,

@@ -165,7 +165,9 @@ struct Fmt {
 // together (one round trip per round, not per chunk).  The producers always
 // write whole chunks (an odd word count gets a tagged pad word), so a chunk is
 // valid iff both tags match.  Tag mode spins; grid-sync mode checks once.
-template <bool F16, int BT, int K>
+// ROW16 (dense tensor-core comparator): every unit gets a 16-byte hs row
+// (ldmatrix rows); with BT = 4 the upper 8 bytes stay zero.
+template <bool F16, int BT, int K, bool ROW16 = false>
 __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, unsigned char* hs, int n_words,
                                           uint32_t want, bool spin, int32_t* status,
                                           unsigned long long timeout_ns, uint32_t backoff_ns = 0,
@@ -190,7 +192,11 @@ __device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, un
             for (int j = 0; j < K; ++j) {
                 if ((pend >> j) & 1u) {
                     if ((tag_of(v[j].x) == want) & (tag_of(v[j].y) == want)) {
-                        Fmt<F16, BT>::store(hs, base + j * nt, v[j].x, v[j].y, true, ps);
+                        if (ROW16 && BT == 4)
+                            *reinterpret_cast<uint2*>(hs + 16 * (base + j * nt)) =
+                                make_uint2(static_cast<uint32_t>(v[j].x), static_cast<uint32_t>(v[j].y));
+                        else
+                            Fmt<F16, BT>::store(hs, base + j * nt, v[j].x, v[j].y, true, ps);
                         pend &= ~(1u << j);
                     }
                 }
@@ -495,6 +501,79 @@ __device__ __forceinline__ void operate_smem_tier(float (&acc)[BT], const unsign
     }
 }
 
+// ---------------------------------------------------------------------------
+// Dense tensor-core comparator (the
+// dense persistent RNN of Sec. 3.2, whose V100 version keeps U_r in registers
+// and runs on CUDA cores).  Here a CTA owns MT tiles of 16 rows and the 16
+// warps split the H columns into k-blocks of 16: warp w multiplies its
+// k-blocks with mma.sync.m16n8k16 (A = U_r fragment from registers or shared
+// memory, B = 16 staged h rows via ldmatrix.trans, N = 8 samples), the warps'
+// partial 16x8 tiles are summed in shared memory in a fixed order (no
+// atomics: deterministic), and the result lands in zs like the sparse
+// butterfly's.  A per-CTA tile is 16 x 8 x H: far below tcgen05's 128-row
+// minimum, so the warp-level MMA is the fitting unit here.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void ldmatrix_x2_trans(uint32_t& b0, uint32_t& b1, const void* row_addr) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(row_addr));
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];" : "=r"(b0), "=r"(b1) : "r"(a));
+}
+__device__ __forceinline__ void mma_16816(float& d0, float& d1, float& d2, float& d3, const uint4& a, uint32_t b0,
+                                          uint32_t b1) {
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+        "{%0, %1, %2, %3};"
+        : "+f"(d0), "+f"(d1), "+f"(d2), "+f"(d3)
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+
+template <int NF, int MT>
+struct DenseFrags {
+    uint4 a[NF];  // fragment f = kk * MT + m (k-block kk of this warp, row tile m)
+    __device__ __forceinline__ void load(const RecParams& p, size_t img0, int nf_reg) {
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+            a[f] = f < nf_reg ? p.img_dense[img0 + static_cast<size_t>(f) * p.threads] : make_uint4(0u, 0u, 0u, 0u);
+    }
+    // red: [warps][MT][16][8] fp32 partial tiles; hs: [hs_rows][16 B]
+    __device__ __forceinline__ void operate(const unsigned char* hs, const uint4* ws, float* red, int kpw, int nf_reg,
+                                            int nt) const {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        // two accumulator sets (even / odd k-blocks) halve the dependent mma chain
+        float e0[MT], e1[MT], e2[MT], e3[MT], o0[MT], o1[MT], o2[MT], o3[MT];
+#pragma unroll
+        for (int m = 0; m < MT; ++m) e0[m] = e1[m] = e2[m] = e3[m] = o0[m] = o1[m] = o2[m] = o3[m] = 0.0f;
+        const unsigned char* hw = hs + (static_cast<size_t>(warp) * kpw * 16 + (lane & 15)) * 16;
+#pragma unroll
+        for (int f = 0; f < NF; f += MT) {
+            if (f < nf_reg) {  // warp-uniform
+                uint32_t b0, b1;
+                ldmatrix_x2_trans(b0, b1, hw + (f / MT) * 256);
+#pragma unroll
+                for (int m = 0; m < MT; ++m) {
+                    if ((f / MT) & 1)
+                        mma_16816(o0[m], o1[m], o2[m], o3[m], a[f + m], b0, b1);
+                    else
+                        mma_16816(e0[m], e1[m], e2[m], e3[m], a[f + m], b0, b1);
+                }
+            }
+        }
+        const int nf = MT * kpw;
+        for (int f = nf_reg; f < nf; f += MT) {  // shared-memory fragments
+            uint32_t b0, b1;
+            ldmatrix_x2_trans(b0, b1, hw + (f / MT) * 256);
+#pragma unroll
+            for (int m = 0; m < MT; ++m)
+                mma_16816(e0[m], e1[m], e2[m], e3[m], ws[static_cast<size_t>(f + m - nf_reg) * nt + threadIdx.x], b0, b1);
+        }
+        const int gid = lane >> 2, tig = lane & 3;
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+            float* r = red + ((warp * MT + m) * 16 + gid) * 8 + 2 * tig;
+            *reinterpret_cast<float2*>(r) = make_float2(e0[m] + o0[m], e1[m] + o1[m]);
+            *reinterpret_cast<float2*>(r + 64) = make_float2(e2[m] + o2[m], e3[m] + o3[m]);
+        }
+    }
+};
+
 // Max threads per CTA of each instance.  The register file is split over
 // the 4 SM sub-partitions (16K registers each), so with W warps a thread may
 // hold at most 512 / ceil(W/4) registers: 256 threads -> 255, 384 -> 168,
@@ -527,9 +606,13 @@ __device__ __forceinline__ void cp_async_commit_wait_all() {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <int NP, int BT, int G, bool F16>
-__global__ void __launch_bounds__(MaxThreadsBT<NP, F16, BT>::value, 1) srnn_persistent_kernel(const RecParams p) {
+// MT = 0: the sparse kernel (NP register slots per lane).  MT >= 1: the dense
+// tensor-core comparator (NP register A fragments per lane, MT row tiles).
+template <int NP, int BT, int G, bool F16, int MT = 0>
+__global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16, BT>::value, 1)
+    srnn_persistent_kernel(const RecParams p) {
     using F = Fmt<F16, BT>;
+    constexpr bool DENSE = MT > 0;
     extern __shared__ __align__(16) unsigned char smem[];
     const int H = p.H;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
@@ -541,15 +624,16 @@ __global__ void __launch_bounds__(MaxThreadsBT<NP, F16, BT>::value, 1) srnn_pers
     const int umax_bt = p.units_max * BT;
     // shared memory: hs [H][BT] at offset 0 (E bytes per unit), then fp32 areas
     unsigned char* hs = smem;
-    float* zs = reinterpret_cast<float*>(smem + ((static_cast<size_t>(H) * F::E + 15) & ~static_cast<size_t>(15)));
+    const size_t hs_bytes = DENSE ? static_cast<size_t>(p.hs_rows) * 16 : static_cast<size_t>(H) * F::E;
+    float* zs = reinterpret_cast<float*>(smem + ((hs_bytes + 15) & ~static_cast<size_t>(15)));
     float* bpsb = zs + G * umax_bt;                          // b' double buffer: [2][item][G]
     float* cs = bpsb + 2 * G * umax_bt;                      // LSTM c: [n_tiles][item]
     int* s_abort = reinterpret_cast<int*>(cs + (G == 4 ? p.n_tiles * umax_bt : 0));
     unsigned char* ws = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(s_abort + 1) + 15) & ~static_cast<uintptr_t>(15));  // smem weight tier
 
-    const int L = p.lanes_per_row;
-    const int n_w = p.warp_slots[cta * (p.threads >> 5) + warp];
+    const int L = DENSE ? 32 : p.lanes_per_row;
+    const int n_w = DENSE ? 0 : p.warp_slots[cta * (p.threads >> 5) + warp];
     const int n_words = H * F::WPR;
     const int ps = H * 16;                      // BT = 16: second hs plane
     const unsigned char* hs2 = hs + ps;
@@ -558,10 +642,24 @@ __global__ void __launch_bounds__(MaxThreadsBT<NP, F16, BT>::value, 1) srnn_pers
 
     // ---- prologue: weights HBM -> registers (once per forward) ----
     Weights<NP, BT, F16> W;
+    DenseFrags<DENSE ? NP : 1, DENSE ? MT : 1> DW;
     const int ns = p.smem_slots;  // shared-memory tier slots per lane (multiple of 4)
     const size_t img_cta = static_cast<size_t>(cta) * (NP + ns) * p.threads;
-    W.load(p, img_cta + tid, n_w);
-    if (ns > 0) {
+    const int dense_nf_reg = DENSE ? min(NP, p.dense_nf) : 0;
+    float* red = nullptr;  // dense: [warps][MT][16][8] partial tiles, after the fragment tier
+    if constexpr (DENSE) {
+        const size_t img_d = static_cast<size_t>(cta) * p.dense_nf * p.threads;
+        DW.load(p, img_d + tid, dense_nf_reg);
+        const size_t n = static_cast<size_t>(p.dense_nf - dense_nf_reg) * p.threads;
+        const uint4* src = p.img_dense + img_d + static_cast<size_t>(dense_nf_reg) * p.threads;
+        for (size_t i = tid; i < n; i += nt) reinterpret_cast<uint4*>(ws)[i] = src[i];
+        red = reinterpret_cast<float*>(ws + n * 16);
+        // staged h rows: zero once (rows >= H and, for BT = 4, the upper 8 bytes are never written)
+        for (size_t i = tid; i < hs_bytes / 16; i += nt) reinterpret_cast<uint4*>(hs)[i] = make_uint4(0u, 0u, 0u, 0u);
+    } else {
+        W.load(p, img_cta + tid, n_w);
+    }
+    if (!DENSE && ns > 0) {
         const size_t n = static_cast<size_t>(ns) * p.threads;
         if (F16) {
             const uint32_t* src = p.img_f16 + img_cta + static_cast<size_t>(NP) * p.threads;
@@ -664,7 +762,7 @@ __global__ void __launch_bounds__(MaxThreadsBT<NP, F16, BT>::value, 1) srnn_pers
             // ---- load: h_{s-1} tile k -> hs ----
             const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
                 p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
-            if (!load_tile<F16, BT, LoadK<NP, F16>::value>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
+            if (!load_tile<F16, BT, LoadK<NP, F16>::value, DENSE>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
                                                             !grid_sync, p.status, p.timeout_ns, p.poll_backoff_ns,
                                                             p.loader_threads, ps))
                 *s_abort = 1;
@@ -673,7 +771,24 @@ __global__ void __launch_bounds__(MaxThreadsBT<NP, F16, BT>::value, 1) srnn_pers
             if (*s_abort) goto done;
 
             // ---- operate + reduce ----
-            {
+            if constexpr (DENSE) {
+                DW.operate(hs, reinterpret_cast<const uint4*>(ws), red, p.dense_kpw, dense_nf_reg, nt);
+                if (prof) prof[4] = clock64();
+                __syncthreads();
+                // fixed-order sum of the 16 warps' partial tiles -> zs[local row][sample]
+                for (int e = tid; e < G * U * BT; e += nt) {
+                    const int r = e / BT, b = e % BT;
+                    const float* q = red + r * 8 + b;
+                    float v[kDenseThreads / 32];  // all loads in flight, then a fixed-order sum
+#pragma unroll
+                    for (int w = 0; w < kDenseThreads / 32; ++w) v[w] = q[w * MT * 128];
+                    float z = 0.0f;
+#pragma unroll
+                    for (int w = 0; w < kDenseThreads / 32; ++w) z += v[w];
+                    zs[e] = z;
+                }
+                if (prof) prof[5] = clock64();
+            } else {
                 float acc[BT];
 #pragma unroll
                 for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
@@ -789,10 +904,10 @@ done:
     return;
 }
 
-template <int NP, int BT, int G, bool F16>
+template <int NP, int BT, int G, bool F16, int MT = 0>
 static int launch_one(const RecParams& p, int num_ctas, size_t smem, void* stream, bool query_only,
                       int* regs_out, int* max_blocks_out) {
-    auto fn = srnn_persistent_kernel<NP, BT, G, F16>;
+    auto fn = srnn_persistent_kernel<NP, BT, G, F16, MT>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return static_cast<int>(e);
     if (regs_out != nullptr || max_blocks_out != nullptr) {
@@ -804,7 +919,7 @@ static int launch_one(const RecParams& p, int num_ctas, size_t smem, void* strea
             int nb = 0;
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, p.threads, smem);
             if (e != cudaSuccess) return static_cast<int>(e);
-            *max_blocks_out = p.threads > MaxThreadsBT<NP, F16, BT>::value ? 0 : nb;
+            *max_blocks_out = p.threads > (MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16, BT>::value) ? 0 : nb;
         }
     }
     if (query_only) return 0;

@@ -15,7 +15,7 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_1804_10223_b200 import SrnnError, from_problem, inputs  # noqa: E402
+from paper_1804_10223_b200 import FLAG_DENSE_TC, SrnnError, from_problem, inputs  # noqa: E402
 
 
 def t_events(fn, reps=5):
@@ -86,9 +86,10 @@ def cusparse_us(prob, B, T):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
-    ap.add_argument("--experiment", default="c3", choices=["c3", "e4", "e5"],
+    ap.add_argument("--experiment", default="c3", choices=["c3", "e4", "e5", "f1"],
                     help="c3: hidden x batch x density grid; e4: constant nnz 1.32M (PAPER.md:161); "
-                         "e5: load-balanced vs unbalanced pruning at 2304 @ 25% (PAPER.md:188)")
+                         "e5: load-balanced vs unbalanced pruning at 2304 @ 25% (PAPER.md:188); "
+                         "f1: sparse vs the dense tensor-core persistent comparator (SURVEY.md 8(f)1)")
     a = ap.parse_args()
     T = 256
     if a.experiment == "c3":
@@ -98,11 +99,15 @@ def main():
         points = [(H, B, d, "unstructured") for H in Hs for B in Bs for d in ds]
     elif a.experiment == "e4":  # constant nnz = 2304^2 * 0.25 = 11520^2 * 0.01 = 1,327,104
         points = [(H, 4, 1327104 / (H * H), "unstructured") for H in (2304, 3072, 4096, 5760, 7168, 9216, 11520)]
+    elif a.experiment == "f1":  # where does sparse stop winning against a dense persistent kernel on B200?
+        points = [(H, B, d, "unstructured") for H in (1152, 2304, 3584) for B in (1, 4, 8)
+                  for d in (0.01, 0.1, 0.3, 0.5, 1.0)]
     else:  # E5: row-balanced vs unbalanced at 2304 @ 25%, B = 4
         points = [(2304, 4, 0.25, "unstructured"), (2304, 4, 0.25, "row_balanced"),
                   (1024, 4, 0.125, "unstructured"), (1024, 4, 0.125, "row_balanced")]
     dense_cache = {}
     cudnn_cache = {}
+    dtc_cache = {}
     for H, B, d, pattern in points:
                 rec = {"H": H, "B": B, "density": d, "T": T, "pattern": pattern, "experiment": a.experiment}
                 try:
@@ -125,6 +130,25 @@ def main():
                     m.close()
                 except SrnnError as e:
                     rec["ours"] = f"not on chip / unsupported: {e}"
+                if a.experiment == "f1":
+                    try:
+                        key = (H, B)
+                        if key not in dtc_cache:
+                            dm = from_problem(prob, prec="fp16", flags=FLAG_DENSE_TC)
+                            bpd = dm.input_projection(torch.from_numpy(prob["x"]).cuda())
+                            yd = torch.empty(T, B, H, device="cuda")
+                            dm.recurrence(bpd, y=yd)
+                            torch.cuda.synchronize()
+                            dtc_cache[key] = 1000 * t_events(lambda: dm.recurrence(bpd, y=yd)) / T
+                            dm.status()
+                            dm.close()
+                        rec["dense_tc_persistent_us_per_step"] = dtc_cache[key]
+                        if "ours_us_per_step" in rec:
+                            rec["speedup_vs_dense_tc"] = dtc_cache[key] / rec["ours_us_per_step"]
+                    except SrnnError as e:
+                        rec["dense_tc"] = f"not on chip / unsupported: {e}"
+                    print(json.dumps(rec), flush=True)
+                    continue
                 try:
                     key = (H, B)
                     if key not in dense_cache:

@@ -175,3 +175,29 @@ def test_density_zero_and_one_layouts():
         m = host_plan(prob, "fp32")
         dense, cnt, _ = reconstruct(m, prob)
         assert np.array_equal(dense, csr_dense(prob))
+
+
+def test_dense_tc_plan_host_only():
+    """SRNN_FLAG_DENSE_TC comparator plan: row tiles,
+    k-blocks per warp and fragment tiers follow from H, G and the SM count."""
+    from paper_1804_10223_b200 import FLAG_DENSE_TC
+    for H, B, cell, mt, kpw, reg, sm in ((2304, 4, "rnn", 1, 9, 9, 0), (1024, 4, "lstm", 2, 4, 8, 0),
+                                         (3584, 8, "rnn", 2, 14, 12, 16), (100, 1, "rnn", 1, 1, 1, 0)):
+        prob = inputs.make_problem(H, 8, B, 2, 0.05, cell=cell)
+        m = SparseRNN(H, 8, B, 2, 0.05, cell=cell, prec="fp16", flags=FLAG_HOST_ONLY | FLAG_DENSE_TC)
+        m.load_weights(prob["rowptr"], prob["col"], prob["val"], prob["wx"], prob["bias"])
+        inf = m.info()
+        assert (inf["dense_m_tiles"], inf["dense_kblocks_per_warp"]) == (mt, kpw), inf
+        assert (inf["dense_frags_reg"], inf["dense_frags_smem"]) == (reg, sm), inf
+        assert inf["batch_tile"] == (8 if B > 4 else 4) and inf["threads_per_cta"] == 512
+        assert inf["smem_bytes_per_cta"] <= 232448
+        m.close()
+    # fp32 mode has no dense tensor-core variant; > 32 rows per CTA does not fit the compiled tiles
+    with pytest.raises(SrnnError) as e:
+        SparseRNN(512, 8, 1, 1, 0.1, prec="fp32", flags=FLAG_HOST_ONLY | FLAG_DENSE_TC)
+    assert e.value.code == -7
+    prob = inputs.make_problem(2048, 8, 1, 1, 0.01, cell="lstm")
+    m = SparseRNN(2048, 8, 1, 1, 0.01, cell="lstm", prec="fp16", flags=FLAG_HOST_ONLY | FLAG_DENSE_TC)
+    with pytest.raises(SrnnError) as e:
+        m.load_weights(prob["rowptr"], prob["col"], prob["val"], prob["wx"], prob["bias"])
+    assert e.value.code == -2

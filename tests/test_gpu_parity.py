@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_1804_10223_b200 import (FLAG_DEBUG_JITTER, FLAG_FP32_STAGING, FLAG_GRID_SYNC, FLAG_NAIVE_LAYOUT,
+from paper_1804_10223_b200 import (FLAG_DEBUG_JITTER, FLAG_DENSE_TC, FLAG_FP32_STAGING, FLAG_GRID_SYNC, FLAG_NAIVE_LAYOUT,
                                    FLAG_RESERVE_SMS, from_problem, inputs)
 
 pytestmark = pytest.mark.gpu
@@ -353,3 +353,40 @@ def test_forward_host_pipelined(cuda_device, prec, cell, B, T):
     assert np.array_equal(outs[1], dev[1].cpu().numpy())
     o = oracle.forward(prob)
     assert np.abs(outs[0].astype(np.float64) - o["y"]).max() <= TOL[prec]
+
+
+# ---- dense tensor-core persistent comparator (SRNN_FLAG_DENSE_TC) ----
+
+@pytest.mark.parametrize("cell,H,B,T,d,act", [
+    ("rnn", 256, 1, 16, 0.10, "relu"),    # C1 shape, one k-block per warp, B padded to the tile of 4
+    ("rnn", 300, 3, 20, 0.05, "tanh"),    # ragged H: zero rows/columns in the last k-block
+    ("rnn", 1000, 6, 12, 0.30, "relu"),   # tile of 8, ragged batch
+    ("rnn", 2304, 4, 48, 0.30, "relu"),   # C2 shape (9 register fragments per lane)
+    ("rnn", 3584, 9, 8, 0.10, "tanh"),    # two row tiles, 16 fragments in shared memory, two batch tiles
+    ("lstm", 1024, 4, 20, 0.125, "relu"), # C4 shape (two row tiles)
+    ("lstm", 200, 8, 6, 0.10, "relu"),
+])
+def test_dense_tc_parity(cuda_device, cell, H, B, T, d, act):
+    pattern = "row_balanced" if cell == "lstm" else "unstructured"
+    prob = inputs.make_problem(H, H, B, T, d, cell=cell, act=act, pattern=pattern, h0="random",
+                               c0="random" if cell == "lstm" else "zero", seed_offset=H + 5)
+    g, _, _ = check(prob, "fp16", flags=FLAG_DENSE_TC)
+    assert g["info"]["dense_m_tiles"] >= 1
+
+
+def test_dense_tc_integer_exact_and_deterministic(cuda_device):
+    prob = inputs.make_integer_problem(200, 6, 4, 3, 0.01, cell="rnn", act="identity")
+    o = oracle.forward(prob)
+    assert np.abs(o["y"]).max() < 2 ** 11
+    g = run_gpu(prob, "fp16", flags=FLAG_DENSE_TC)
+    assert np.array_equal(g["y"].astype(np.float64), o["y"])
+    prob = inputs.make_problem(777, 777, 3, 40, 0.1, act="tanh", h0="random")
+    a = run_gpu(prob, "fp16", flags=FLAG_DENSE_TC)
+    b = run_gpu(prob, "fp16", flags=FLAG_DENSE_TC | FLAG_DEBUG_JITTER)
+    assert np.array_equal(a["y"], b["y"])
+
+
+def test_dense_tc_C2_full(cuda_device):
+    """The comparator at the headline configuration, every output vs the oracle."""
+    prob = inputs.make_problem(**{k: v for k, v in inputs.CONFIGS["C2"].items() if k != "prec"})
+    check(prob, "fp16", flags=FLAG_DENSE_TC)
