@@ -671,13 +671,16 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     }
 
     const int act = p.act;
-    const int krow = warp * (32 / L) + lane / L;  // local row of this lane
+    const int lg_l = __ffs(L) - 1;  // L is a power of two: shifts, no per-step integer division
+    const int krow = (warp << (5 - lg_l)) + (lane >> lg_l);  // local row of this lane
+    // lane of the row that stores sample sbase (L >= BT), hoisted out of the time loop
+    const bool zs_writer = (lane & (L - 1)) < BT && krow < G * U;
     // epilogue fast path (one item per thread): item e1 = tid -> (unit, sample)
     const int e1 = tid, e1_b = tid % BT, e1_unit = u0 + tid / BT;
     const bool e1_ok = tid < n_items;
     const float* zs_e1 = zs + e1;
     float* const y_e1 = (p.y != nullptr && e1_ok) ? p.y + static_cast<size_t>(e1_b) * H + e1_unit : nullptr;
-    const bool row_leader = (lane % L) == 0 && krow < G * U;
+    const bool row_leader = (lane & (L - 1)) == 0 && krow < G * U;
     if (tid == 0) *s_abort = 0;
 
     // Publish item e's h of (step s, tile k) as tagged words.  Called by all
@@ -829,7 +832,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                 }
                 if (prof) prof[5] = clock64();
                 if (L >= BT) {
-                    if ((lane % L) < BT && krow < G * U) zs[krow * BT + sbase] = acc[0];
+                    if (zs_writer) zs[krow * BT + sbase] = acc[0];
                 } else if (row_leader) {
 #pragma unroll
                     for (int b = 0; b < BT; ++b) zs[krow * BT + b] = acc[b];
