@@ -65,3 +65,87 @@ def forward_partitioned(local_forward, x_global, group=None):
     start, count = shard(B, world, rank)
     y_local = local_forward(x_global[:, start:start + count].contiguous())
     return gather_batch(y_local, group=group, global_batch=B)
+
+
+# ---------------------------------------------------------------------------
+# Stacked layers pipelined across ranks (the NMT case
+# study is a 2-layer LSTM).  Rank r owns layer r.  The sequence
+# is cut into time chunks; rank r runs chunk c of its layer while rank r - 1
+# runs chunk c + 1 (a wavefront over (layer, chunk)), and each finished chunk
+# of y is handed to the next rank with one point-to-point send (NCCL p2p over
+# NVLink on GPUs, gloo on CPU).  The recurrent state (h, and c for LSTM) is
+# carried from chunk to chunk through the layer's h0/c0 -> hT/cT arguments,
+# so the result equals the unchunked layer-by-layer run: chunking changes
+# neither the per-step arithmetic nor its order.
+# ---------------------------------------------------------------------------
+
+def chunks(T: int, n_chunks: int):
+    """Contiguous time spans [(t0, length)] covering [0, T) (sizes differ by at most 1)."""
+    n = max(1, min(n_chunks, T)) if T > 0 else 1
+    return [shard(T, n, c) for c in range(n)]
+
+
+def layer_step(plan):
+    """Chunk function of one SparseRNN plan: (x_chunk, state) -> (y_chunk, state), state = (hT, cT)."""
+    def step(x_chunk, state):
+        h0, c0 = state if state is not None else (None, None)
+        out = plan.forward(x_chunk, h0, c0)
+        return out[0], (out[1], out[2] if len(out) > 2 else None)
+    return step
+
+
+def forward_stacked_chunked(layer_steps, x, n_chunks):
+    """Single-process wavefront order of the pipelined stack (one GPU, or a reference for tests):
+    for each time chunk, run it through every layer in turn, carrying each layer's state."""
+    import torch
+
+    states = [None] * len(layer_steps)
+    outs = []
+    for t0, tn in chunks(int(x.shape[0]), n_chunks):
+        inp = x[t0:t0 + tn].contiguous()
+        for li, f in enumerate(layer_steps):
+            inp, states[li] = f(inp, states[li])
+        outs.append(inp)
+    return torch.cat(outs, 0)
+
+
+def forward_layer_pipelined(local_layer_step, x_global, n_chunks, layer_widths, group=None):
+    """Rank r runs layer r of a stacked model over time chunks, pipelined across ranks.
+
+    local_layer_step(x_chunk [Tc, B, I_r], state) -> (y_chunk [Tc, B, H_r], state)
+    x_global: [T, B, I_0] (only rank 0 reads its values; every rank uses its shape/device)
+    layer_widths: H_r of every layer (rank r receives chunks of width H_{r-1}).
+    Returns the last layer's y [T, B, H_last] on every rank.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if len(layer_widths) != world:
+        raise ValueError("one layer per rank: len(layer_widths) must equal the world size")
+    T, B, _ = x_global.shape
+    dev, dt = x_global.device, x_global.dtype
+
+    def peer(r):  # global rank of group rank r
+        return r if group is None else dist.get_global_rank(group, r)
+
+    state = None
+    outs = []
+    for t0, tn in chunks(int(T), n_chunks):
+        if rank == 0:
+            inp = x_global[t0:t0 + tn].contiguous()
+        else:
+            inp = torch.empty((tn, B, layer_widths[rank - 1]), dtype=dt, device=dev)
+            dist.recv(inp, src=peer(rank - 1), group=group)
+        y, state = local_layer_step(inp, state)
+        if rank + 1 < world:
+            dist.send(y.contiguous(), dst=peer(rank + 1), group=group)
+        else:
+            outs.append(y)
+    if rank == world - 1:
+        y_all = torch.cat(outs, 0).contiguous()
+    else:
+        y_all = torch.empty((T, B, layer_widths[-1]), dtype=dt, device=dev)
+    dist.broadcast(y_all, src=peer(world - 1), group=group)
+    return y_all

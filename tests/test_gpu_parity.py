@@ -390,3 +390,35 @@ def test_dense_tc_C2_full(cuda_device):
     """The comparator at the headline configuration, every output vs the oracle."""
     prob = inputs.make_problem(**{k: v for k, v in inputs.CONFIGS["C2"].items() if k != "prec"})
     check(prob, "fp16", flags=FLAG_DENSE_TC)
+
+
+# ---- stacked layers, time-chunked wavefront (SURVEY.md Sec. 8(f)3) ----
+
+@pytest.mark.parametrize("prec,cell", [("fp16", "rnn"), ("fp16", "lstm"), ("fp32", "rnn")])
+def test_stacked_chunked_wavefront(cuda_device, prec, cell):
+    """Two stacked layers run chunk by chunk (state carried through h0/c0 -> hT/cT, the
+    order of the cross-rank layer pipeline) equal the unchunked layer-by-layer run bit for
+    bit, and the oracle chain within tolerance."""
+    import torch
+    from paper_1804_10223_b200.multigpu import forward_stacked_chunked, layer_step
+    T, B = 40, 4
+    p0 = inputs.make_problem(640, 320, B, T, 0.1, cell=cell, act="tanh", seed_offset=11)
+    p1 = inputs.make_problem(512, 640, B, T, 0.2, cell=cell, act="tanh", seed_offset=12)
+    plans = [from_problem(p, prec=prec) for p in (p0, p1)]
+    x = torch.from_numpy(p0["x"]).cuda()
+    steps = [layer_step(m) for m in plans]
+    full = forward_stacked_chunked(steps, x, 1)
+    for n in (3, 7):
+        got = forward_stacked_chunked(steps, x, n)
+        torch.cuda.synchronize()
+        assert torch.equal(got, full), n
+    for m in plans:
+        m.status()
+        m.close()
+    q0 = dict(p0)
+    o0 = oracle.forward(q0)
+    q1 = dict(p1)
+    q1["x"] = o0["y"].astype(np.float32)
+    o1 = oracle.forward(q1)
+    err = np.abs(full.cpu().numpy().astype(np.float64) - o1["y"]).max()
+    assert err <= 3 * TOL[prec], err

@@ -12,7 +12,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_1804_10223_b200 import inputs
-from paper_1804_10223_b200.multigpu import forward_partitioned, shard
+from paper_1804_10223_b200.multigpu import chunks, forward_layer_pipelined, forward_partitioned, shard
 
 
 def test_shard_covers_batch_exactly():
@@ -63,3 +63,61 @@ def test_gloo_world2_partitioned_equals_single(tmp_path, B):
     got = np.load(tmp_path / "y.npy")
     assert got.shape == ref.shape
     assert np.array_equal(got, ref)
+
+
+# ---- stacked layers pipelined across ranks ----
+
+def _stack_problems(cell):
+    # layer 0: I = 12 -> H = 40; layer 1: I = 40 -> H = 32 (2-layer stack)
+    p0 = inputs.make_problem(40, 12, 3, 9, 0.2, cell=cell, act="tanh", seed_offset=1)
+    p1 = inputs.make_problem(32, 40, 3, 9, 0.25, cell=cell, act="tanh", seed_offset=2)
+    return p0, p1
+
+
+def _oracle_layer_step(prob):
+    import oracle
+
+    def step(x_chunk, state):
+        p = dict(prob)
+        p["x"] = x_chunk.numpy().astype(np.float32)
+        p["T"] = x_chunk.shape[0]
+        p["h0"] = None if state is None else state[0]
+        p["c0"] = None if state is None else state[1]
+        o = oracle.forward(p)
+        # outputs of a layer are the next layer's fp32 inputs
+        return torch.from_numpy(o["y"].astype(np.float32)), (o["hT"], o.get("cT"))
+    return step
+
+
+def _pipe_worker(rank, world, port, cell, n_chunks, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    probs = _stack_problems(cell)
+    y = forward_layer_pipelined(_oracle_layer_step(probs[rank]), torch.from_numpy(probs[0]["x"]), n_chunks,
+                                [probs[0]["H"], probs[1]["H"]])
+    np.save(os.path.join(out_dir, f"y{rank}.npy"), y.numpy())
+    dist.destroy_process_group()
+
+
+def test_chunks_cover_sequence():
+    for T in (1, 7, 256):
+        for n in (1, 3, 8, 300):
+            cs = chunks(T, n)
+            assert cs[0][0] == 0 and sum(c for _, c in cs) == T
+            assert all(a + b == c for (a, b), (c, _) in zip(cs, cs[1:]))
+
+
+@pytest.mark.parametrize("cell,n_chunks", [("rnn", 3), ("lstm", 4), ("rnn", 1)])
+def test_gloo_world2_layer_pipeline_equals_unchunked(tmp_path, cell, n_chunks):
+    """Rank r = layer r, time chunks handed over by send/recv: every rank's result equals the
+    unchunked layer-by-layer run bit for bit (state carried through h0/c0)."""
+    port = _free_port()
+    mp.spawn(_pipe_worker, args=(2, port, cell, n_chunks, str(tmp_path)), nprocs=2, join=True)
+    probs = _stack_problems(cell)
+    x1 = _oracle_layer_step(probs[0])(torch.from_numpy(probs[0]["x"]), None)[0]
+    ref = _oracle_layer_step(probs[1])(x1, None)[0].numpy()
+    for r in range(2):
+        got = np.load(tmp_path / f"y{r}.npy")
+        assert got.shape == ref.shape
+        assert np.array_equal(got, ref)
