@@ -38,7 +38,8 @@ def _compile(src, verbose=False):
     newest_dep = max([os.path.getmtime(src)] + [os.path.getmtime(d) for d in _deps()])
     if os.path.exists(obj) and os.path.getmtime(obj) >= newest_dep:
         return obj, ""
-    cmd = [nvcc()] + ARCH + ["-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+    extra = os.environ.get("SRNN_NVCC_FLAGS", "").split()  # A/B experiments only (e.g. -DSRNN_PIPE_OPERATE)
+    cmd = [nvcc()] + ARCH + extra + ["-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                              "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj + ".tmp"]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"]
