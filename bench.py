@@ -311,6 +311,7 @@ def main():
     e2e_val = None
     xh = torch.empty(T, B, prob["I"])
     yh = torch.empty(T, B, H)
+    hh = torch.empty(B, H)
     if not args.no_e2e:
         from paper_1804_10223_b200 import FLAG_RESERVE_SMS
         m_dev = m

@@ -57,6 +57,8 @@ def main():
         for d in raw(rep):
             name = d["kernel"]
             key = "recurrent" if "persistent" in name else ("gemm_tc" if "gemm_tc" in name else name[:40])
+            if key == "recurrent" and ", 0>(" not in name:  # template MT > 0: dense tensor-core comparator
+                key = "recurrent_dense_tc"
             out["captures"][key] = d
             if key == "recurrent":
                 out["recurrent_dram_bytes_per_launch"] = to_bytes(d["dram__bytes_read.sum"]) + to_bytes(d["dram__bytes_write.sum"])
