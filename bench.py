@@ -339,7 +339,10 @@ def main():
         clocks = clk.summary()
         f_peak_hz = 1965e6
         smem_peak = info["sm_count"] * SMEM_BYTES_PER_CLK * f_peak_hz / 1e9  # GB/s
-        gather_bytes = 4.0 * prob["nnz"] * B * T  # algorithmic: one fp32 h element per (nonzero, sample, step)
+        # algorithmic: one staged h element per (nonzero, sample, step) -- fp16 (2 B) in fp16 mode
+        # (h is staged and exchanged in fp16, R9), fp32 (4 B) in fp32 mode
+        h_bytes = 2.0 if (prec == "fp16" and not (args.flags & (1 << 5))) else 4.0
+        gather_bytes = h_bytes * prob["nnz"] * B * T
         achieved = gather_bytes / t_rec / 1e9
         traffic, traffic_src = load_traffic()
         out = {
@@ -362,7 +365,7 @@ def main():
                          "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": "derived: 148 SMs x 128 B/clk shared-memory crossbar x 1965 MHz "
                                         "(B300_MICROARCH.md smem BW, B200_PROFILING.md clocks)",
-                         "note": "achieved = algorithmic h-gather bytes (4 B x nnz x B x T) / recurrent kernel "
+                         "note": f"achieved = algorithmic h-gather bytes ({h_bytes:g} B x nnz x B x T) / recurrent kernel "
                                  "time (CUDA events); the per-step exchange latency is not in this bound"},
             "e2e": {"value": e2e_val, "unit": "GFLOP/s", "h2d_bytes_per_step": int(xh.numel() * 4),
                     "d2h_bytes_per_step": int(yh.numel() * 4 + hh.numel() * 4),
