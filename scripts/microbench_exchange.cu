@@ -62,6 +62,8 @@ struct Args {
     unsigned* flags;            // [ncta]
     uint2* raw;                 // [2][ncta*upc] raw fp16x4 data
     long long* out;
+    unsigned delay_ns;
+    unsigned long long* pflags;  // [consumer][producer] step words
 };
 
 __global__ void k_pingpong(Args a) {
@@ -123,6 +125,142 @@ __global__ void k_a2a_bulk(Args a) {
                     if ((pend >> j & 1) && (v[j].x >> 32) == static_cast<unsigned long long>(s) &&
                         (v[j].y >> 32) == static_cast<unsigned long long>(s))
                         pend &= ~(1u << j);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (pend >> j & 1) v[j] = ld_relaxed_v2(src + base + j * blockDim.x);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// replicated bulk: producers write their slice into R copies, consumer c polls copy c % R
+// (tests whether 148 SMs polling the same L2 lines -- hot-line serialisation -- is the cost).
+// DELAY: __nanosleep before the first poll round (is the first, early round wasted?)
+template <int R>
+__global__ void k_a2a_rep(Args a) {
+    const int n = gridDim.x;
+    const int per = a.upc * a.wpu;
+    const int total = n * per;
+    const int chunks = total / 2;
+    for (int s = 1; s <= a.steps; ++s) {
+        unsigned long long* buf = a.words + static_cast<size_t>(s & 1) * total * R;
+        for (int i = threadIdx.x; i < per; i += blockDim.x) {
+            const unsigned long long w = (static_cast<unsigned long long>(s) << 32) | i;
+#pragma unroll
+            for (int r = 0; r < R; ++r) st_relaxed(buf + static_cast<size_t>(r) * total + blockIdx.x * per + i, w);
+        }
+        if (a.delay_ns) __nanosleep(a.delay_ns);
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(buf + static_cast<size_t>(blockIdx.x % R) * total);
+        for (int base = threadIdx.x; base < chunks; base += 8 * blockDim.x) {
+            ulonglong2 v[8];
+            unsigned pend = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                int idx = base + j * blockDim.x;
+                if (idx < chunks) {
+                    v[j] = ld_relaxed_v2(src + idx);
+                    pend |= 1u << j;
+                }
+            }
+            while (pend) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if ((pend >> j & 1) && (v[j].x >> 32) == static_cast<unsigned long long>(s) &&
+                        (v[j].y >> 32) == static_cast<unsigned long long>(s))
+                        pend &= ~(1u << j);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (pend >> j & 1) v[j] = ld_relaxed_v2(src + base + j * blockDim.x);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// overlapped polling: two register sets of the same chunks, the second round issued GAP ns
+// after the first, then each stale set is re-issued as soon as it has been checked, so two
+// rounds are always in flight and the L2 is sampled every ~RTT/2 instead of every RTT.
+__global__ void k_a2a_ov(Args a) {
+    const int n = gridDim.x;
+    const int per = a.upc * a.wpu;
+    const int total = n * per;
+    const int chunks = total / 2;
+    for (int s = 1; s <= a.steps; ++s) {
+        unsigned long long* dst = a.words + static_cast<size_t>(s & 1) * total;
+        for (int i = threadIdx.x; i < per; i += blockDim.x)
+            st_relaxed(dst + blockIdx.x * per + i, (static_cast<unsigned long long>(s) << 32) | i);
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(dst);
+        const unsigned long long want = static_cast<unsigned long long>(s);
+        for (int base = threadIdx.x; base < chunks; base += 8 * blockDim.x) {
+            ulonglong2 va[8], vb[8];
+            unsigned pend = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (base + j * blockDim.x < chunks) {
+                    va[j] = ld_relaxed_v2(src + base + j * blockDim.x);
+                    pend |= 1u << j;
+                }
+            if (a.delay_ns) __nanosleep(a.delay_ns);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (pend >> j & 1) vb[j] = ld_relaxed_v2(src + base + j * blockDim.x);
+            while (true) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if ((pend >> j & 1) && (va[j].x >> 32) == want && (va[j].y >> 32) == want) pend &= ~(1u << j);
+                if (!pend) break;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (pend >> j & 1) va[j] = ld_relaxed_v2(src + base + j * blockDim.x);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if ((pend >> j & 1) && (vb[j].x >> 32) == want && (vb[j].y >> 32) == want) pend &= ~(1u << j);
+                if (!pend) break;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (pend >> j & 1) vb[j] = ld_relaxed_v2(src + base + j * blockDim.x);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// per-consumer flag arrays: producer p writes word [c][p] = step for EVERY consumer c (148
+// relaxed stores into 148 different lines), consumer c polls only its own 148-word array
+// (no line is polled by more than one SM), then reads the tagged data once (stale chunks
+// re-polled: the flags are only a hint, the tags stay the correctness check -- no fences).
+__global__ void k_a2a_pflag(Args a) {
+    const int n = gridDim.x;
+    const int per = a.upc * a.wpu;
+    const int total = n * per;
+    const int chunks = total / 2;
+    for (int s = 1; s <= a.steps; ++s) {
+        unsigned long long* dst = a.words + static_cast<size_t>(s & 1) * total;
+        for (int i = threadIdx.x; i < per; i += blockDim.x)
+            st_relaxed(dst + blockIdx.x * per + i, (static_cast<unsigned long long>(s) << 32) | i);
+        if (a.delay_ns == 0) __syncthreads();  // data stores issued before the flags (not ordered: a hint)
+        for (int c = threadIdx.x; c < n; c += blockDim.x)
+            st_relaxed(a.pflags + static_cast<size_t>(c) * n + blockIdx.x, static_cast<unsigned long long>(s));
+        for (int p = threadIdx.x; p < n; p += blockDim.x)
+            while (ld_relaxed(a.pflags + static_cast<size_t>(blockIdx.x) * n + p) < static_cast<unsigned long long>(s)) {
+            }
+        __syncthreads();
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(dst);
+        const unsigned long long want = static_cast<unsigned long long>(s);
+        for (int base = threadIdx.x; base < chunks; base += 8 * blockDim.x) {
+            ulonglong2 v[8];
+            unsigned pend = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (base + j * blockDim.x < chunks) {
+                    v[j] = ld_relaxed_v2(src + base + j * blockDim.x);
+                    pend |= 1u << j;
+                }
+            while (pend) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if ((pend >> j & 1) && (v[j].x >> 32) == want && (v[j].y >> 32) == want) pend &= ~(1u << j);
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
                     if (pend >> j & 1) v[j] = ld_relaxed_v2(src + base + j * blockDim.x);
@@ -289,10 +427,12 @@ static float run(void* fn, Args a, int grid, int block) {
     cudaEventCreate(&e1);
     cudaMemset(a.words, 0, static_cast<size_t>(2) * 148 * 64 * 8 * 8);
     cudaMemset(a.flags, 0, 148 * 4 * 4);
+    cudaMemset(a.pflags, 0, static_cast<size_t>(148) * 148 * 8);
     cudaLaunchCooperativeKernel(fn, grid, block, args, 0, 0);  // warm
     cudaDeviceSynchronize();
     cudaMemset(a.words, 0, static_cast<size_t>(2) * 148 * 64 * 8 * 8);
     cudaMemset(a.flags, 0, 148 * 4 * 4);
+    cudaMemset(a.pflags, 0, static_cast<size_t>(148) * 148 * 8);
     cudaEventRecord(e0);
     cudaLaunchCooperativeKernel(fn, grid, block, args, 0, 0);
     cudaEventRecord(e1);
@@ -311,6 +451,8 @@ int main(int argc, char** argv) {
     a.upc = argc > 1 ? atoi(argv[1]) : 16;
     a.wpu = argc > 2 ? atoi(argv[2]) : 2;
     a.steps = argc > 3 ? atoi(argv[3]) : 2000;
+    a.delay_ns = 0;
+    cudaMalloc(&a.pflags, static_cast<size_t>(148) * 148 * 8);
     int ncta = 148;
     cudaMalloc(&a.words, static_cast<size_t>(2) * 148 * 64 * 8 * 8);
     cudaMalloc(&a.flags, 148 * 4 * 4);
@@ -328,6 +470,15 @@ int main(int argc, char** argv) {
         printf(", \"a2a_bulk_tagged_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_bulk), a, ncta, blk));
         printf(", \"a2a_sentinel_then_bulk_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_sent), a, ncta, blk));
         printf(", \"a2a_release_acquire_raw_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_relacq), a, ncta, blk));
+        printf(", \"a2a_rep1_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_rep<1>), a, ncta, blk));
+        printf(", \"a2a_rep2_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_rep<2>), a, ncta, blk));
+        printf(", \"a2a_rep4_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_rep<4>), a, ncta, blk));
+        printf(", \"a2a_rep8_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_rep<8>), a, ncta, blk));
+        for (unsigned d : {200u, 400u, 800u}) {
+            Args b = a;
+            b.delay_ns = d;
+            printf(", \"a2a_rep1_delay%u_us\": %.4f", d, run(reinterpret_cast<void*>(k_a2a_rep<1>), b, ncta, blk));
+        }
     }
     {
         const size_t smem = static_cast<size_t>(2) * ncta * a.upc * a.wpu * 8;
@@ -339,6 +490,25 @@ int main(int argc, char** argv) {
             b.upc = a.upc * ncta / grid + (a.upc * ncta % grid ? 1 : 0);  // same h size on fewer CTAs
             printf(", \"a2a_cluster%d_ctas\": %d, \"a2a_cluster%d_us\": %.4f", cs, grid, cs,
                    run_cluster(fn, b, grid, 512, cs, smem + 4096));
+        }
+    }
+    printf(", \"a2a_pflag_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_pflag), a, ncta, 512));
+    {
+        Args b = a;
+        b.delay_ns = 1;  // no barrier between the data and the flag stores
+        printf(", \"a2a_pflag_nobar_us\": %.4f", run(reinterpret_cast<void*>(k_a2a_pflag), b, ncta, 512));
+    }
+    for (unsigned d : {0u, 100u, 200u, 300u, 500u}) {
+        Args b = a;
+        b.delay_ns = d;
+        printf(", \"a2a_overlap_gap%u_us\": %.4f", d, run(reinterpret_cast<void*>(k_a2a_ov), b, ncta, 512));
+    }
+    // scaling of the replicated-bulk all-to-all (R = 1) with the CTA count (same h bytes) and block size
+    for (int g : {16, 37, 74, 148}) {
+        for (int blk : {256, 512, 1024}) {
+            Args b = a;
+            b.upc = a.upc * ncta / g;
+            printf(", \"a2a_ctas%d_thr%d_us\": %.4f", g, blk, run(reinterpret_cast<void*>(k_a2a_rep<1>), b, g, blk));
         }
     }
     printf(", \"bytes_tagged_per_cta\": %d, \"bytes_raw_per_cta\": %d}\n", ncta * a.upc * a.wpu * 8, ncta * a.upc * 8);
