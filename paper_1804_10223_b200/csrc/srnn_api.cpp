@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -67,7 +68,7 @@ struct srnn_plan {
     // pipelined srnn_forward_host
     uint32_t* d_ready = nullptr;     // b' rows ready (monotone counter)
     uint32_t* d_progress = nullptr;  // per-CTA progress increments (monotone counter)
-    uint32_t ready_base = 0, progress_base = 0;
+    uint32_t ready_cur = 0, progress_base = 0;  // ready_cur: value of *d_ready between calls
     cudaStream_t s_rec = nullptr, s_out = nullptr, s_copy = nullptr;
     cudaEvent_t ev_in = nullptr, ev_rec = nullptr;
     cudaEvent_t ev_chunk[10] = {};  // x chunk c resident (s_copy -> projection stream)
@@ -976,25 +977,35 @@ srnn_status_t srnn_forward_host(srnn_plan_t p, int32_t T, int32_t B, const float
     // batch allows (a partial tile costs the projection as much as a full one)
     int in_b[10] = {0};
     int n_chunks = 0;
+    static const int max_in = std::max(1, std::min(8, std::getenv("SRNN_PIPE_IN_CHUNKS") ? std::atoi(std::getenv("SRNN_PIPE_IN_CHUNKS")) : 8));
+    static const int max_out = std::max(1, std::getenv("SRNN_PIPE_OUT_CHUNKS") ? std::atoi(std::getenv("SRNN_PIPE_OUT_CHUNKS")) : 16);
+    // the persistent kernel is enqueued on `st` right behind chunk 0's projection (same-stream
+    // order, no cross-stream event on the critical path); later chunks are projected on s_rec
+    static const bool k_on_st = !(std::getenv("SRNN_PIPE_KERNEL_ON_ST") && std::atoi(std::getenv("SRNN_PIPE_KERNEL_ON_ST")) == 0);
+    cudaStream_t kst = k_on_st ? st : p->s_rec;
+    cudaStream_t pst = k_on_st ? p->s_rec : st;
     {
         const int q = std::max(1, 128 / B);  // steps per 128 rows
-        int per = (T + 7) / 8;
+        int per = (T + max_in - 1) / max_in;
         per = ((per + q - 1) / q) * q;
-        for (int s0 = 0; s0 < T && n_chunks < 8; s0 += per) in_b[++n_chunks] = std::min(T, s0 + per);
+        for (int s0 = 0; s0 < T && n_chunks < max_in; s0 += per) in_b[++n_chunks] = std::min(T, s0 + per);
         in_b[n_chunks] = T;
     }
     // output chunks: 16 even ones (the last one's copy is the exposed tail)
-    const int every = (T + std::min(16, T) - 1) / std::min(16, T);
+    const int every = (T + std::min(max_out, T) - 1) / std::min(max_out, T);
     const int n_out = (T + every - 1) / every;
-    const uint32_t ready_base = p->ready_base, prog_base = p->progress_base;
-    if (h0_host) e = cudaMemcpyAsync(p->d_h0, h0_host, hb, cudaMemcpyHostToDevice, p->s_rec);
-    if (e == cudaSuccess && c0_host && p->G == 4) e = cudaMemcpyAsync(p->d_c0, c0_host, hb, cudaMemcpyHostToDevice, p->s_rec);
+    const uint32_t prog_base = p->progress_base;
+    if (h0_host) e = cudaMemcpyAsync(p->d_h0, h0_host, hb, cudaMemcpyHostToDevice, kst);
+    if (e == cudaSuccess && c0_host && p->G == 4) e = cudaMemcpyAsync(p->d_c0, c0_host, hb, cudaMemcpyHostToDevice, kst);
     if (e != cudaSuccess) return SRNN_ERR_CUDA;
     // SRNN_PIPE_TRACE: timing events at every stage, printed to stderr (diagnostics)
     static const bool trace = std::getenv("SRNN_PIPE_TRACE") != nullptr;
     std::vector<std::pair<std::string, cudaEvent_t>> tr;
+    const auto host_t0 = std::chrono::steady_clock::now();
+    std::vector<std::pair<std::string, double>> host_tr;  // host enqueue times (trace only)
     auto mark = [&](const std::string& label, cudaStream_t where) {
         if (!trace) return;
+        host_tr.emplace_back(label, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - host_t0).count());
         cudaEvent_t ev;
         cudaEventCreate(&ev);
         cudaEventRecord(ev, where);
@@ -1014,15 +1025,20 @@ srnn_status_t srnn_forward_host(srnn_plan_t p, int32_t T, int32_t B, const float
         mark("x" + std::to_string(c) + " in", p->s_copy);
         return SRNN_OK;
     };
+    // The kernel treats steps <= *d_ready - ready_base as projected.  Chunk 0 is projected on
+    // the kernel's own stream before it starts, so the base is chosen to cover it without a
+    // stream memory op on the critical path; chunk c >= 1 then writes ready_base + its last step.
+    const uint32_t ready_base = p->ready_cur - static_cast<uint32_t>(in_b[1]);
     // chunk c: projection once its x rows are resident, then d_ready = base + (its last step + 1)
-    auto feed_chunk = [&](int c, int sms) -> srnn_status_t {
+    auto feed_chunk = [&](int c, int sms, cudaStream_t fst) -> srnn_status_t {
         const int s0 = in_b[c], s1 = in_b[c + 1];
         const int64_t r0 = static_cast<int64_t>(s0) * B, nr = static_cast<int64_t>(s1 - s0) * B;
-        if (cudaStreamWaitEvent(st, p->ev_chunk[c], 0) != cudaSuccess) return SRNN_ERR_CUDA;
-        srnn_status_t fs = project_rows(p, r0, nr, p->d_x, p->d_bprime, st, sms);
+        if (cudaStreamWaitEvent(fst, p->ev_chunk[c], 0) != cudaSuccess) return SRNN_ERR_CUDA;
+        srnn_status_t fs = project_rows(p, r0, nr, p->d_x, p->d_bprime, fst, sms);
         if (fs != SRNN_OK) return fs;
-        mark("b'" + std::to_string(c) + " ready", st);
-        if (g_write32(st, reinterpret_cast<CUdeviceptr>(p->d_ready), ready_base + static_cast<uint32_t>(s1),
+        mark("b'" + std::to_string(c) + " ready", fst);
+        if (c == 0) return SRNN_OK;  // covered by ready_base
+        if (g_write32(fst, reinterpret_cast<CUdeviceptr>(p->d_ready), ready_base + static_cast<uint32_t>(s1),
                       CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
             return SRNN_ERR_CUDA;
         return SRNN_OK;
@@ -1030,27 +1046,25 @@ srnn_status_t srnn_forward_host(srnn_plan_t p, int32_t T, int32_t B, const float
     // The first chunk is projected on every SM before the persistent kernel
     // starts; the others on the SMs it leaves free, while it runs.
     srnn_status_t s = copy_chunk(0);
-    if (s == SRNN_OK) s = feed_chunk(0, p->sm_count);
+    if (s == SRNN_OK) s = feed_chunk(0, p->sm_count, kst);
     if (s != SRNN_OK) return s;
-    if (cudaEventRecord(p->ev_in, st) != cudaSuccess || cudaStreamWaitEvent(p->s_rec, p->ev_in, 0) != cudaSuccess)
-        return SRNN_ERR_CUDA;
     PipeArgs pa;
     pa.bp_ready = p->d_ready;
     pa.bp_ready_base = ready_base;
     pa.progress = y_host ? p->d_progress : nullptr;
     pa.every = every;
-    mark("kernel launch", p->s_rec);
+    mark("kernel launch", kst);
     s = recurrence_impl(p, T, B, p->d_bprime, h0_host ? p->d_h0 : nullptr, c0_host ? p->d_c0 : nullptr,
-                        y_host ? p->d_y : nullptr, p->d_hT, p->G == 4 ? p->d_cT : nullptr, p->s_rec, pa);
+                        y_host ? p->d_y : nullptr, p->d_hT, p->G == 4 ? p->d_cT : nullptr, kst, pa);
     if (s != SRNN_OK) return s;
-    mark("kernel done", p->s_rec);
-    if (cudaEventRecord(p->ev_rec, p->s_rec) != cudaSuccess) return SRNN_ERR_CUDA;
+    mark("kernel done", kst);
+    if (cudaEventRecord(p->ev_rec, kst) != cudaSuccess) return SRNN_ERR_CUDA;
     for (int c = 1; c < n_chunks; ++c) {
         s = copy_chunk(c);
         if (s != SRNN_OK) return s;
     }
     for (int c = 1; c < n_chunks; ++c) {
-        s = feed_chunk(c, p->sm_count - p->lay.num_ctas);
+        s = feed_chunk(c, p->sm_count - p->lay.num_ctas, pst);
         if (s != SRNN_OK) return s;
     }
     (void)GH;
@@ -1068,13 +1082,14 @@ srnn_status_t srnn_forward_host(srnn_plan_t p, int32_t T, int32_t B, const float
         }
         p->progress_base = prog_base + C * static_cast<uint32_t>(n_out);
     }
-    p->ready_base = ready_base + static_cast<uint32_t>(T) + 1;
+    if (n_chunks > 1) p->ready_cur = ready_base + static_cast<uint32_t>(T);
     e = cudaStreamWaitEvent(p->s_out, p->ev_rec, 0);
     if (e == cudaSuccess && hT_host) e = cudaMemcpyAsync(hT_host, p->d_hT, hb, cudaMemcpyDeviceToHost, p->s_out);
     if (e == cudaSuccess && cT_host && p->G == 4) e = cudaMemcpyAsync(cT_host, p->d_cT, hb, cudaMemcpyDeviceToHost, p->s_out);
     if (e == cudaSuccess) e = cudaMemcpyAsync(p->h_status, p->d_status, 4, cudaMemcpyDeviceToHost, p->s_out);
     if (e == cudaSuccess) e = cudaStreamSynchronize(p->s_out);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->s_rec);
     if (e != cudaSuccess) return SRNN_ERR_CUDA;
     mark("end", p->s_out);
     if (trace) {
@@ -1084,6 +1099,7 @@ srnn_status_t srnn_forward_host(srnn_plan_t p, int32_t T, int32_t B, const float
             cudaEventElapsedTime(&ms, tr[0].second, t.second);
             std::fprintf(stderr, "srnn pipe: %8.1f us  %s\n", 1000.0 * ms, t.first.c_str());
         }
+        for (auto& h : host_tr) std::fprintf(stderr, "srnn pipe host: %8.1f us  %s enqueued\n", h.second, h.first.c_str());
         for (auto& t : tr) cudaEventDestroy(t.second);
     }
     if (*p->h_status != 0) return srnn_plan_status(p);  // reads and clears it

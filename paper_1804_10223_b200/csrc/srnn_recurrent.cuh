@@ -722,11 +722,14 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     if (grid_sync) cg::this_grid().sync();
     __syncthreads();
 
+    // pipelined host forward: b' arrives in chunks of steps and the ready counter only
+    // grows, so each thread re-polls (acquire) only when its last observed value is behind
+    uint32_t bp_seen = p.bp_ready_base;
     auto issue_bprime = [&](int s, int k, int b) {
         float* dstb = bpsb + b * G * umax_bt;
-        if (p.bp_ready != nullptr && tid < n_items) {  // pipelined host forward: wait for this step's b'
+        if (p.bp_ready != nullptr && tid < n_items && static_cast<int32_t>(bp_seen - p.bp_ready_base) < s) {
             Watchdog wdb{0ull, 0u};
-            while (static_cast<int32_t>(ld_acquire_u32(p.bp_ready) - p.bp_ready_base) < s)
+            while (static_cast<int32_t>((bp_seen = ld_acquire_u32(p.bp_ready)) - p.bp_ready_base) < s)
                 if (watchdog_tick(wdb, p.status, p.timeout_ns)) break;
         }
         for (int j = 0; j < item_rounds; ++j) {
