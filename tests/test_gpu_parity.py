@@ -424,3 +424,14 @@ def test_stacked_chunked_wavefront(cuda_device, prec, cell):
     o1 = oracle.forward(q1)
     err = np.abs(full.cpu().numpy().astype(np.float64) - o1["y"]).max()
     assert err <= 3 * TOL[prec], err
+
+
+@pytest.mark.parametrize("H,B,T,d", [
+    (5760, 4, 32, 0.10),   # C3 large-H corner (smem weight tier / narrow lanes), every output
+    (1152, 32, 24, 0.50),  # C3 large-batch / high-density corner: two tiles of 16
+    (4096, 8, 32, 0.01),   # C3 low-density corner, one tile of 8
+])
+def test_C3_sweep_corners(cuda_device, H, B, T, d):
+    prob = inputs.make_problem(H, H, B, T, d, act="relu", h0="random", seed_offset=3)
+    g, o, err = check(prob, "fp16")
+    print("C3 corner", H, B, d, "err", err, g["info"]["num_ctas"], g["info"]["batch_tile"])
