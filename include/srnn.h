@@ -88,6 +88,10 @@ typedef enum { SRNN_PREC_FP32 = 0, SRNN_PREC_FP16W_FP32ACC = 1 } srnn_prec_t;
                                               chunks are copied and projected (GEMM on the free SMs)
                                               while the persistent kernel runs, y chunks are copied
                                               back as the kernel reports progress               */
+#define SRNN_FLAG_DEBUG_DROP_PUBLISH (1u << 9) /* fault injection: CTA 0 never publishes h_2 (a lost
+                                              exchange message); the device watchdog must end the
+                                              kernel and srnn_plan_status report SRNN_ERR_TIMEOUT
+                                              (timeout: env SRNN_TIMEOUT_MS, default 2000)       */
 #define SRNN_FLAG_DENSE_TC       (1u << 8) /* comparator: the DENSE persistent
                                               RNN of PAPER.md:51-71 (Sec. 3.2, Diamos et al.)
                                               re-done for sm_100a tensor cores.  U_r is densified

@@ -1102,7 +1102,12 @@ srnn_status_t srnn_forward_host(srnn_plan_t p, int32_t T, int32_t B, const float
         for (auto& h : host_tr) std::fprintf(stderr, "srnn pipe host: %8.1f us  %s enqueued\n", h.second, h.first.c_str());
         for (auto& t : tr) cudaEventDestroy(t.second);
     }
-    if (*p->h_status != 0) return srnn_plan_status(p);  // reads and clears it
+    if (*p->h_status != 0) {
+        // the aborted kernel bumped the progress counter past every wait: resynchronise
+        uint32_t v = 0;
+        if (cudaMemcpy(&v, p->d_progress, 4, cudaMemcpyDeviceToHost) == cudaSuccess) p->progress_base = v;
+        return srnn_plan_status(p);  // reads and clears it
+    }
     return SRNN_OK;
 }
 

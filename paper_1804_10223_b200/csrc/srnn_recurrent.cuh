@@ -40,6 +40,7 @@ namespace cg = cooperative_groups;
 constexpr uint32_t kFlagGridSync = 1u << 0;
 constexpr uint32_t kFlagJitter = 1u << 4;
 constexpr uint32_t kFlagProfile = 1u << 6;
+constexpr uint32_t kFlagDropPublish = 1u << 9;
 
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -686,6 +687,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     // Publish item e's h of (step s, tile k) as tagged words.  Called by all
     // threads of the CTA (the fp16 pairing uses a shuffle); `ok` masks items.
     auto publish = [&](int s, int k, int e, bool ok, float h) {
+        if ((p.flags & kFlagDropPublish) && cta == 0 && s == 2) return;  // fault injection (CTA-uniform)
         unsigned long long* dst = p.xbuf + static_cast<size_t>((s & 1) * p.n_tiles + k) * tile_stride;
         const uint32_t tag = p.epoch + static_cast<uint32_t>(s);
         if ((n_words & 1) && cta == 0 && e == 0)  // keep every 16-byte chunk whole: tagged pad word
@@ -907,6 +909,9 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
         }
     }
 done:
+    // An aborted launch (watchdog / lost message) still releases the host pipeline's
+    // y-copy waits on the progress counter (the host re-reads the counter on error).
+    if (*s_abort && p.progress != nullptr && tid == 0) atomicAdd(p.progress, 1u << 20);
     return;
 }
 

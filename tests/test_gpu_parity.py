@@ -435,3 +435,30 @@ def test_C3_sweep_corners(cuda_device, H, B, T, d):
     prob = inputs.make_problem(H, H, B, T, d, act="relu", h0="random", seed_offset=3)
     g, o, err = check(prob, "fp16")
     print("C3 corner", H, B, d, "err", err, g["info"]["num_ctas"], g["info"]["batch_tile"])
+
+
+@pytest.mark.parametrize("flags", [0, FLAG_DENSE_TC])
+def test_lost_message_watchdog(cuda_device, monkeypatch, flags):
+    """Fault injection: CTA 0 drops its h_2 publish.  The device
+    watchdog must end the persistent kernel (no hang) and surface SRNN_ERR_TIMEOUT;
+    the status word is cleared by reading it and a fresh plan runs correctly."""
+    import torch
+    from paper_1804_10223_b200 import SrnnError
+    from paper_1804_10223_b200._lib import FLAG_DEBUG_DROP_PUBLISH
+    monkeypatch.setenv("SRNN_TIMEOUT_MS", "200")
+    prob = inputs.make_problem(512, 512, 4, 8, 0.1, act="tanh")
+    m = from_problem(prob, prec="fp16", flags=flags | FLAG_DEBUG_DROP_PUBLISH)
+    m.forward(torch.from_numpy(prob["x"]).cuda())
+    torch.cuda.synchronize()
+    with pytest.raises(SrnnError) as e:
+        m.status()
+    assert e.value.code == -6
+    m.status()  # cleared
+    m.close()
+    # the pipelined host call must not hang on its y-copy waits either
+    m = from_problem(prob, prec="fp16", flags=flags | FLAG_DEBUG_DROP_PUBLISH | FLAG_RESERVE_SMS)
+    with pytest.raises(SrnnError) as e:
+        m.forward_host(prob["x"])
+    assert e.value.code == -6
+    m.close()
+    check(prob, "fp16", flags=flags)
