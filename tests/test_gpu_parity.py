@@ -462,3 +462,31 @@ def test_lost_message_watchdog(cuda_device, monkeypatch, flags):
     assert e.value.code == -6
     m.close()
     check(prob, "fp16", flags=flags)
+
+
+@pytest.mark.parametrize("concurrent", [False, True])
+def test_bidirectional_layer(cuda_device, concurrent):
+    """Forward + time-reversed backward plan, y = [y_fwd ; flip(y_bwd)], against the oracle
+    run on x and on x reversed; concurrent: the two directions on two streams, half the SMs
+    each (slow on B200, but it must stay correct and deadlock-free)."""
+    import torch
+    from paper_1804_10223_b200.layers import BiSparseRNN
+    T, B, H = 24, 4, 700
+    pf = inputs.make_problem(H, 300, B, T, 0.1, act="tanh", seed_offset=21)
+    pb = inputs.make_problem(H, 300, B, T, 0.1, act="tanh", seed_offset=22)
+    pb["x"] = pf["x"]
+    n = torch.cuda.get_device_properties(0).multi_processor_count // 2 if concurrent else 0
+    bi = BiSparseRNN.from_problems(pf, pb, prec="fp16", num_ctas=n)
+    st = (torch.cuda.Stream(), torch.cuda.Stream()) if concurrent else None
+    y, hf, hb = bi.forward(torch.from_numpy(pf["x"]).cuda(), streams=st)
+    torch.cuda.synchronize()
+    bi.status()
+    bi.close()
+    of = oracle.forward(pf)
+    qb = dict(pb)
+    qb["x"] = np.ascontiguousarray(pf["x"][::-1])
+    ob = oracle.forward(qb)
+    ref = np.concatenate([of["y"], ob["y"][::-1]], axis=2)
+    err = np.abs(y.cpu().numpy().astype(np.float64) - ref).max()
+    assert err <= TOL["fp16"], err
+    assert np.abs(hb.cpu().numpy() - ob["hT"]).max() <= TOL["fp16"]
