@@ -6,8 +6,8 @@ package.  The product package ``paper_1804_10223_b200`` never imports it and
 shares no code with it; the C source ``srnn_oracle.c`` is compiled here with
 plain ``gcc -O2`` (no fast-math) into ``oracle/_build/libsrnn_oracle.so``.
 
-Functions follow PAPER.md Eq. 1/2 (lines 43-49, Sec. 3.1) and the LSTM case
-study (App. B) -- see the header of ``srnn_oracle.c`` for the
+Functions follow PAPER.md Eq. 1/2 (lines 43-49, Sec. 3.1), the LSTM case
+study (App. B) and the GRU cell extension (R15) -- see the header of ``srnn_oracle.c`` for the
 exact definitions and DESIGN.md for the readings (R1..R8) they rely on.
 
 Inputs are the user's fp32 arrays upcast exactly to float64 (SURVEY.md
@@ -55,6 +55,8 @@ def _load():
             lib.oracle_rnn_forward.restype = None
             lib.oracle_lstm_forward.argtypes = [ctypes.c_int32] * 3 + [P] * 10
             lib.oracle_lstm_forward.restype = None
+            lib.oracle_gru_forward.argtypes = [ctypes.c_int32] * 3 + [P] * 9
+            lib.oracle_gru_forward.restype = None
             _lib = lib
     return _lib
 
@@ -134,6 +136,25 @@ def lstm_forward(H, rowptr, col, val, bp, h0=None, c0=None):
     return y, hT, cT
 
 
+def gru_forward(H, rowptr, col, val, bp, bhn=None, h0=None):
+    """GRU (cell extension, R15): 3H CSR rows [r; z; n], n-gate recurrent bias bhn [H].
+
+    bp: [T, B, 3H]. Returns (y [T,B,H], hT [B,H]) float64.
+    """
+    bp = _d(bp)
+    T, B, R = bp.shape
+    assert R == 3 * H
+    rp, cl, vl = _csr(rowptr, col, val)
+    assert rp.shape[0] == 3 * H + 1
+    bhn = _d(bhn)
+    h0 = _d(h0)
+    y = np.empty((T, B, H), dtype=np.float64)
+    hT = np.empty((B, H), dtype=np.float64)
+    work = np.empty(4 * H, dtype=np.float64)
+    _load().oracle_gru_forward(H, B, T, _p(rp), _p(cl), _p(vl), _p(bp), _p(bhn), _p(h0), _p(y), _p(hT), _p(work))
+    return y, hT
+
+
 def forward(prob, act=None, quantize_fp16=False):
     """Whole hot path on a problem dict from ``paper_1804_10223_b200.inputs``.
 
@@ -150,8 +171,14 @@ def forward(prob, act=None, quantize_fp16=False):
         val = np.asarray(val, np.float32).astype(np.float16).astype(np.float64)
         wx = np.asarray(wx, np.float32).astype(np.float16).astype(np.float64)
         x = np.asarray(x, np.float32).astype(np.float16).astype(np.float64)
-    bp = input_projection(x, wx, prob["bias"])
     H = prob["H"]
+    bias = prob["bias"]
+    if cell == "gru":  # bias = [b_r; b_z; b_n; b_hn] (4H): the projection takes the first 3H
+        bp = input_projection(x, wx, None if bias is None else np.asarray(bias)[:3 * H])
+        y, hT = gru_forward(H, prob["rowptr"], prob["col"], val, bp,
+                            None if bias is None else np.asarray(bias)[3 * H:], prob.get("h0"))
+        return {"y": y, "hT": hT, "bp": bp}
+    bp = input_projection(x, wx, bias)
     if cell == "rnn":
         y, hT = rnn_forward(H, prob["rowptr"], prob["col"], val, bp, prob.get("h0"), act)
         return {"y": y, "hT": hT, "bp": bp}

@@ -146,3 +146,37 @@ void oracle_lstm_forward(int32_t H, int32_t B, int32_t T, const int64_t *rowptr,
         if (cT) memcpy(cT + (int64_t)b * H, c, sizeof(double) * (size_t)H);
     }
 }
+
+/*
+ * GRU over T steps (SURVEY.md Sec. 8(f)4 cell extension; not in the paper --
+ * DESIGN.md reading R15: the "reset gate after the product" form of cuDNN /
+ * torch.nn.GRU, so each step needs one sparse product of h_{t-1}):
+ *   U (CSR) has 3H rows: gate blocks [r; z; n], row q*H + j = gate q of unit j.
+ *   bp: [T][B][3H] = W x_t + b (b_r, b_z already include the recurrent biases)
+ *   bhn: [H] recurrent bias of the n gate (inside r * (.)), or NULL (= 0)
+ *     r = sigma(U_r h + bp_r)     z = sigma(U_z h + bp_z)
+ *     n = tanh(bp_n + r * (U_n h + bhn))      h' = (1 - z) * n + z * h
+ *   h0: [B][H] or NULL; y: [T][B][H]; hT: [B][H] or NULL
+ *   work: scratch of H + 3*H doubles
+ */
+void oracle_gru_forward(int32_t H, int32_t B, int32_t T, const int64_t *rowptr,
+                        const int32_t *col, const double *val, const double *bp,
+                        const double *bhn, const double *h0, double *y, double *hT,
+                        double *work) {
+    double *h = work, *z = work + H;
+    for (int32_t b = 0; b < B; ++b) {
+        for (int32_t j = 0; j < H; ++j) h[j] = h0 ? h0[(int64_t)b * H + j] : 0.0;
+        for (int32_t t = 0; t < T; ++t) {
+            oracle_spmv(3 * H, rowptr, col, val, h, z);
+            const double *bpt = bp + ((int64_t)t * B + b) * 3 * H;
+            for (int32_t j = 0; j < H; ++j) {
+                double r = oracle_sigmoid(z[j] + bpt[j]);
+                double u = oracle_sigmoid(z[H + j] + bpt[H + j]);
+                double n = tanh(bpt[2 * H + j] + r * (z[2 * H + j] + (bhn ? bhn[j] : 0.0)));
+                h[j] = (1.0 - u) * n + u * h[j];
+            }
+            if (y) memcpy(y + ((int64_t)t * B + b) * H, h, sizeof(double) * (size_t)H);
+        }
+        if (hT) memcpy(hT + (int64_t)b * H, h, sizeof(double) * (size_t)H);
+    }
+}

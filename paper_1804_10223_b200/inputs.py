@@ -69,7 +69,7 @@ def make_problem(H, I=None, B=4, T=256, density=0.1, cell="rnn", act="relu",
                  pattern="unstructured", seed_offset=0, rho=0.8, h0="zero", c0="zero"):
     """Synthetic problem with the paper's shapes (see module docstring)."""
     I = H if I is None else I
-    G = 4 if cell == "lstm" else 1
+    G = {"rnn": 1, "lstm": 4, "gru": 3}[cell]
     R = G * H
     rowptr, col = sparse_pattern(R, H, density, pattern, seed_offset)
     nnz = int(rowptr[-1])
@@ -79,7 +79,8 @@ def make_problem(H, I=None, B=4, T=256, density=0.1, cell="rnn", act="relu",
     ax = np.sqrt(3.0 / I)
     wx = _rng("wx", seed_offset).uniform(-ax, ax, size=(R, I)).astype(np.float32)
     x = _rng("x", seed_offset).uniform(-1.0, 1.0, size=(T, B, I)).astype(np.float32)
-    bias = _rng("b", seed_offset).uniform(-0.1, 0.1, size=R).astype(np.float32)
+    # GRU: [b_r; b_z; b_n; b_hn] -- the n gate's recurrent bias sits inside r * (.)
+    bias = _rng("b", seed_offset).uniform(-0.1, 0.1, size=R + (H if cell == "gru" else 0)).astype(np.float32)
     prob = {"H": H, "I": I, "B": B, "T": T, "density": density, "cell": cell, "act": act,
             "pattern": pattern, "G": G, "rowptr": rowptr, "col": col, "val": val,
             "wx": wx, "bias": bias, "x": x, "h0": None, "c0": None, "nnz": nnz}

@@ -164,6 +164,41 @@ def test_sparse_lstm_vs_torch_lstm_densified():
     np.testing.assert_allclose(o["y"], yt.numpy(), rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("density,pattern", [(1.0, "unstructured"), (0.3, "row_balanced")])
+def test_gru_vs_torch_gru_densified(density, pattern):
+    """GRU cell extension (R15) == torch.nn.GRU float64 with the pruned zeros put
+    back: gate blocks [r; z; n], bias_ih = b[:3H], bias_hh = [0; 0; b_hn]."""
+    torch = pytest.importorskip("torch")
+    H, I, B, T = 18, 7, 3, 6
+    p = inputs.make_problem(H, I, B, T, density, cell="gru", pattern=pattern, h0="random")
+    gru = torch.nn.GRU(I, H, dtype=torch.float64)
+    with torch.no_grad():
+        gru.weight_hh_l0.copy_(torch.from_numpy(csr_to_dense(p["rowptr"], p["col"], p["val"], 3 * H, H)))
+        gru.weight_ih_l0.copy_(torch.from_numpy(p["wx"].astype(np.float64)))
+        gru.bias_ih_l0.copy_(torch.from_numpy(p["bias"][:3 * H].astype(np.float64)))
+        gru.bias_hh_l0.zero_()
+        gru.bias_hh_l0[2 * H:].copy_(torch.from_numpy(p["bias"][3 * H:].astype(np.float64)))
+        yt, hn = gru(torch.from_numpy(p["x"].astype(np.float64)), torch.from_numpy(p["h0"].astype(np.float64))[None])
+    o = oracle.forward(p)
+    np.testing.assert_allclose(o["y"], yt.numpy(), rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(o["hT"], hn[0].numpy(), rtol=1e-12, atol=1e-12)
+
+
+def test_gru_zero_weights_and_saturated_update_gate():
+    """Closed forms: U = W = 0, b = 0 -> r = z = 1/2, n = 0, h_t = h_0 / 2^t; a saturated update
+    gate (b_z -> +inf) keeps h = h_0 for any input."""
+    H, B, T = 5, 2, 4
+    p = inputs.make_problem(H, 3, B, T, 0.0, cell="gru", h0="random")
+    p["wx"] = np.zeros_like(p["wx"])
+    p["bias"] = np.zeros_like(p["bias"])
+    o = oracle.forward(p)
+    for t in range(T):
+        np.testing.assert_array_equal(o["y"][t], p["h0"].astype(np.float64) / 2.0 ** (t + 1))
+    p["bias"][H:2 * H] = 1e4
+    o = oracle.forward(p)
+    np.testing.assert_array_equal(o["hT"], p["h0"].astype(np.float64))
+
+
 # ------------------------------------------------------------- invariants ---
 
 @pytest.mark.parametrize("act", ["relu", "tanh", "identity"])
