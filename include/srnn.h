@@ -23,7 +23,9 @@
  *     srnn_destroy.  Nothing is retained after a call returns except what
  *     srnn_load_weights copies.
  *   - Layouts are row-major, fp32 unless stated: x [T][B][I], h0/c0/hT/cT
- *     [B][H], y [T][B][H], W_x [G*H][I], bias [G*H]; G = 1 (RNN) or 4 (LSTM).
+ *     [B][H], y [T][B][H], W_x [G*H][I], bias [G*H]; G = 1 (RNN), 4 (LSTM) or
+ *     3 (GRU, whose bias has 4H entries: [b_r; b_z; b_n; b_hn]).  c0/cT are
+ *     used by the LSTM only.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
  *     stream).  Device work is enqueued asynchronously; errors of the
  *     asynchronous part surface through srnn_plan_status after the caller
@@ -57,8 +59,10 @@ typedef enum {
     SRNN_ERR_UNSUPPORTED = -7    /* configuration not supported by this build     */
 } srnn_status_t;
 
-/* Cell type: vanilla RNN (Eq. 2) or LSTM. */
-typedef enum { SRNN_CELL_RNN = 0, SRNN_CELL_LSTM = 1 } srnn_cell_t;
+/* Cell type: vanilla RNN (Eq. 2), LSTM, or GRU (a cell extension
+ * beyond the paper; reading R15: gate blocks
+ * [r; z; n], n = tanh(W_n x + b_n + r * (U_n h + b_hn)), h' = (1 - z) n + z h). */
+typedef enum { SRNN_CELL_RNN = 0, SRNN_CELL_LSTM = 1, SRNN_CELL_GRU = 2 } srnn_cell_t;
 
 /* Activation g of Eq. 1/2 ("g is an elementwise activation
  * function"; unspecified by the paper -> a parameter, R1).
@@ -167,7 +171,8 @@ srnn_status_t srnn_plan_query(srnn_plan_t plan, srnn_plan_info_t *out);
 /* Load the layer's weights (host pointers; copied, caller may free after).
  *   wh_rowptr [G*H+1] int32, wh_col [nnz] int32 in [0,H), wh_val [nnz] fp32:
  *       U_r in CSR (rows = gate*H + unit for LSTM), no duplicate (row,col);
- *   wx [G*H][I] fp32 row-major (dense W), bias [G*H] fp32 or NULL.
+ *   wx [G*H][I] fp32 row-major (dense W), bias [G*H] fp32 or NULL
+ *       (GRU: [4H] = [b_r; b_z; b_n; b_hn], the last block the n gate's recurrent bias).
  * Runs the packer (PAPER.md:91 zero padding, :99-100 + App. A Alg. 1
  * bank-aware order, re-targeted to sm_100a shared-memory phases; fp16 RNE
  * quantisation in FP16W mode) and uploads the image (skipped in host-only

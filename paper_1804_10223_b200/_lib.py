@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("SRNN_LIB") or os.path.join(_PKG, "libsrnn.so")  # SRN
 SRNN_OK = 0
 STATUS = {0: "SRNN_OK", -1: "SRNN_ERR_INVALID_VALUE", -2: "SRNN_ERR_NOT_ON_CHIP", -3: "SRNN_ERR_BAD_WEIGHTS",
           -4: "SRNN_ERR_STATE", -5: "SRNN_ERR_CUDA", -6: "SRNN_ERR_TIMEOUT", -7: "SRNN_ERR_UNSUPPORTED"}
-CELL = {"rnn": 0, "lstm": 1}
+CELL = {"rnn": 0, "lstm": 1, "gru": 2}
 ACT = {"relu": 0, "tanh": 1, "identity": 2}
 PREC = {"fp32": 0, "fp16": 1}
 FLAG_GRID_SYNC = 1 << 0
@@ -131,7 +131,7 @@ class SparseRNN:
         self.cfg = Config(hidden, input, batch, max_steps, float(density), CELL[cell], ACT[act], PREC[prec],
                           device, flags, num_ctas, lanes_per_row, batch_tile)
         self.H, self.I, self.B_max, self.T_max = hidden, input, batch, max_steps
-        self.G = 4 if cell == "lstm" else 1
+        self.G = {"rnn": 1, "lstm": 4, "gru": 3}[cell]
         self.cell, self.prec = cell, prec
         self.device = device
         h = ctypes.c_void_p()
@@ -165,6 +165,8 @@ class SparseRNN:
         bias = None if bias is None else np.ascontiguousarray(bias, dtype=np.float32)
         assert rowptr.shape == (self.G * self.H + 1,), rowptr.shape
         assert wx.shape == (self.G * self.H, self.I), wx.shape
+        if bias is not None:  # GRU: [b_r; b_z; b_n; b_hn]
+            assert bias.shape == ((self.G + (1 if self.cell == "gru" else 0)) * self.H,), bias.shape
         _check("srnn_load_weights", self.lib.srnn_load_weights(
             self.handle, _ptr(rowptr), _ptr(col), _ptr(val), int(col.shape[0]), _ptr(wx), _ptr(bias)))
         return self

@@ -54,6 +54,7 @@ struct srnn_plan {
     alignas(64) CUtensorMap map_x16;
     alignas(64) CUtensorMap map_wx16;
     float* d_bias = nullptr;
+    float* d_bhn = nullptr;         // GRU: n-gate recurrent bias [H]
     float* d_bprime = nullptr;      // [T_max][B_max][G*H]
     unsigned long long* d_xbuf = nullptr;
     int32_t* d_status = nullptr;
@@ -105,7 +106,7 @@ int elem_bytes(bool f16, int bt) { return f16 ? 2 * bt : 4 * bt; }
 size_t smem_for(const srnn_plan* p, int units_max, int bt, int n_tiles) {
     size_t s = (static_cast<size_t>(p->cfg.hidden) * elem_bytes(p->f16, bt) + 15) & ~static_cast<size_t>(15);
     s += 3 * static_cast<size_t>(p->G) * units_max * bt * 4;  // zs + double-buffered b' staging
-    if (p->G == 4) s += static_cast<size_t>(n_tiles) * units_max * bt * 4;
+    if (p->G >= 3) s += static_cast<size_t>(n_tiles) * units_max * bt * 4;  // LSTM c / GRU fp32 h
     return s + 16;
 }
 
@@ -117,6 +118,7 @@ void free_device(srnn_plan* p) {
     cudaFree(p->d_wx16);
     cudaFree(p->d_x16);
     cudaFree(p->d_bias);
+    cudaFree(p->d_bhn);
     cudaFree(p->d_bprime);
     cudaFree(p->d_xbuf);
     cudaFree(p->d_status);
@@ -210,9 +212,9 @@ size_t dense_smem(const srnn_plan* p, int umax) {
 
 srnn_status_t create_dense(srnn_plan* p, srnn_plan_t* out) {
     const srnn_config_t& c = p->cfg;
-    if (!p->f16) {
+    if (!p->f16 || p->G == 3) {
         delete p;
-        return SRNN_ERR_UNSUPPORTED;  // fp16 fragments and fp16 h staging only
+        return SRNN_ERR_UNSUPPORTED;  // fp16 fragments and fp16 h staging only; RNN and LSTM cells
     }
     int bt = c.batch > 4 ? 8 : 4;
     if (c.batch_tile == 4 || c.batch_tile == 8) bt = c.batch_tile;
@@ -335,7 +337,7 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     const srnn_config_t& c = *cfg;
     if (c.hidden < 1 || c.hidden > 65536 || c.input < 1 || c.batch < 1 || c.max_steps < 0) return SRNN_ERR_INVALID_VALUE;
     if (!(c.density >= 0.0f && c.density <= 1.0f)) return SRNN_ERR_INVALID_VALUE;
-    if (c.cell != SRNN_CELL_RNN && c.cell != SRNN_CELL_LSTM) return SRNN_ERR_INVALID_VALUE;
+    if (c.cell != SRNN_CELL_RNN && c.cell != SRNN_CELL_LSTM && c.cell != SRNN_CELL_GRU) return SRNN_ERR_INVALID_VALUE;
     if (c.act < SRNN_ACT_RELU || c.act > SRNN_ACT_IDENTITY) return SRNN_ERR_INVALID_VALUE;
     if (c.prec != SRNN_PREC_FP32 && c.prec != SRNN_PREC_FP16W_FP32ACC) return SRNN_ERR_INVALID_VALUE;
     if (c.lanes_per_row != 0 &&
@@ -349,7 +351,7 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     srnn_plan* p = new (std::nothrow) srnn_plan();
     if (!p) return SRNN_ERR_INVALID_VALUE;
     p->cfg = c;
-    p->G = c.cell == SRNN_CELL_LSTM ? 4 : 1;
+    p->G = c.cell == SRNN_CELL_LSTM ? 4 : c.cell == SRNN_CELL_GRU ? 3 : 1;
     p->host_only = (c.flags & SRNN_FLAG_HOST_ONLY) != 0;
     if (const char* t = std::getenv("SRNN_TIMEOUT_MS")) p->timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
     if (!p->host_only) {
@@ -730,6 +732,12 @@ search_again:
             else
                 e = cudaMemset(p->d_bias, 0, static_cast<size_t>(R) * 4);
         }
+        cudaFree(p->d_bhn);
+        p->d_bhn = nullptr;
+        if (e == cudaSuccess && G == 3 && bias) {  // GRU: bias[3H .. 4H) = b_hn
+            e = cudaMalloc(&p->d_bhn, static_cast<size_t>(H) * 4);
+            if (e == cudaSuccess) e = cudaMemcpy(p->d_bhn, bias + R, static_cast<size_t>(H) * 4, cudaMemcpyHostToDevice);
+        }
         if (e != cudaSuccess) return SRNN_ERR_CUDA;
         // Compiled register count and co-residency check for the instance.
         RecParams rp{};
@@ -847,6 +855,7 @@ static srnn_status_t recurrence_impl(srnn_plan_t p, int32_t T, int32_t B, const 
     rp.bprime = bprime;
     rp.h0 = h0;
     rp.c0 = p->G == 4 ? c0 : nullptr;
+    rp.bias_hn = p->G == 3 ? p->d_bhn : nullptr;
     rp.y = y;
     rp.hT = hT;
     rp.cT = p->G == 4 ? cT : nullptr;

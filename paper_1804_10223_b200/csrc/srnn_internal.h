@@ -35,6 +35,7 @@ struct RecParams {
     const float* bprime;  // [T][B][G*H]
     const float* h0;      // [B][H] or null
     const float* c0;      // [B][H] or null
+    const float* bias_hn; // GRU: [H] recurrent bias of the n gate (inside r * (.)), or null
     float* y;             // [T][B][H] or null
     float* hT;            // [B][H] or null
     float* cT;            // [B][H] or null

@@ -628,8 +628,8 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     const size_t hs_bytes = DENSE ? static_cast<size_t>(p.hs_rows) * 16 : static_cast<size_t>(H) * F::E;
     float* zs = reinterpret_cast<float*>(smem + ((hs_bytes + 15) & ~static_cast<size_t>(15)));
     float* bpsb = zs + G * umax_bt;                          // b' double buffer: [2][item][G]
-    float* cs = bpsb + 2 * G * umax_bt;                      // LSTM c: [n_tiles][item]
-    int* s_abort = reinterpret_cast<int*>(cs + (G == 4 ? p.n_tiles * umax_bt : 0));
+    float* cs = bpsb + 2 * G * umax_bt;                      // LSTM c / GRU fp32 h_{t-1}: [n_tiles][item]
+    int* s_abort = reinterpret_cast<int*>(cs + (G >= 3 ? p.n_tiles * umax_bt : 0));
     unsigned char* ws = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(s_abort + 1) + 15) & ~static_cast<uintptr_t>(15));  // smem weight tier
 
@@ -716,6 +716,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                 h = (p.h0 != nullptr && bg < p.B) ? p.h0[static_cast<size_t>(bg) * H + unit] : 0.0f;
                 if (G == 4)
                     cs[k * umax_bt + e] = (p.c0 != nullptr && bg < p.B) ? p.c0[static_cast<size_t>(bg) * H + unit] : 0.0f;
+                if (G == 3) cs[k * umax_bt + e] = h;  // GRU keeps its own fp32 h_{t-1} (the exchange carries fp16 in fp16 mode)
             }
             publish(0, k, e, ok, h);
         }
@@ -874,6 +875,17 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                     const int unit = u0 + e / BT, bg = k * BT + e % BT;
                     if (G == 1) {
                         h = activation<F16>(p.act, zs[e] + bps[e]);
+                    } else if (G == 3) {
+                        // GRU (R15): r, z from the product; the reset gate scales the
+                        // n-gate product + b_hn; the previous h of this item stays in fp32 in cs
+                        const int ub = U * BT;
+                        const float r = sigmoid_g<F16>(zs[0 * ub + e] + bps[e * G + 0]);
+                        const float u = sigmoid_g<F16>(zs[1 * ub + e] + bps[e * G + 1 % G]);
+                        const float bhn = p.bias_hn != nullptr ? p.bias_hn[unit] : 0.0f;
+                        const float n = tanh_g<F16>(fmaf(r, zs[2 * ub + e] + bhn, bps[e * G + 2 % G]));
+                        float* hp = &cs[k * umax_bt + e];
+                        h = fmaf(u, *hp - n, n);  // (1 - u) n + u h_prev
+                        *hp = h;
                     } else {
                         const int ub = U * BT;
                         const float zi = zs[0 * ub + e] + bps[e * G + 0];
@@ -952,12 +964,17 @@ int launch_np(int bt, int g, const RecParams& p, int num_ctas, size_t smem, void
     SRNN_CASE(1, 4)
     SRNN_CASE(2, 4)
     SRNN_CASE(4, 4)
+    SRNN_CASE(1, 3)
+    SRNN_CASE(2, 3)
+    SRNN_CASE(4, 3)
     if constexpr (F16) {
         SRNN_CASE(8, 1)
         SRNN_CASE(8, 4)
+        SRNN_CASE(8, 3)
         if constexpr (NP <= kMaxNP16) {
             SRNN_CASE(16, 1)
             SRNN_CASE(16, 4)
+            SRNN_CASE(16, 3)
         }
     }
 #undef SRNN_CASE

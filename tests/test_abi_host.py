@@ -201,3 +201,23 @@ def test_dense_tc_plan_host_only():
     with pytest.raises(SrnnError) as e:
         m.load_weights(prob["rowptr"], prob["col"], prob["val"], prob["wx"], prob["bias"])
     assert e.value.code == -2
+
+
+def test_gru_plan_host_only_and_dense_unsupported():
+    """GRU (3 gate rows per unit) packs like the other cells; the dense comparator has no GRU."""
+    from paper_1804_10223_b200 import FLAG_DENSE_TC
+    prob = inputs.make_problem(96, 16, 4, 3, 0.2, cell="gru")
+    m = SparseRNN(96, 16, 4, 3, 0.2, cell="gru", prec="fp16", flags=FLAG_HOST_ONLY)
+    m.load_weights(prob["rowptr"], prob["col"], prob["val"], prob["wx"], prob["bias"])
+    col, val, row = m.export_layout()
+    dense = np.zeros((3 * 96, 96))
+    np.add.at(dense, (row[row >= 0], col[row >= 0]), val[row >= 0].astype(np.float64))
+    ref = np.zeros((3 * 96, 96))
+    for r in range(3 * 96):
+        for i in range(prob["rowptr"][r], prob["rowptr"][r + 1]):
+            ref[r, prob["col"][i]] = np.float16(prob["val"][i])
+    assert np.array_equal(dense, ref)
+    m.close()
+    with pytest.raises(SrnnError) as e:
+        SparseRNN(96, 16, 4, 3, 0.2, cell="gru", prec="fp16", flags=FLAG_HOST_ONLY | FLAG_DENSE_TC)
+    assert e.value.code == -7

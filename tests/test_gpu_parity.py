@@ -490,3 +490,24 @@ def test_bidirectional_layer(cuda_device, concurrent):
     err = np.abs(y.cpu().numpy().astype(np.float64) - ref).max()
     assert err <= TOL["fp16"], err
     assert np.abs(hb.cpu().numpy() - ob["hT"]).max() <= TOL["fp16"]
+
+
+# ---- GRU cell extension (R15) ----
+
+@pytest.mark.parametrize("prec", ["fp32", "fp16"])
+@pytest.mark.parametrize("H,B,T,d,pattern", [
+    (128, 4, 10, 0.125, "row_balanced"),
+    (257, 1, 12, 0.12, "unstructured"),
+    (96, 5, 7, 0.3, "unstructured"),
+    (200, 8, 6, 0.1, "row_balanced"),
+    (300, 16, 5, 0.1, "unstructured"),
+])
+def test_gru_parity_small(cuda_device, prec, H, B, T, d, pattern):
+    prob = inputs.make_problem(H, H, B, T, d, cell="gru", pattern=pattern, h0="random", seed_offset=H + 7)
+    check(prob, prec)
+
+
+def test_gru_C4_shape_full(cuda_device):
+    """GRU at the LSTM case study's shape (H = 1024, B = 4, T = 100, 12.5% row-balanced), fp16."""
+    prob = inputs.make_problem(1024, 1024, 4, 100, 0.125, cell="gru", pattern="row_balanced")
+    check(prob, "fp16")
