@@ -257,6 +257,7 @@ def main():
     y = torch.empty(T, B, H, device=dev)
     hT = torch.empty(B, H, device=dev)
     yall = torch.empty(world, T, B, H, device=dev) if world > 1 else None
+    hall = torch.empty(world, B, H, device=dev) if world > 1 else None
     flush = torch.empty(256 * 1024 * 1024 // 4, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream()
 
@@ -273,7 +274,7 @@ def main():
             if args.gather == "y":
                 dist.all_gather_into_tensor(yall, y)
             else:
-                dist.all_gather_into_tensor(yall[:, 0, :B], hT)
+                dist.all_gather_into_tensor(hall, hT)
         if ev:
             ev[3].record(stream)
 
