@@ -21,6 +21,7 @@ WANT = [
     "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct",
     "smsp__average_warp_latency_issue_stalled_long_scoreboard",
     "local_load", "lsu_mem_local",
+    "l1tex__m_xbar2l1tex_read_bytes.sum", "lts__t_requests.sum",
 ]
 
 
