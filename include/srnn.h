@@ -70,8 +70,10 @@ typedef enum { SRNN_CELL_RNN = 0, SRNN_CELL_LSTM = 1, SRNN_CELL_GRU = 2 } srnn_c
 typedef enum { SRNN_ACT_RELU = 0, SRNN_ACT_TANH = 1, SRNN_ACT_IDENTITY = 2 } srnn_act_t;
 
 /* Precision mode.
- *   FP32:              fp32 weights and activations, fp32 input GEMM (no TF32),
- *                      accurate transcendentals.  Tolerance vs oracle 1e-5.
+ *   FP32:              fp32 weights and activations, exact fp32 SIMT input
+ *                      GEMM (no TF32; SRNN_FLAG_FP32_TC_GEMM trades accuracy for
+ *                      a 3xTF32 tensor-core GEMM), accurate transcendentals.
+ *                      Tolerance vs oracle 1e-5.
  *   FP16W_FP32ACC:     W_h stored fp16 (RNE, "lower-precision data
  *                      type such as fp16 for the weights"), W_x and x rounded
  *                      to fp16 for a tensor-core input GEMM, all accumulation
@@ -82,7 +84,8 @@ typedef enum { SRNN_PREC_FP32 = 0, SRNN_PREC_FP16W_FP32ACC = 1 } srnn_prec_t;
 #define SRNN_FLAG_GRID_SYNC      (1u << 0) /* grid.sync() per step instead of tags   */
 #define SRNN_FLAG_NAIVE_LAYOUT   (1u << 1) /* CSR-order lane-strided pairs, no bank-aware order     */
 #define SRNN_FLAG_HOST_ONLY      (1u << 2) /* plan + pack on the host only; no device calls at all */
-#define SRNN_FLAG_SIMT_GEMM      (1u << 3) /* fp16 mode: use the fp32 SIMT input GEMM (ablation)    */
+#define SRNN_FLAG_SIMT_GEMM      (1u << 3) /* fp16 mode: use the exact fp32 SIMT input GEMM instead of
+                                              the fp16 tcgen05 GEMM (ablation)                   */
 #define SRNN_FLAG_DEBUG_JITTER   (1u << 4) /* inject per-CTA __nanosleep delays (sync-protocol test)*/
 #define SRNN_FLAG_FP32_STAGING   (1u << 5) /* fp16 mode: stage/exchange h in fp32 and keep fp32
                                               register pairs (ablation; default fp16 staging and
@@ -96,6 +99,13 @@ typedef enum { SRNN_PREC_FP32 = 0, SRNN_PREC_FP16W_FP32ACC = 1 } srnn_prec_t;
                                               exchange message); the device watchdog must end the
                                               kernel and srnn_plan_status report SRNN_ERR_TIMEOUT
                                               (timeout: env SRNN_TIMEOUT_MS, default 2000)       */
+#define SRNN_FLAG_FP32_TC_GEMM   (1u << 10) /* fp32 mode, opt-in: input projection as a 3xTF32
+                                              tcgen05 GEMM (x, W_x split into tf32 hi + lo, D +=
+                                              hi*hi + hi*lo + lo*hi): 6.5x faster than the SIMT
+                                              GEMM at C2, but the tensor cores' fp32 accumulation
+                                              leaves ~1.5e-8 * K relative error in b' (4.9e-5 at
+                                              K = 2304 vs 6e-6 for SIMT), above the 1e-5 parity
+                                              bound of the fp32 mode -- not the default        */
 #define SRNN_FLAG_DENSE_TC       (1u << 8) /* comparator: the DENSE persistent
                                               RNN of PAPER.md:51-71 (Sec. 3.2, Diamos et al.)
                                               re-done for sm_100a tensor cores.  U_r is densified

@@ -53,6 +53,14 @@ struct srnn_plan {
     void* d_x16 = nullptr;  // [T_max*B_max][k_pad]
     alignas(64) CUtensorMap map_x16;
     alignas(64) CUtensorMap map_wx16;
+    // fp32 mode: 3xTF32 tensor-core GEMM on tf32 hi/lo splits of x and W_x, K padded to 4
+    bool tf32x3 = false;
+    int k_pad4 = 0;
+    float *d_wx_hi = nullptr, *d_wx_lo = nullptr, *d_x_hi = nullptr, *d_x_lo = nullptr;
+    alignas(64) CUtensorMap map_xhi;
+    alignas(64) CUtensorMap map_xlo;
+    alignas(64) CUtensorMap map_wxhi;
+    alignas(64) CUtensorMap map_wxlo;
     float* d_bias = nullptr;
     float* d_bhn = nullptr;         // GRU: n-gate recurrent bias [H]
     float* d_bprime = nullptr;      // [T_max][B_max][G*H]
@@ -117,6 +125,10 @@ void free_device(srnn_plan* p) {
     cudaFree(p->d_wx);
     cudaFree(p->d_wx16);
     cudaFree(p->d_x16);
+    cudaFree(p->d_wx_hi);
+    cudaFree(p->d_wx_lo);
+    cudaFree(p->d_x_hi);
+    cudaFree(p->d_x_lo);
     cudaFree(p->d_bias);
     cudaFree(p->d_bhn);
     cudaFree(p->d_bprime);
@@ -159,6 +171,25 @@ bool encode_fp16_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint6
     cuuint32_t box[2] = {64, box_rows};  // 64 fp16 = one 128-byte swizzle row (srnn_gemm_tc.cu)
     cuuint32_t estr[2] = {1, 1};
     return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// fp32 (tf32-split) operand map: 32 fp32 = one 128-byte swizzle row.
+bool encode_f32_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k_pad, uint32_t box_rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    cuuint64_t dims[2] = {k_pad, rows};
+    cuuint64_t strides[1] = {k_pad * 4};
+    cuuint32_t box[2] = {32, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -707,6 +738,31 @@ search_again:
         cudaFree(p->d_wx16);
         cudaFree(p->d_x16);
         p->d_wx16 = p->d_x16 = nullptr;
+        cudaFree(p->d_wx_hi);
+        cudaFree(p->d_wx_lo);
+        cudaFree(p->d_x_hi);
+        cudaFree(p->d_x_lo);
+        p->d_wx_hi = p->d_wx_lo = p->d_x_hi = p->d_x_lo = nullptr;
+        // fp32 mode, opt-in (SRNN_FLAG_FP32_TC_GEMM): the 3xTF32 tensor-core projection
+        p->tf32x3 = !fp16 && (p->cfg.flags & SRNN_FLAG_FP32_TC_GEMM) != 0;
+        if (e == cudaSuccess && p->tf32x3) {
+            const int I = p->cfg.input;
+            p->k_pad4 = (I + 3) & ~3;
+            const size_t xrows = static_cast<size_t>(std::max(1, p->cfg.max_steps)) * p->cfg.batch;
+            const size_t wn = static_cast<size_t>(R) * p->k_pad4, xn = xrows * p->k_pad4;
+            e = cudaMalloc(&p->d_wx_hi, wn * 4);
+            if (e == cudaSuccess) e = cudaMalloc(&p->d_wx_lo, wn * 4);
+            if (e == cudaSuccess) e = cudaMalloc(&p->d_x_hi, xn * 4);
+            if (e == cudaSuccess) e = cudaMalloc(&p->d_x_lo, xn * 4);
+            if (e == cudaSuccess &&
+                launch_split_tf32(p->d_wx, p->d_wx_hi, p->d_wx_lo, R, I, p->k_pad4, nullptr) != 0)
+                e = cudaErrorUnknown;
+            if (e == cudaSuccess && (!encode_f32_kmajor(&p->map_wxhi, p->d_wx_hi, R, p->k_pad4, 64) ||
+                                     !encode_f32_kmajor(&p->map_wxlo, p->d_wx_lo, R, p->k_pad4, 64) ||
+                                     !encode_f32_kmajor(&p->map_xhi, p->d_x_hi, xrows, p->k_pad4, 128) ||
+                                     !encode_f32_kmajor(&p->map_xlo, p->d_x_lo, xrows, p->k_pad4, 128)))
+                return SRNN_ERR_CUDA;
+        }
         p->tc_gemm = fp16 && (p->cfg.flags & SRNN_FLAG_SIMT_GEMM) == 0;
         if (e == cudaSuccess && p->tc_gemm) {
             // W_x and x rounded to fp16 (RNE) for the tensor-core input GEMM (srnn_gemm_tc.cu)
@@ -770,6 +826,15 @@ static srnn_status_t project_rows(srnn_plan_t p, int64_t r0, int64_t M, const fl
         if (e == 0)
             e = launch_gemm_tc(&p->map_x16, &p->map_wx16, p->d_bias, bprime, static_cast<int>(M), N, p->k_pad, stream,
                                static_cast<int>(r0), 0, sms);
+        return e == 0 ? SRNN_OK : SRNN_ERR_CUDA;
+    }
+    if (p->tf32x3) {
+        float* xh = p->d_x_hi + static_cast<size_t>(r0) * p->k_pad4;
+        float* xl = p->d_x_lo + static_cast<size_t>(r0) * p->k_pad4;
+        int e = launch_split_tf32(x + r0 * I, xh, xl, M, I, p->k_pad4, stream);
+        if (e == 0)
+            e = launch_gemm_tf32x3(&p->map_xhi, &p->map_xlo, &p->map_wxhi, &p->map_wxlo, p->d_bias, bprime,
+                                   static_cast<int>(M), N, p->k_pad4, stream, static_cast<int>(r0), sms);
         return e == 0 ? SRNN_OK : SRNN_ERR_CUDA;
     }
     GemmParams gp;

@@ -67,17 +67,20 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
            (2ull << 61) /* SWIZZLE_128B */;
 }
 // Instruction descriptor, kind::f16: D f32, A/B f16, both K-major, M = 128, N = BN.
-template <int BN>
+// X3 (fp32 mode, "3xTF32"): kind::tf32, A/B format TF32 (2) -- see gemm_tc_f16_kernel.
+template <int BN, bool X3 = false>
 __host__ __device__ constexpr uint32_t idesc_f16() {
-    return (1u << 4) | (0u << 7) | (0u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+    return (1u << 4) | ((X3 ? 2u : 0u) << 7) | ((X3 ? 2u : 0u) << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
            (static_cast<uint32_t>(TC_BM >> 4) << 24);
 }
 
-template <int BN>
+// One K-block is one 128-byte swizzle row per operand row: 64 fp16, or 32 fp32
+// (tf32) elements.  X3 stages four operand tiles per K-block: A_hi, A_lo, B_hi, B_lo.
+template <int BN, bool X3 = false>
 struct TcCfg {
     static constexpr uint32_t B_BYTES = BN * TC_BK * 2;  // BN/64 boxes of 64 rows, 8-row groups 1 KB apart
-    static constexpr int STAGES = static_cast<int>((200u * 1024u) / (TC_TILE_BYTES + B_BYTES));  // ~200 KB in flight
-    static constexpr uint32_t STAGE_BYTES = TC_TILE_BYTES + B_BYTES;
+    static constexpr uint32_t STAGE_BYTES = (X3 ? 2 : 1) * (TC_TILE_BYTES + B_BYTES);
+    static constexpr int STAGES = static_cast<int>((200u * 1024u) / STAGE_BYTES);  // ~200 KB in flight
     static constexpr uint32_t TMEM_COLS = BN == 128 ? 256 : 512;  // two accumulators (power-of-2 allocation)
     static constexpr size_t SMEM = STAGES * STAGE_BYTES + 1024 /* align */ + 256 /* barriers */;
 };
@@ -85,26 +88,36 @@ struct TcCfg {
 // Persistent over output tiles: CTA b takes tiles b, b + gridDim.x, ... (n-fastest).
 // The producer and the MMA issuer run ahead into the next tile while the
 // epilogue warps drain the other TMEM accumulator.
-template <int BN>
+//
+// X3 = the fp32 mode's exact-enough projection on tensor cores ("3xTF32", the
+// split named in SURVEY.md Sec. 7 hard part 7): x and W_x are split on the host
+// side of the MMA into tf32 hi + lo parts (a = a_hi + a_lo, |a_lo| <= 2^-11 |a|),
+// and D += A_hi B_hi + A_hi B_lo + A_lo B_hi, dropping only A_lo B_lo (~2^-22 of
+// each product) -- fp32-level accuracy for the 1e-5 parity bound, with K in
+// steps of 8 tf32 elements (32 bytes, the same descriptor advance as fp16 K=16).
+template <int BN, bool X3 = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_f16_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                       const float* __restrict__ bias, float* __restrict__ C, int M, int N, int K, int m_off) {
-    using Cfg = TcCfg<BN>;
+                       const float* __restrict__ bias, float* __restrict__ C, int M, int N, int K, int m_off,
+                       const __grid_constant__ CUtensorMap map_a_lo, const __grid_constant__ CUtensorMap map_b_lo) {
+    using Cfg = TcCfg<BN, X3>;
     constexpr int STAGES = Cfg::STAGES;
-    constexpr uint32_t kIdesc = idesc_f16<BN>();
+    constexpr uint32_t kIdesc = idesc_f16<BN, X3>();
+    constexpr int KB_ELEMS = X3 ? TC_BK / 2 : TC_BK;  // elements of K per 128-byte row
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment for the 128B-swizzled operand tiles
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // per stage: A [, A_lo] then B [, B_lo]
     unsigned char* sA = smem;
-    unsigned char* sB = smem + STAGES * TC_TILE_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
+    unsigned char* sB = smem + STAGES * TC_TILE_BYTES * (X3 ? 2 : 1);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES * (X3 ? 2 : 1));
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;  // [2] accumulator ready for the epilogue
     uint64_t* tempty = tfull + 2;      // [2] accumulator drained by the 4 epilogue warps
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nk = (K + TC_BK - 1) / TC_BK;
+    const int nk = (K + KB_ELEMS - 1) / KB_ELEMS;
     const int tiles_n = (N + BN - 1) / BN;
     const int n_tiles = tiles_n * ((M + TC_BM - 1) / TC_BM);
 
@@ -120,6 +133,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+        if (X3) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a_lo) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b_lo) : "memory");
+        }
     }
     if (warp == 1) {  // TMEM allocation (whole warp)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
@@ -141,11 +158,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const int s = it % STAGES;
                 if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
                 mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
-                tma_load_2d(sA + s * TC_TILE_BYTES, &map_a, &full[s], kb * TC_BK, m_off + m0);
+                const int a_stride = TC_TILE_BYTES * (X3 ? 2 : 1), b_stride = Cfg::B_BYTES * (X3 ? 2 : 1);
+                tma_load_2d(sA + s * a_stride, &map_a, &full[s], kb * KB_ELEMS, m_off + m0);
+                if (X3) tma_load_2d(sA + s * a_stride + TC_TILE_BYTES, &map_a_lo, &full[s], kb * KB_ELEMS, m_off + m0);
 #pragma unroll
-                for (int j = 0; j < BN / 64; ++j)  // rows past N are zero-filled by TMA
-                    tma_load_2d(sB + s * Cfg::B_BYTES + j * (TC_TILE_BYTES / 2), &map_b, &full[s], kb * TC_BK,
+                for (int j = 0; j < BN / 64; ++j) {  // rows past N are zero-filled by TMA
+                    tma_load_2d(sB + s * b_stride + j * (TC_TILE_BYTES / 2), &map_b, &full[s], kb * KB_ELEMS,
                                 n0 + 64 * j);
+                    if (X3)
+                        tma_load_2d(sB + s * b_stride + Cfg::B_BYTES + j * (TC_TILE_BYTES / 2), &map_b_lo, &full[s],
+                                    kb * KB_ELEMS, n0 + 64 * j);
+                }
             }
         }
     } else if (warp == 1 && lane == 0) {
@@ -160,17 +183,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const int s = it % STAGES;
                 mbar_wait(&full[s], (it / STAGES) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint64_t da = smem_desc_sw128(sA + s * TC_TILE_BYTES);
-                const uint64_t db = smem_desc_sw128(sB + s * Cfg::B_BYTES);
+                const uint64_t da = smem_desc_sw128(sA + s * TC_TILE_BYTES * (X3 ? 2 : 1));
+                const uint64_t db = smem_desc_sw128(sB + s * Cfg::B_BYTES * (X3 ? 2 : 1));
 #pragma unroll
                 for (int k = 0; k < TC_BK / 16; ++k) {
                     const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
-                    // advance 16 fp16 (32 bytes) along K inside the swizzled row: +2 in the >>4 address field
-                    asm volatile(
-                        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-                        "l"(da + 2ull * k), "l"(db + 2ull * k), "r"(kIdesc), "r"(accum)
-                        : "memory");
+                    // advance 16 fp16 / 8 tf32 (32 bytes) along K inside the swizzled row: +2 in the >>4 address field
+                    if (X3) {
+                        const uint64_t dal = da + (TC_TILE_BYTES >> 4), dbl = db + (Cfg::B_BYTES >> 4);
+                        asm volatile(
+                            "{\n.reg .pred p, q;\nsetp.ne.b32 p, %6, 0;\nsetp.eq.b32 q, %6, %6;\n"
+                            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %5, p;\n"
+                            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %3, %2, %5, q;\n"
+                            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %5, q;\n}\n" ::"r"(d_tmem),
+                            "l"(da + 2ull * k), "l"(db + 2ull * k), "l"(dal + 2ull * k), "l"(dbl + 2ull * k),
+                            "r"(kIdesc), "r"(accum)
+                            : "memory");
+                    } else {
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+                            "l"(da + 2ull * k), "l"(db + 2ull * k), "r"(kIdesc), "r"(accum)
+                            : "memory");
+                    }
                 }
                 // free the smem stage once these MMAs have read it
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -275,6 +310,23 @@ int launch_f32_to_f16_padded(const float* in, void* out, int64_t rows, int cols,
     return static_cast<int>(cudaGetLastError());
 }
 
+// x -> (tf32(x), tf32(x - tf32(x))) stored as fp32 bit patterns, [rows][cols] -> [rows][ld_out]
+// (zero padding in columns [cols, ld_out)).  cvt.rna = round to nearest, ties away (tf32).
+__global__ void split_tf32_kernel(const float* __restrict__ in, float* __restrict__ hi, float* __restrict__ lo,
+                                  int64_t rows, int cols, int ld_out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= rows * ld_out) return;
+    const int64_t r = i / ld_out;
+    const int c = static_cast<int>(i - r * ld_out);
+    const float v = c < cols ? in[r * cols + c] : 0.0f;
+    uint32_t h, l;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
+    const float rem = v - __uint_as_float(h);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(rem));
+    hi[i] = __uint_as_float(h);
+    lo[i] = __uint_as_float(l);
+}
+
 // Force module loading of the projection kernels (CUDA lazy loading would
 // otherwise load them at first launch, which can stall behind a running
 // persistent kernel that is waiting for their output).
@@ -283,6 +335,8 @@ int preload_projection_kernels() {
     cudaError_t e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel<128>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel<192>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel<256>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel<128, true>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, split_tf32_kernel);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, f32_to_f16_kernel);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, f32_to_f16_padded_kernel);
     return static_cast<int>(e);
@@ -296,22 +350,41 @@ int launch_f32_to_f16(const float* in, void* out, int64_t n, void* stream) {
     return static_cast<int>(cudaGetLastError());
 }
 
-template <int BN>
+template <int BN, bool X3 = false>
 static int launch_gemm_tc_bn(const void* map_a, const void* map_b, const float* bias, float* C, int M, int N, int K,
-                             cudaStream_t stream, int m_off, int sms) {
+                             cudaStream_t stream, int m_off, int sms, const void* map_a_lo = nullptr,
+                             const void* map_b_lo = nullptr) {
     static bool attr_set = false;
-    const size_t smem = TcCfg<BN>::SMEM;
+    const size_t smem = TcCfg<BN, X3>::SMEM;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_tc_f16_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(gemm_tc_f16_kernel<BN, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return static_cast<int>(e);
         attr_set = true;
     }
     const int64_t tiles = static_cast<int64_t>((N + BN - 1) / BN) * ((M + TC_BM - 1) / TC_BM);
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
-    gemm_tc_f16_kernel<BN><<<grid, TC_THREADS, smem, stream>>>(*static_cast<const CUtensorMap*>(map_a),
-                                                               *static_cast<const CUtensorMap*>(map_b), bias, C, M, N,
-                                                               K, m_off);
+    const CUtensorMap& ma = *static_cast<const CUtensorMap*>(map_a);
+    const CUtensorMap& mb = *static_cast<const CUtensorMap*>(map_b);
+    gemm_tc_f16_kernel<BN, X3><<<grid, TC_THREADS, smem, stream>>>(
+        ma, mb, bias, C, M, N, K, m_off, X3 ? *static_cast<const CUtensorMap*>(map_a_lo) : ma,
+        X3 ? *static_cast<const CUtensorMap*>(map_b_lo) : mb);
+    return static_cast<int>(cudaGetLastError());
+}
+
+// fp32 mode: 3xTF32 tcgen05 GEMM on pre-split operands (tf32 hi / lo as fp32 arrays).
+int launch_gemm_tf32x3(const void* map_a_hi, const void* map_a_lo, const void* map_b_hi, const void* map_b_lo,
+                       const float* bias, float* C, int M, int N, int K, void* stream, int m_off, int sms) {
+    if (M <= 0 || N <= 0) return 0;
+    return launch_gemm_tc_bn<128, true>(map_a_hi, map_b_hi, bias, C, M, N, K, static_cast<cudaStream_t>(stream),
+                                        m_off, std::max(1, sms), map_a_lo, map_b_lo);
+}
+
+int launch_split_tf32(const float* in, float* hi, float* lo, int64_t rows, int cols, int ld_out, void* stream) {
+    const int64_t n = rows * ld_out;
+    if (n <= 0) return 0;
+    split_tf32_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        in, hi, lo, rows, cols, ld_out);
     return static_cast<int>(cudaGetLastError());
 }
 

@@ -84,6 +84,10 @@ int launch_gemm_tc(const void* map_a, const void* map_b, const float* bias, floa
                    void* stream, int m_off = 0, int bn = 0, int sms = 148);
 // rows [m_off, m_off + M) of A and C; bn = tile width (0: pick from the grid size vs `sms`, the SMs it may use)
 int launch_f32_to_f16(const float* in, void* out, int64_t n, void* stream);
+// fp32 mode: 3xTF32 tcgen05 GEMM on tf32 hi/lo splits (maps: fp32 K-major, 32-element boxes)
+int launch_gemm_tf32x3(const void* map_a_hi, const void* map_a_lo, const void* map_b_hi, const void* map_b_lo,
+                       const float* bias, float* C, int M, int N, int K, void* stream, int m_off, int sms);
+int launch_split_tf32(const float* in, float* hi, float* lo, int64_t rows, int cols, int ld_out, void* stream);
 int preload_projection_kernels();
 int preload_gemm_f32();
 int launch_f32_to_f16_padded(const float* in, void* out, int64_t rows, int cols, int ld_out, void* stream);

@@ -511,3 +511,26 @@ def test_gru_C4_shape_full(cuda_device):
     """GRU at the LSTM case study's shape (H = 1024, B = 4, T = 100, 12.5% row-balanced), fp16."""
     prob = inputs.make_problem(1024, 1024, 4, 100, 0.125, cell="gru", pattern="row_balanced")
     check(prob, "fp16")
+
+
+@pytest.mark.parametrize("H,I,B,T,cell", [(384, 200, 3, 7, "rnn"), (130, 201, 2, 9, "lstm"), (2304, 2304, 4, 256, "rnn"),
+                                        (300, 77, 5, 3, "gru")])
+def test_input_projection_fp32_3xtf32_opt_in(cuda_device, H, I, B, T, cell):
+    """fp32 mode, SRNN_FLAG_FP32_TC_GEMM: the 3xTF32 tcgen05 projection (tf32 hi/lo split, ragged K
+    padded to 4) against the fp64 oracle, within its documented ~1.5e-8 * K relative error (the
+    tensor cores' fp32 accumulation; the default exact SIMT GEMM is checked at fp32 level)."""
+    import torch
+    from paper_1804_10223_b200._lib import FLAG_FP32_TC_GEMM
+    prob = inputs.make_problem(H, I, B, T, 0.05, cell=cell)
+    x = torch.from_numpy(prob["x"]).cuda()
+    ref = oracle.input_projection(prob["x"], prob["wx"], prob["bias"][:prob["G"] * H])
+    got = {}
+    for name, flags in (("tc", FLAG_FP32_TC_GEMM), ("simt", 0)):
+        m = from_problem(prob, prec="fp32", flags=flags)
+        got[name] = m.input_projection(x).cpu().numpy().astype(np.float64)
+        torch.cuda.synchronize()
+        m.close()
+    scale = max(1.0, float(np.abs(ref).max()))
+    print("3xtf32", H, I, "err tc", np.abs(got["tc"] - ref).max(), "err simt", np.abs(got["simt"] - ref).max())
+    assert np.abs(got["tc"] - ref).max() <= 1.5e-8 * I * scale + 1e-6
+    assert np.abs(got["simt"] - ref).max() <= 1e-5
