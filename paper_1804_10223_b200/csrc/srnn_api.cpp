@@ -385,6 +385,9 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     p->G = c.cell == SRNN_CELL_LSTM ? 4 : c.cell == SRNN_CELL_GRU ? 3 : 1;
     p->host_only = (c.flags & SRNN_FLAG_HOST_ONLY) != 0;
     if (const char* t = std::getenv("SRNN_TIMEOUT_MS")) p->timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
+    // test hook: start the timestep tags near the u32 wrap so the wrap path (buffer clear +
+    // epoch restart) is exercised in a few calls
+    if (const char* t = std::getenv("SRNN_DEBUG_EPOCH0")) p->epoch = static_cast<uint32_t>(std::strtoull(t, nullptr, 10));
     if (!p->host_only) {
         DeviceGuard g(c.device);
         if (!g.ok) {

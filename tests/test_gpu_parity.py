@@ -534,3 +534,23 @@ def test_input_projection_fp32_3xtf32_opt_in(cuda_device, H, I, B, T, cell):
     print("3xtf32", H, I, "err tc", np.abs(got["tc"] - ref).max(), "err simt", np.abs(got["simt"] - ref).max())
     assert np.abs(got["tc"] - ref).max() <= 1.5e-8 * I * scale + 1e-6
     assert np.abs(got["simt"] - ref).max() <= 1e-5
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp16"])
+def test_tag_epoch_wrap(cuda_device, monkeypatch, prec):
+    """Timestep tags are u32 epoch + s: a plan whose epoch starts just below 2^32 must clear its
+    exchange buffers and restart the epoch instead of wrapping into stale tags -- every call,
+    before and after the restart, matches the oracle."""
+    import torch
+    monkeypatch.setenv("SRNN_DEBUG_EPOCH0", str(2 ** 32 - 30))
+    prob = inputs.make_problem(300, 300, 4, 12, 0.1, act="tanh", h0="random")
+    m = from_problem(prob, prec=prec)
+    o = oracle.forward(prob)
+    x = torch.from_numpy(prob["x"]).cuda()
+    h0 = torch.from_numpy(prob["h0"]).cuda()
+    for _ in range(4):  # 13 tags per call: the third call wraps
+        y, _ = m.forward(x, h0)
+        torch.cuda.synchronize()
+        m.status()
+        assert np.abs(y.cpu().numpy() - o["y"]).max() <= TOL[prec]
+    m.close()
