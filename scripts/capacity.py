@@ -34,7 +34,24 @@ def main():
     ap.add_argument("--B", type=int, default=4)
     ap.add_argument("--prec", default="fp16")
     ap.add_argument("--device", action="store_true")
+    ap.add_argument("--curve", action="store_true",
+                    help="Fig. 2b analogue (PAPER.md:151): largest on-chip H per density, one JSON line each")
     a = ap.parse_args()
+    if a.curve:
+        for d in (0.01, 0.02, 0.05, 0.10, 0.20, 0.30, 0.50, 1.0):
+            lo, hi = 256, 65536
+            if not fits(lo, d, a.B, a.prec, a.device):
+                print(json.dumps({"density": d, "H_max": None}), flush=True)
+                continue
+            while hi - lo > 64:
+                mid = (lo + hi) // 2
+                if fits(mid, d, a.B, a.prec, a.device):
+                    lo = mid
+                else:
+                    hi = mid
+            print(json.dumps({"density": d, "B": a.B, "prec": a.prec, "device_checked": a.device, "H_max": lo,
+                              "nnz_at_max": int(round(d * lo * lo))}), flush=True)
+        return
     lo, hi = 256, 8192
     while hi - lo > 16:
         mid = (lo + hi) // 2

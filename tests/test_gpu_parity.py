@@ -267,9 +267,10 @@ def test_smem_weight_tier_forced(cuda_device, monkeypatch, prec, cell, B):
 @pytest.mark.parametrize("H,d", [(13445, 0.02), (19200, 0.01), (27648, 0.005)])
 def test_capacity_large_hidden_on_chip(cuda_device, H, d):
     """a10 / SURVEY d-iv: 5x the largest dense layer that fits still runs fully on chip --
-    every output checked.  Dense references: this library's sparse format at density 1
-    (H = 2689, scripts/capacity.py; 5x = 13445) and the dense tensor-core persistent
-    comparator SRNN_FLAG_DENSE_TC (H = 3829 at B = 4, registers + shared memory; 5x = 19145)."""
+    every output checked.  Dense references (B = 4, device-checked, profiles/capacity_curve_r01.md):
+    this library's format at density 1 (H = 3252; 5x = 16260) and the dense tensor-core
+    persistent comparator SRNN_FLAG_DENSE_TC (H = 3829; 5x = 19145): 19200 and 27648 exceed
+    both; 13445 @ 2% is an intermediate point."""
     prob = inputs.make_problem(H, 64, 1, 6, d, act="tanh", h0="random")
     g, o, err = check(prob, "fp16")
     print(H, d, g["info"])
