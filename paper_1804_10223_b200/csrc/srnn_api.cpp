@@ -556,7 +556,7 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
 search_again:
     std::vector<int> cands_c;
     if (p->cfg.num_ctas > 0) {
-        cands_c.push_back(p->cfg.num_ctas);
+        cands_c.push_back(std::min(p->cfg.num_ctas, H));  // every CTA owns >= 1 unit (its publish writes the pad word)
     } else {
         int reserve = 0;
         if (p->cfg.flags & SRNN_FLAG_RESERVE_SMS) {
