@@ -138,6 +138,15 @@ def test_cta_counts(cuda_device, C, H, prec):
     check(prob, prec, num_ctas=C)
 
 
+@pytest.mark.parametrize("cell", ["rnn", "lstm"])
+def test_forced_cta_count_above_hidden(cuda_device, cell):
+    """More CTAs forced than units (H = 101, odd word count at B = 1): clamped to H, no CTA
+    without units (whose publish would never write the exchange pad word)."""
+    prob = inputs.make_problem(101, 64, 1, 6, 0.1, cell=cell, act="tanh", h0="random")
+    g, _, _ = check(prob, "fp16", num_ctas=148)
+    assert g["info"]["num_ctas"] == 101
+
+
 def test_T0_T1_repeat_and_smaller_batch(cuda_device):
     import torch
     prob = inputs.make_problem(320, 320, 4, 6, 0.1, act="tanh", h0="random")
