@@ -351,7 +351,9 @@ def main():
             "warmup": max(3, args.warmup), "ms_per_step": t_step * 1000, "us_per_timestep": t_step * 1e6 / T,
             "us_per_timestep_recurrence": t_rec * 1e6 / T, "ms_input_gemm": t_gemm * 1000,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32 accumulate (fp16 W_h/W_x storage)" if prec == "fp16" else "f32",
+            "dtype": "f16" if prec == "fp16" else "f32",
+            "dtype_note": "fp16 multiplies (W_h, W_x, x and the staged h rounded RNE), fp32 accumulate; b', "
+                          "activations, LSTM c and y in fp32" if prec == "fp16" else "fp32 throughout, no TF32",
             "data": "synthetic (seeded PCG64: uniform unstructured pattern, U(-a,a) weights)",
             "config": {"workload": describe(cfg, prec, args.config), "H": H, "I": cfg["I"], "B_per_rank": B,
                        "global_batch": B * world, "T": T, "density": cfg["density"], "nnz": prob["nnz"],
