@@ -225,6 +225,28 @@ def load_traffic():
         return None, None
 
 
+def launch_list_kernel_us(substr):
+    """Median duration (µs) of a kernel in the committed ncu launch list (cold, serialised), if any."""
+    import csv
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "launches_r*.csv")))
+    if not files:
+        return None, None
+    vals, hdr = [], None
+    try:
+        for r in csv.reader(open(files[-1])):
+            if "Kernel Name" in r:
+                hdr = r
+                continue
+            if hdr and len(r) == len(hdr):
+                d = dict(zip(hdr, r))
+                if substr in d["Kernel Name"] and d.get("Metric Name") == "gpu__time_duration.sum":
+                    vals.append(float(d["Metric Value"]) / 1000.0)  # ns -> µs
+    except Exception:
+        return None, None
+    return (statistics.median(vals) if vals else None), os.path.relpath(files[-1], ROOT)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -385,7 +407,15 @@ def main():
                              "achieved_tflops": gemm_flops / t_gemm / 1e12,
                              "peak_tflops": 1663.3 if prec == "fp16" else None,
                              "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; fp16 has the same dense rate)",
-                             "frac": (gemm_flops / t_gemm / 1e12) / 1663.3 if prec == "fp16" else None}
+                             "frac": (gemm_flops / t_gemm / 1e12) / 1663.3 if prec == "fp16" else None,
+                             "note": "ms covers the whole srnn_input_projection call (x f32->f16 conversion + GEMM + "
+                                     "launch gaps)"}
+        if prec == "fp16":
+            k_us, k_src = launch_list_kernel_us("gemm_tc_f16_kernel")
+            if k_us:
+                out["input_gemm"].update({"gemm_kernel_only_us": k_us,
+                                          "gemm_kernel_only_frac": gemm_flops / (k_us * 1e-6) / 1e12 / 1663.3,
+                                          "gemm_kernel_only_source": k_src + " (ncu launch list, cold L2, serialised)"})
         # Latency roofline of the recurrent kernel: the measured exchange/sync floor (same
         # H, B, plan shape, density 0: no pairs, everything else identical) plus the
         # shared-memory time of the packer's predicted wavefronts (busiest CTA, per step).
