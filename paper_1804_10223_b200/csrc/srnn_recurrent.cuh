@@ -597,6 +597,17 @@ struct LoadK {
     static constexpr int value = F16 ? (NP <= 48 ? 8 : 4) : 4;
 };
 
+// fp16 tiles of 4 with up to 24 register slots: 5 poll slots per thread.  At H ~ 2304 on
+// 512 threads a thread owns 4-5 chunks, and the shorter unrolled loop (fewer live
+// registers and predicated slots than K = 8) measured 6-10% faster per step (C2 2.334 ->
+// 2.188 µs, 2304 @ 10% 2.252 -> 2.014, LSTM C4 2.071 -> 2.023); at H = 3584 (9 chunks per
+// thread) K = 5 and K = 8 both take two batches and tie.  A runtime choice between the
+// two inside one kernel spills (48 bytes) and loses everything.
+template <int NP, bool F16, int BT>
+struct LoadKTile {
+    static constexpr int value = (F16 && BT == 4 && NP <= 24) ? 5 : LoadK<NP, F16>::value;
+};
+
 __device__ __forceinline__ void cp_async_f32(float* dst_smem, const float* src) {
     const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst_smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
@@ -771,7 +782,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
             // ---- load: h_{s-1} tile k -> hs ----
             const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
                 p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
-            if (!load_tile<F16, BT, LoadK<NP, F16>::value, DENSE>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
+            if (!load_tile<F16, BT, LoadKTile<NP, F16, BT>::value, DENSE>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
                                                             !grid_sync, p.status, p.timeout_ns, p.poll_backoff_ns,
                                                             p.loader_threads, ps))
                 *s_abort = 1;
