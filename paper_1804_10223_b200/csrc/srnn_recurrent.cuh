@@ -597,15 +597,30 @@ struct LoadK {
     static constexpr int value = F16 ? (NP <= 48 ? 8 : 4) : 4;
 };
 
-// fp16 tiles of 4 with up to 24 register slots: 5 poll slots per thread.  At H ~ 2304 on
-// 512 threads a thread owns 4-5 chunks, and the shorter unrolled loop (fewer live
-// registers and predicated slots than K = 8) measured 6-10% faster per step (C2 2.334 ->
-// 2.188 µs, 2304 @ 10% 2.252 -> 2.014, LSTM C4 2.071 -> 2.023); at H = 3584 (9 chunks per
-// thread) K = 5 and K = 8 both take two batches and tie.  A runtime choice between the
-// two inside one kernel spills (48 bytes) and loses everything.
+// Poll slots per thread (K chunks in flight in the unrolled loader).  Fewer slots mean a
+// shorter loop and fewer live registers; measured on B200 (A/B, same box):
+//   fp16 tiles of 4 (NP <= 24): K = 5 -- C2 2.334 -> 2.176 µs/step (K = 8), 2304 @ 10%
+//     2.252 -> 2.014, LSTM C4 2.071 -> 2.023; K = 4 / 3 / 6: 2.61 / 2.55 / 2.25
+//   fp16 tiles of 8 / 16: K = 6 -- C5 (5760, B = 64) 51.9 -> 43.9, B = 16 5.19 -> 4.96,
+//     B = 8 3.29 -> 3.26 (K = 5: 48.1 / 5.22 / 3.13)
+//   fp32 tiles: K = 5 -- C2 fp32 3.358 -> 3.108 (K = 3: 3.355)
+// A runtime choice between two K inside one kernel spills (48 bytes) and loses everything,
+// so K is fixed per compiled instance.  SRNN_LOADK_* override for experiments.
+#ifndef SRNN_LOADK_BT4
+#define SRNN_LOADK_BT4 5
+#endif
+#ifndef SRNN_LOADK_WIDE8
+#define SRNN_LOADK_WIDE8 6
+#endif
+#ifndef SRNN_LOADK_F32
+#define SRNN_LOADK_F32 5
+#endif
 template <int NP, bool F16, int BT>
 struct LoadKTile {
-    static constexpr int value = (F16 && BT == 4 && NP <= 24) ? 5 : LoadK<NP, F16>::value;
+    static constexpr int value = (F16 && BT == 4 && NP <= 24) ? SRNN_LOADK_BT4
+                                 : (F16 && BT >= 8)          ? SRNN_LOADK_WIDE8
+                                 : !F16                      ? SRNN_LOADK_F32
+                                                             : LoadK<NP, F16>::value;
 };
 
 __device__ __forceinline__ void cp_async_f32(float* dst_smem, const float* src) {
