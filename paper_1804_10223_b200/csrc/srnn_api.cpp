@@ -86,6 +86,7 @@ struct srnn_plan {
     bool dense = false;
     int dense_mt = 0, dense_kpw = 0, dense_nf = 0, dense_inst = 0, hs_rows = 0;
     std::vector<uint4> dense_img;  // host image [cta][frag][thread] (freed after upload)
+    bool k8 = false;               // sparse fp16 tile-of-4 plan that needs 8 poll slots per thread
 };
 
 namespace {
@@ -689,6 +690,10 @@ search_again:
     p->smem_bytes = smem_for(p, umax, p->BT, p->n_tiles_max) + 16 +
                     static_cast<size_t>(best_ns) * fin.threads * pair_bytes;
     p->np_inst = best_inst;
+    // fp16 tiles of 4 with <= 24 register slots poll 5 chunks per thread (LoadKTile); a plan
+    // whose threads own more chunks than that takes the 8-slot instance of the same width
+    // instead of paying a second poll round trip per step.
+    p->k8 = p->f16 && p->BT == 4 && best_inst <= 24 && (H + best.threads - 1) / best.threads > 5;
     p->model_cost = best_cost;
     p->ns_slots = best_ns;
     p->lay = std::move(fin);
@@ -801,6 +806,7 @@ search_again:
         // Compiled register count and co-residency check for the instance.
         RecParams rp{};
         rp.threads = l.threads;
+        rp.k8 = p->k8 ? 1 : 0;
         int regs = 0, maxb = 0;
         int le = p->dense ? launch_dense(p->dense_inst, p->dense_mt, p->BT, G, rp, l.num_ctas, p->smem_bytes, nullptr,
                                          true, &regs, &maxb)
@@ -914,6 +920,7 @@ static srnn_status_t recurrence_impl(srnn_plan_t p, int32_t T, int32_t B, const 
     rp.units_max = umax;
     rp.epoch = p->epoch;
     rp.flags = p->cfg.flags;
+    rp.k8 = p->k8 ? 1 : 0;
     if (p->f16)
         rp.img_f16 = static_cast<const uint32_t*>(p->d_img);
     else

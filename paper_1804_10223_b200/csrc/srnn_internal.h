@@ -52,6 +52,7 @@ struct RecParams {
     uint32_t bp_ready_base;
     uint32_t* progress;        // +1 per CTA every progress_every steps (after y is stored), or null
     int32_t progress_every;
+    int32_t k8;                // host-side instance choice: fp16 tiles of 4 polling 8 chunks per thread
     // SRNN_FLAG_DENSE_TC comparator (dense U_r as mma.sync A fragments)
     const uint4* img_dense;    // [cta][frag][thread] A fragments (4 x 2 fp16), frag = kk * MT + m
     int32_t dense_kpw;         // k-blocks (16 columns) per warp

@@ -633,7 +633,8 @@ __device__ __forceinline__ void cp_async_commit_wait_all() {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// MT = 0: the sparse kernel (NP register slots per lane).  MT >= 1: the dense
+// MT = 0: the sparse kernel (NP register slots per lane); MT = -1: the same with 8 poll
+// slots per thread (fp16 tiles of 4 whose threads own > 5 chunks).  MT >= 1: the dense
 // tensor-core comparator (NP register A fragments per lane, MT row tiles).
 template <int NP, int BT, int G, bool F16, int MT = 0>
 __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16, BT>::value, 1)
@@ -797,7 +798,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
             // ---- load: h_{s-1} tile k -> hs ----
             const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
                 p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
-            if (!load_tile<F16, BT, LoadKTile<NP, F16, BT>::value, DENSE>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
+            if (!load_tile<F16, BT, (MT < 0 ? LoadK<NP, F16>::value : LoadKTile<NP, F16, BT>::value), DENSE>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
                                                             !grid_sync, p.status, p.timeout_ns, p.poll_backoff_ns,
                                                             p.loader_threads, ps))
                 *s_abort = 1;
@@ -984,6 +985,13 @@ int launch_np(int bt, int g, const RecParams& p, int num_ctas, size_t smem, void
 #define SRNN_CASE(BT_, G_)                                                                                    \
     if (bt == BT_ && g == G_)                                                                                 \
         return launch_one<NP, BT_, G_, F16>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out);
+    if constexpr (F16 && NP <= 24) {  // fp16 tiles of 4 needing 8 poll slots per thread
+        if (bt == 4 && p.k8) {
+            if (g == 1) return launch_one<NP, 4, 1, F16, -1>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out);
+            if (g == 3) return launch_one<NP, 4, 3, F16, -1>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out);
+            if (g == 4) return launch_one<NP, 4, 4, F16, -1>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out);
+        }
+    }
     SRNN_CASE(1, 1)
     SRNN_CASE(2, 1)
     SRNN_CASE(4, 1)
