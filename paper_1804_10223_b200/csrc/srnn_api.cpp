@@ -693,7 +693,13 @@ search_again:
     // fp16 tiles of 4 with <= 24 register slots poll 5 chunks per thread (LoadKTile); a plan
     // whose threads own more chunks than that takes the 8-slot instance of the same width
     // instead of paying a second poll round trip per step.
-    p->k8 = p->f16 && p->BT == 4 && best_inst <= 24 && (H + best.threads - 1) / best.threads > 5;
+    {
+        // poll slots per thread of the default instance (LoadKTile in srnn_recurrent.cuh)
+        const int ksmall = p->BT == 4 ? (best_inst <= 24 ? 5 : (best_inst <= 48 ? 8 : 4)) : (p->BT >= 8 ? 6 : 0);
+        const int64_t chunks = static_cast<int64_t>(H) * (p->BT / 2) / 2;  // 16-byte chunks per tile (fp16)
+        const int64_t c = (chunks + best.threads - 1) / best.threads;          // per thread
+        p->k8 = p->f16 && ksmall > 0 && ksmall < 8 && (c + 7) / 8 < (c + ksmall - 1) / ksmall;
+    }
     p->model_cost = best_cost;
     p->ns_slots = best_ns;
     p->lay = std::move(fin);

@@ -798,7 +798,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
             // ---- load: h_{s-1} tile k -> hs ----
             const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
                 p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
-            if (!load_tile<F16, BT, (MT < 0 ? LoadK<NP, F16>::value : LoadKTile<NP, F16, BT>::value), DENSE>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
+            if (!load_tile<F16, BT, (MT < 0 ? 8 : LoadKTile<NP, F16, BT>::value), DENSE>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
                                                             !grid_sync, p.status, p.timeout_ns, p.poll_backoff_ns,
                                                             p.loader_threads, ps))
                 *s_abort = 1;
@@ -985,11 +985,18 @@ int launch_np(int bt, int g, const RecParams& p, int num_ctas, size_t smem, void
 #define SRNN_CASE(BT_, G_)                                                                                    \
     if (bt == BT_ && g == G_)                                                                                 \
         return launch_one<NP, BT_, G_, F16>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out);
-    if constexpr (F16 && NP <= 24) {  // fp16 tiles of 4 needing 8 poll slots per thread
-        if (bt == 4 && p.k8) {
-            if (g == 1) return launch_one<NP, 4, 1, F16, -1>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out);
-            if (g == 3) return launch_one<NP, 4, 3, F16, -1>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out);
-            if (g == 4) return launch_one<NP, 4, 4, F16, -1>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out);
+    if constexpr (F16) {  // plans whose threads own more chunks than the default slots: 8 poll slots
+        if (p.k8) {
+#define SRNN_K8(BT_)                                                                                          \
+    if (bt == BT_) {                                                                                          \
+        if (g == 1) return launch_one<NP, BT_, 1, F16, -1>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out); \
+        if (g == 3) return launch_one<NP, BT_, 3, F16, -1>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out); \
+        if (g == 4) return launch_one<NP, BT_, 4, F16, -1>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out); \
+    }
+            if constexpr (NP <= 24) { SRNN_K8(4) }
+            SRNN_K8(8)
+            if constexpr (NP <= kMaxNP16) { SRNN_K8(16) }
+#undef SRNN_K8
         }
     }
     SRNN_CASE(1, 1)
