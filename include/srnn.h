@@ -90,7 +90,9 @@ typedef enum { SRNN_PREC_FP32 = 0, SRNN_PREC_FP16W_FP32ACC = 1 } srnn_prec_t;
 #define SRNN_FLAG_FP32_STAGING   (1u << 5) /* fp16 mode: stage/exchange h in fp32 and keep fp32
                                               register pairs (ablation; default fp16 staging and
                                               one register per pair)        */
-#define SRNN_FLAG_PROFILE        (1u << 6) /* record per-CTA phase timestamps (srnn_plan_debug_timeline) */
+#define SRNN_FLAG_PROFILE        (1u << 6) /* record per-CTA phase timestamps (srnn_plan_debug_timeline);
+                                              diagnostics build libsrnn_profile.so only, else
+                                              srnn_plan_create returns SRNN_ERR_UNSUPPORTED */
 #define SRNN_FLAG_RESERVE_SMS    (1u << 7) /* leave 4 SMs free so srnn_forward_host can pipeline: x
                                               chunks are copied and projected (GEMM on the free SMs)
                                               while the persistent kernel runs, y chunks are copied
@@ -243,11 +245,14 @@ srnn_status_t srnn_plan_status(srnn_plan_t plan);
 srnn_status_t srnn_plan_export_layout(srnn_plan_t plan, int32_t *col_out, float *val_out,
                                       int32_t *row_out, int64_t capacity);
 
-/* Debug: with SRNN_FLAG_PROFILE, copy the clock64 stamps of the last forward
- * to host `out` as [num_ctas][T][num_tiles][8] int64 (SM cycle counter of
- * that CTA's SM, thread 0): 0 step start, 1 h staged (after the barrier),
- * 2 after the second barrier, 3 h published, 4 operate loop done, 5 butterfly
- * done, 6 b' copies landed; 7 unused.
+/* Debug: with SRNN_FLAG_PROFILE, copy the stamps of the last forward to host
+ * `out` as [num_ctas][T][num_tiles][16] int64.  Slots 0-7 and 10 are clock64
+ * (SM cycle counter of that CTA's SM, thread 0): 0 step start, 1 h staged
+ * (after the barrier), 2 after the second barrier, 3 h published, 4 operate
+ * loop done, 5 butterfly done, 6 b' copies landed, 7 after the post-publish
+ * barrier, 10 thread 0's first poll round returned.  8: poll rounds of
+ * thread 0, 9: max poll rounds over the CTA's threads.  11 / 12: %globaltimer
+ * (ns, comparable across CTAs) at 3 / 1.  13-15 unused.
  * `capacity` in elements; returns the element count via *count.
  * Errors: SRNN_ERR_STATE without the flag or before a forward. */
 srnn_status_t srnn_plan_debug_timeline(srnn_plan_t plan, int64_t *out, int64_t capacity, int64_t *count);

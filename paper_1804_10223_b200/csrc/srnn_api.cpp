@@ -64,9 +64,12 @@ struct srnn_plan {
     float* d_bias = nullptr;
     float* d_bhn = nullptr;         // GRU: n-gate recurrent bias [H]
     float* d_bprime = nullptr;      // [T_max][B_max][G*H]
-    unsigned long long* d_xbuf = nullptr;
+    unsigned char* d_xbuf = nullptr;  // exchange images [2][n_tiles_max][tile_bytes] (srnn_recurrent.cuh Fmt)
+    int32_t* d_xdirty = nullptr;       // set on device by an aborted launch
     int32_t* d_status = nullptr;
-    size_t xbuf_words = 0;
+    size_t xbuf_bytes = 0;
+    int64_t tile_bytes = 0;
+    int xbuf_valid_tiles = 0;          // tiles whose stale tags follow the global step sequence
     uint32_t epoch = 1;
     // host-call staging (srnn_forward_host)
     cudaStream_t stream = nullptr;
@@ -134,6 +137,7 @@ void free_device(srnn_plan* p) {
     cudaFree(p->d_bhn);
     cudaFree(p->d_bprime);
     cudaFree(p->d_xbuf);
+    cudaFree(p->d_xdirty);
     cudaFree(p->d_status);
     cudaFree(p->d_x);
     cudaFree(p->d_h0);
@@ -209,9 +213,8 @@ double cost_model(const Layout& lay, int bt, int H, int n_tiles, bool f16, int i
     int lg = 0;
     while ((1 << lg) < lay.lanes_per_row) ++lg;
     const double reduce = lg * (30.0 + 2.0 * bt);
-    const double words_per_unit = f16 ? (bt >= 2 ? bt / 2.0 : 1.0) : bt;
-    const double chunks = static_cast<double>(H) * words_per_unit / 2.0;
-    const double k = (f16 && inst <= 48) ? 8.0 : 4.0;  // LoadK<NP, F16> in srnn_recurrent.cuh
+    const double chunks = static_cast<double>(exchange_tile_bytes(H, f16, bt)) / 16.0;
+    const double k = poll_slots(inst, f16, bt, false);
     const double groups = std::ceil(chunks / (lay.threads * k));
     const double load = groups * 900.0 + chunks * 16.0 / 48.0;
     int umax = 0;
@@ -226,6 +229,26 @@ double cost_model(const Layout& lay, int bt, int H, int n_tiles, bool f16, int i
 }
 
 }  // namespace
+
+// Exchange images, status words, b' buffer and the plan stream (sparse and dense plans).
+srnn_status_t alloc_exchange(srnn_plan* p) {
+    const srnn_config_t& c = p->cfg;
+    p->tile_bytes = exchange_tile_bytes(c.hidden, p->f16 || p->dense, p->BT);
+    p->xbuf_bytes = 2 * static_cast<size_t>(p->n_tiles_max) * p->tile_bytes;
+    p->xbuf_valid_tiles = 0;  // the first launch writes the stale tags (kernel re-init)
+    const size_t bp_elems = static_cast<size_t>(std::max(1, c.max_steps)) * c.batch * p->G * c.hidden;
+    if (cudaMalloc(&p->d_xbuf, p->xbuf_bytes) != cudaSuccess ||
+        cudaMalloc(&p->d_xdirty, sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&p->d_status, sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&p->d_bprime, bp_elems * sizeof(float)) != cudaSuccess ||
+        cudaMemset(p->d_xbuf, 0, p->xbuf_bytes) != cudaSuccess ||
+        cudaMemset(p->d_xdirty, 0, sizeof(int32_t)) != cudaSuccess ||
+        cudaMemset(p->d_status, 0, sizeof(int32_t)) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess)  // memsets complete before any non-blocking stream
+        return SRNN_ERR_CUDA;
+    return SRNN_OK;
+}
 
 // ---------------------------------------------------------------------------
 // SRNN_FLAG_DENSE_TC: the dense persistent RNN comparator (SURVEY.md Sec.
@@ -258,16 +281,7 @@ srnn_status_t create_dense(srnn_plan* p, srnn_plan_t* out) {
     p->hs_rows = 256 * kpw;
     if (!p->host_only) {
         DeviceGuard g(c.device);
-        const size_t tile_stride = (static_cast<size_t>(c.hidden) * (bt / 2) + 1) & ~static_cast<size_t>(1);
-        p->xbuf_words = 2 * static_cast<size_t>(p->n_tiles_max) * tile_stride;
-        const size_t bp_elems = static_cast<size_t>(std::max(1, c.max_steps)) * c.batch * p->G * c.hidden;
-        if (cudaMalloc(&p->d_xbuf, p->xbuf_words * 8) != cudaSuccess ||
-            cudaMalloc(&p->d_status, sizeof(int32_t)) != cudaSuccess ||
-            cudaMalloc(&p->d_bprime, bp_elems * sizeof(float)) != cudaSuccess ||
-            cudaMemset(p->d_xbuf, 0, p->xbuf_words * 8) != cudaSuccess ||
-            cudaMemset(p->d_status, 0, sizeof(int32_t)) != cudaSuccess ||
-            cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaDeviceSynchronize() != cudaSuccess) {
+        if (alloc_exchange(p) != SRNN_OK) {
             free_device(p);
             delete p;
             return SRNN_ERR_CUDA;
@@ -380,6 +394,9 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
         c.batch_tile != 16)
         return SRNN_ERR_INVALID_VALUE;
 
+#ifndef SRNN_PROFILE
+    if (c.flags & SRNN_FLAG_PROFILE) return SRNN_ERR_UNSUPPORTED;  // timestamps exist only in libsrnn_profile.so
+#endif
     srnn_plan* p = new (std::nothrow) srnn_plan();
     if (!p) return SRNN_ERR_INVALID_VALUE;
     p->cfg = c;
@@ -453,17 +470,7 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     }
     if (!p->host_only) {
         DeviceGuard g(c.device);
-        const int wpr = p->f16 ? (bt >= 2 ? bt / 2 : 1) : bt;  // tagged words per unit
-        const size_t tile_stride = (static_cast<size_t>(c.hidden) * wpr + 1) & ~static_cast<size_t>(1);
-        p->xbuf_words = 2 * static_cast<size_t>(p->n_tiles_max) * tile_stride;
-        const size_t bp_elems = static_cast<size_t>(std::max(1, c.max_steps)) * c.batch * p->G * c.hidden;
-        if (cudaMalloc(&p->d_xbuf, p->xbuf_words * 8) != cudaSuccess ||
-            cudaMalloc(&p->d_status, sizeof(int32_t)) != cudaSuccess ||
-            cudaMalloc(&p->d_bprime, bp_elems * sizeof(float)) != cudaSuccess ||
-            cudaMemset(p->d_xbuf, 0, p->xbuf_words * 8) != cudaSuccess ||
-            cudaMemset(p->d_status, 0, sizeof(int32_t)) != cudaSuccess ||
-            cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaDeviceSynchronize() != cudaSuccess) {  // memsets complete before any non-blocking stream
+        if (alloc_exchange(p) != SRNN_OK) {
             free_device(p);
             delete p;
             return SRNN_ERR_CUDA;
@@ -524,8 +531,10 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
     const int H = p->cfg.hidden, G = p->G, R = G * H;
     // ---- validate CSR (S:125 duplicates; rowptr monotone; col range) ----
     if (rowptr[0] != 0 || rowptr[R] != nnz) return SRNN_ERR_BAD_WEIGHTS;
+    // every row range inside [0, nnz] before any column is read
+    for (int r = 0; r < R; ++r)
+        if (rowptr[r + 1] < rowptr[r] || rowptr[r + 1] > nnz) return SRNN_ERR_BAD_WEIGHTS;
     for (int r = 0; r < R; ++r) {
-        if (rowptr[r + 1] < rowptr[r]) return SRNN_ERR_BAD_WEIGHTS;
         std::vector<int32_t> cs(col + rowptr[r], col + rowptr[r + 1]);
         for (int32_t v : cs)
             if (v < 0 || v >= H) return SRNN_ERR_BAD_WEIGHTS;
@@ -655,7 +664,9 @@ search_again:
         // the 16-sample tile's h staging left no room for the weights: 8-sample tiles
         p->BT = 8;
         p->E = elem_bytes(true, 8);
-        p->n_tiles_max = (p->cfg.batch + 7) / 8;  // exchange words: ceil(B/8)*4H <= ceil(B/16)*8H, xbuf fits
+        p->n_tiles_max = (p->cfg.batch + 7) / 8;  // exchange bytes: ceil(B/8)*16H <= ceil(B/16)*32H, xbuf fits
+        p->tile_bytes = exchange_tile_bytes(H, true, 8);
+        p->xbuf_valid_tiles = 0;
         in.BT = 8;
         in.E = 16;
         goto search_again;
@@ -690,15 +701,14 @@ search_again:
     p->smem_bytes = smem_for(p, umax, p->BT, p->n_tiles_max) + 16 +
                     static_cast<size_t>(best_ns) * fin.threads * pair_bytes;
     p->np_inst = best_inst;
-    // fp16 tiles of 4 with <= 24 register slots poll 5 chunks per thread (LoadKTile); a plan
-    // whose threads own more chunks than that takes the 8-slot instance of the same width
-    // instead of paying a second poll round trip per step.
+    // A plan whose threads own more exchange chunks than the default instance polls at once
+    // (poll_slots) takes the 8-slot instance of the same width, where one is compiled,
+    // instead of paying another poll round trip per step.
     {
-        // poll slots per thread of the default instance (LoadKTile in srnn_recurrent.cuh)
-        const int ksmall = p->BT == 4 ? (best_inst <= 24 ? 5 : (best_inst <= 48 ? 8 : 4)) : (p->BT >= 8 ? 6 : 0);
-        const int64_t chunks = static_cast<int64_t>(H) * (p->BT / 2) / 2;  // 16-byte chunks per tile (fp16)
-        const int64_t c = (chunks + best.threads - 1) / best.threads;          // per thread
-        p->k8 = p->f16 && ksmall > 0 && ksmall < 8 && (c + 7) / 8 < (c + ksmall - 1) / ksmall;
+        const int ksmall = poll_slots(best_inst, p->f16, p->BT, false);
+        const int64_t chunks = exchange_tile_bytes(H, p->f16, p->BT) / 16;  // 16-byte chunks per tile
+        const int64_t c = (chunks + best.threads - 1) / best.threads;       // per thread
+        p->k8 = k8_compiled(best_inst, p->f16, p->BT) && ksmall < 8 && (c + 7) / 8 < (c + ksmall - 1) / ksmall;
     }
     p->model_cost = best_cost;
     p->ns_slots = best_ns;
@@ -906,10 +916,6 @@ static srnn_status_t recurrence_impl(srnn_plan_t p, int32_t T, int32_t B, const 
             e = c0 ? cudaMemcpyAsync(cT, c0, hb, cudaMemcpyDeviceToDevice, st) : cudaMemsetAsync(cT, 0, hb, st);
         return e == cudaSuccess ? SRNN_OK : SRNN_ERR_CUDA;
     }
-    if (static_cast<uint64_t>(p->epoch) + static_cast<uint64_t>(T) + 1 >= 0xffffffffull) {
-        if (cudaMemsetAsync(p->d_xbuf, 0, p->xbuf_words * 8, st) != cudaSuccess) return SRNN_ERR_CUDA;
-        p->epoch = 1;
-    }
     RecParams rp{};
     rp.H = p->cfg.hidden;
     rp.G = p->G;
@@ -941,18 +947,24 @@ static srnn_status_t recurrence_impl(srnn_plan_t p, int32_t T, int32_t B, const 
     rp.hT = hT;
     rp.cT = p->G == 4 ? cT : nullptr;
     rp.xbuf = p->d_xbuf;
+    rp.tile_bytes = static_cast<int32_t>(p->tile_bytes);
+    rp.xbuf_tiles = p->n_tiles_max;
+    rp.xdirty = p->d_xdirty;
+    // 1-bit tags follow the global step (epoch + s, continuous across launches and
+    // across the u32 wrap); tiles idle in the previous launch hold older steps
+    rp.reinit = rp.n_tiles > p->xbuf_valid_tiles ? 1 : 0;
     rp.status = p->d_status;
     rp.timeout_ns = p->timeout_ns;
-    if (const char* d = std::getenv("SRNN_POLL_DELAY_NS")) rp.poll_delay_ns = static_cast<uint32_t>(std::atoi(d));
     if (const char* d = std::getenv("SRNN_POLL_BACKOFF_NS")) rp.poll_backoff_ns = static_cast<uint32_t>(std::atoi(d));
     if (const char* d = std::getenv("SRNN_LOADER_THREADS")) rp.loader_threads = std::atoi(d);
     if (p->cfg.flags & SRNN_FLAG_PROFILE) {
-        const int64_t need = static_cast<int64_t>(p->lay.num_ctas) * T * rp.n_tiles * 8;
+        const int64_t need = static_cast<int64_t>(p->lay.num_ctas) * T * rp.n_tiles * 16;
         if (need > p->prof_elems) {
             cudaFree(p->d_prof);
             p->d_prof = nullptr;
             if (cudaMalloc(&p->d_prof, need * 8) != cudaSuccess) return SRNN_ERR_CUDA;
         }
+        if (cudaMemsetAsync(p->d_prof, 0, need * 8, static_cast<cudaStream_t>(stream)) != cudaSuccess) return SRNN_ERR_CUDA;
         p->prof_elems = need;
         rp.profile = p->d_prof;
     }
@@ -975,6 +987,7 @@ static srnn_status_t recurrence_impl(srnn_plan_t p, int32_t T, int32_t B, const 
     }
     if (e != 0) return SRNN_ERR_CUDA;
     p->epoch += static_cast<uint32_t>(T) + 1;
+    p->xbuf_valid_tiles = rp.n_tiles;
     return SRNN_OK;
 }
 

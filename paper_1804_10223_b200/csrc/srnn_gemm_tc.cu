@@ -355,14 +355,12 @@ template <int BN, bool X3 = false>
 static int launch_gemm_tc_bn(const void* map_a, const void* map_b, const float* bias, float* C, int M, int N, int K,
                              cudaStream_t stream, int m_off, int sms, const void* map_a_lo = nullptr,
                              const void* map_b_lo = nullptr) {
-    static bool attr_set = false;
+    // The shared-memory opt-in is a per-device function attribute: set it on every launch
+    // (cheap, thread-safe; a process may drive plans on several devices).
     const size_t smem = TcCfg<BN, X3>::SMEM;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_tc_f16_kernel<BN, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return static_cast<int>(e);
-        attr_set = true;
-    }
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_f16_kernel<BN, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return static_cast<int>(e);
     const int64_t tiles = static_cast<int64_t>((N + BN - 1) / BN) * ((M + TC_BM - 1) / TC_BM);
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
     const CUtensorMap& ma = *static_cast<const CUtensorMap*>(map_a);

@@ -3,6 +3,12 @@
 #pragma once
 #include <cstdint>
 
+#ifdef __CUDACC__
+#define SRNN_HD __host__ __device__
+#else
+#define SRNN_HD
+#endif
+
 #ifndef SRNN_MAX_THREADS
 #define SRNN_MAX_THREADS 1024
 #endif
@@ -24,7 +30,7 @@ struct RecParams {
     int32_t np_inst;  // register slots per lane (= template NP)
     int32_t smem_slots;  // shared-memory tier slots per lane (multiple of 4; image width = NP + smem_slots)
     int32_t units_max;      // max units of any CTA (smem sizing)
-    uint32_t epoch;   // tag of h_0 for this call; h_s carries epoch + s
+    uint32_t epoch;   // global step of h_0 for this call; h_s is global step epoch + s (1-bit tag: bit 1)
     uint32_t flags;   // SRNN_FLAG_* subset relevant on device
     // packed weights: [cta][slot][thread]
     const uint2* img_f32;      // fp32 mode: {hs byte offset, float bits}
@@ -39,10 +45,13 @@ struct RecParams {
     float* y;             // [T][B][H] or null
     float* hT;            // [B][H] or null
     float* cT;            // [B][H] or null
-    unsigned long long* xbuf;  // tagged exchange words [2][n_tiles][H][BT]
+    unsigned char* xbuf;  // exchange images [2 global-step parities][xbuf_tiles][tile_bytes] (= the hs layout, tag in each LSB)
+    int32_t xbuf_tiles;   // tile stride of xbuf (the plan's maximum, fixed across launches)
+    int32_t tile_bytes;   // bytes of one (parity, tile) image: H * E rounded up to 16 (BT = 16: 2 planes of H * 16)
+    int32_t reinit;       // host: the buffers' stale tags are not those of steps epoch - 2 / epoch - 1 (rewrite them)
+    int32_t* xdirty;      // device: set by an aborted launch (buffers inconsistent), cleared by the next re-init
     int32_t* status;      // device status word (srnn_status_t)
     unsigned long long timeout_ns;
-    uint32_t poll_delay_ns;    // sleep before the first poll of a tile (tuning knob, SRNN_POLL_DELAY_NS)
     uint32_t poll_backoff_ns;  // sleep between stale poll rounds (tuning knob, SRNN_POLL_BACKOFF_NS)
     int32_t loader_threads;    // threads that poll/stage h (0 = all; tuning knob, SRNN_LOADER_THREADS)
     long long* profile;   // SRNN_FLAG_PROFILE: [cta][T][n_tiles][8] clock64 stamps or null
@@ -52,7 +61,7 @@ struct RecParams {
     uint32_t bp_ready_base;
     uint32_t* progress;        // +1 per CTA every progress_every steps (after y is stored), or null
     int32_t progress_every;
-    int32_t k8;                // host-side instance choice: fp16 tiles of 4 polling 8 chunks per thread
+    int32_t k8;                // host-side instance choice: the 8-poll-slot instance (k8_compiled)
     // SRNN_FLAG_DENSE_TC comparator (dense U_r as mma.sync A fragments)
     const uint4* img_dense;    // [cta][frag][thread] A fragments (4 x 2 fp16), frag = kk * MT + m
     int32_t dense_kpw;         // k-blocks (16 columns) per warp
@@ -93,13 +102,42 @@ int preload_projection_kernels();
 int preload_gemm_f32();
 int launch_f32_to_f16_padded(const float* in, void* out, int64_t rows, int cols, int ld_out, void* stream);
 
+// Poll slots (16-byte exchange chunks in flight per loader thread) of each compiled
+// instance; the k8 instances (MT = -1 in srnn_recurrent.cuh) poll 8.  Measured on B200
+// (DESIGN.md Sec. 4 "exchange protocol"); SRNN_LOADK_* override for A/B builds.
+#ifndef SRNN_LOADK_BT4
+#define SRNN_LOADK_BT4 3
+#endif
+#ifndef SRNN_LOADK_WIDE8
+#define SRNN_LOADK_WIDE8 6
+#endif
+#ifndef SRNN_LOADK_F32
+#define SRNN_LOADK_F32 5
+#endif
+SRNN_HD constexpr int poll_slots(int np, bool f16, int bt, bool k8) {
+    return k8 ? 8
+         : (f16 && bt == 4 && np <= 24) ? SRNN_LOADK_BT4
+         : (f16 && bt >= 8)             ? SRNN_LOADK_WIDE8
+         : !f16                         ? SRNN_LOADK_F32
+         : (np <= 48 ? 8 : 4);
+}
+// largest register instance compiled with the 16-sample tile (fp16, two hs planes)
+constexpr int kMaxNP16 = 48;
+// An 8-poll-slot instance exists for this (np, precision, tile)?  Must match launch_np.
+SRNN_HD constexpr bool k8_compiled(int np, bool f16, int bt) {
+    return f16 && ((bt == 4 && np <= 24) || bt == 8 || (bt == 16 && np <= kMaxNP16));
+}
+// Bytes of one exchange image (one parity, one batch tile): the staged hs layout,
+// H units x E bytes (E = 2 BT fp16, 4 BT fp32), padded to whole 16-byte chunks.
+SRNN_HD constexpr int64_t exchange_tile_bytes(int64_t H, bool f16, int bt) {
+    return ((H * (f16 ? 2 : 4) * bt) + 15) / 16 * 16;
+}
+
 // Compiled register-slot instances (pairs per lane); 96 exists only for the
 // fp16 mode (one register per pair).
 constexpr int kNumNP = 9;
 constexpr int kNPList[kNumNP] = {4, 8, 12, 16, 24, 32, 48, 64, 96};
 inline int max_np(bool f16) { return f16 ? 96 : 64; }
-// largest register instance compiled with the 16-sample tile (fp16, two hs planes)
-constexpr int kMaxNP16 = 48;
 inline int max_np(bool f16, int bt) { return bt == 16 ? kMaxNP16 : max_np(f16); }
 // Must match MaxThreadsBT<NP, F16, BT> in srnn_recurrent.cuh.
 inline int max_threads_for(int np, bool f16, int bt = 1) {

@@ -36,14 +36,30 @@ namespace srnn {
 
 namespace cg = cooperative_groups;
 
+// Phase timestamps (SRNN_FLAG_PROFILE) exist only in profile builds (-DSRNN_PROFILE):
+// the production kernel carries no per-step instrumentation branches.
+#ifdef SRNN_PROFILE
+#define SRNN_STAMP(i, v)            \
+    do {                            \
+        if (prof) prof[i] = (v);    \
+    } while (0)
+#else
+#define SRNN_STAMP(i, v) \
+    do {                 \
+    } while (0)
+#endif
+
 // Flag bits mirrored from include/srnn.h (device side only needs these).
 constexpr uint32_t kFlagGridSync = 1u << 0;
 constexpr uint32_t kFlagJitter = 1u << 4;
 constexpr uint32_t kFlagProfile = 1u << 6;
 constexpr uint32_t kFlagDropPublish = 1u << 9;
 
-__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_u16(void* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.b16 [%0], %1;" ::"l"(p), "h"(static_cast<unsigned short>(v)) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_u32(void* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ ulonglong2 ld_relaxed_v2(const ulonglong2* p) {
     ulonglong2 r;
@@ -51,11 +67,6 @@ __device__ __forceinline__ ulonglong2 ld_relaxed_v2(const ulonglong2* p) {
                  : "=l"(r.x), "=l"(r.y)
                  : "l"(p)
                  : "memory");
-    return r;
-}
-__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
-    unsigned long long r;
-    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
     return r;
 }
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
@@ -68,14 +79,6 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-__device__ __forceinline__ unsigned long long pack_tagged(float v, uint32_t tag) {
-    return (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(v);
-}
-__device__ __forceinline__ uint32_t tag_of(unsigned long long w) { return static_cast<uint32_t>(w >> 32); }
-__device__ __forceinline__ float val_of(unsigned long long w) {
-    return __uint_as_float(static_cast<uint32_t>(w));
-}
-
 // g(.) of Eq. 1/2. Accurate libdevice transcendentals (no
 // fast-math: the fp32 parity bound is 1e-5).
 // Transcendentals.  FAST (the fp16-staged path) uses the SFU's tanh.approx.f32
@@ -122,104 +125,117 @@ __device__ __forceinline__ bool watchdog_tick(Watchdog& wd, int32_t* status, uns
 }
 
 // ---------------------------------------------------------------------------
-// Exchange / staging formats.
-//   F32: word = {fp32 h, u32 tag}, one word per (unit, sample); hs[H][BT] fp32.
-//   F16: word = {fp16 h(b), fp16 h(b+1), u32 tag}, ceil(BT/2) words per unit;
-//        hs[H][BT] fp16 ("a lower-precision data type for the
-//        activations would remove the shared memory bandwidth and storage
-//        burden").  A 16-byte chunk (two words) always maps onto a contiguous
-//        piece of hs, so the loader is a pure copy with a tag check.
+// Exchange format (reading R16).  The exchange image of one
+// (step parity, batch tile) is byte for byte the staged layout hs: fp32 [H][BT],
+// fp16 [H][BT] for BT <= 8 and two planes [2][H][8] for BT = 16 (so every
+// gather stays one aligned LDS), padded to whole 16-byte chunks.  Validity
+// travels inside the values: every exchanged value of global step g carries
+// the 1-bit tag (g >> 1) & 1 in its mantissa LSB (PAPER.md:102-105 Lamport
+// scheme re-designed: the "not yet written" test is a tag mismatch instead of
+// the -0.0 sentinel).  Buffers alternate by step parity, so a consumer waiting
+// for step g finds either g (fresh) or g - 2 (stale, opposite tag); every
+// value is its own single-copy-atomic access (16 / 32 bits), so a 16-byte
+// chunk is valid iff all its tags match and may be copied to hs unchanged.
+// The producer rounds h (RNE) to one significand bit less than the exchange
+// type -- 10 bits for fp16, 23 for fp32, LSB zero -- and ORs the tag in; the
+// consumer clears it while staging.  So the staged value is the producer's
+// rounded h exactly (error <= 1 ulp of the exchange type, 0 for values with a
+// shorter significand, e.g. small integers), Inf and NaN survive, and y, c and
+// the accumulation are unaffected.
 // ---------------------------------------------------------------------------
 template <bool F16, int BT>
 struct Fmt {
-    static constexpr int WPR = F16 ? (BT >= 2 ? BT / 2 : 1) : BT;  // words per unit
-    static constexpr int E = F16 ? 2 * BT : 4 * BT;            // hs bytes per unit
-    static constexpr int CHUNK_HS = (F16 && BT == 1) ? 4 : 8;  // hs bytes per 16-byte chunk
-
-    // store chunk `idx` (words w0, w1; w1 valid iff has1) into hs.  BT = 16 (fp16)
-    // stages two planes of 8 samples, [2][H][8] fp16 (`ps` = plane stride H * 16 B),
-    // so each 16-byte gather stays LDS.128-aligned like BT = 8.
-    __device__ __forceinline__ static void store(unsigned char* hs, int idx, unsigned long long w0,
-                                                 unsigned long long w1, bool has1, int ps = 0) {
-        if (F16 && BT == 16) {
-            const int q = idx & 3;
-            unsigned char* d = hs + (q >> 1) * ps + (idx >> 2) * 16 + (q & 1) * 8;
-            *reinterpret_cast<uint2*>(d) = make_uint2(static_cast<uint32_t>(w0), static_cast<uint32_t>(w1));
-        } else if (F16 && BT == 1) {
-            const uint32_t lo = static_cast<uint32_t>(w0) & 0xffffu;
-            if (has1)
-                *reinterpret_cast<uint32_t*>(hs + 4 * idx) = lo | (static_cast<uint32_t>(w1) << 16);
-            else
-                *reinterpret_cast<unsigned short*>(hs + 4 * idx) = static_cast<unsigned short>(lo);
-        } else {
-            if (has1)
-                *reinterpret_cast<uint2*>(hs + 8 * idx) = make_uint2(static_cast<uint32_t>(w0), static_cast<uint32_t>(w1));
-            else
-                *reinterpret_cast<uint32_t*>(hs + 8 * idx) = static_cast<uint32_t>(w0);
+    static constexpr int VB = F16 ? 2 : 4;  // bytes per exchanged value
+    static constexpr int E = VB * BT;       // hs bytes per unit (per plane for BT = 16)
+    static constexpr unsigned long long TAGMASK = F16 ? 0x0001000100010001ull : 0x0000000100000001ull;
+    // byte offset of item (unit, sample b) inside a tile image / hs
+    __device__ __forceinline__ static int offset(int H, int unit, int b) {
+        if (F16 && BT == 16) return (b >> 3) * H * 16 + unit * 16 + (b & 7) * 2;
+        return (unit * BT + b) * VB;
+    }
+    // the exchanged value of h: rounded to an even LSB (RNE), carrying `tag` in the LSB
+    __device__ __forceinline__ static uint32_t encode(float h, uint32_t tag) {
+        uint32_t b = __float_as_uint(h);
+        const bool nan = (b & 0x7fffffffu) > 0x7f800000u;
+        if (F16) {
+            if (!nan) b = (b + 0x1fffu + ((b >> 14) & 1u)) & ~0x3fffu;  // RNE to 9 stored bits (exact in fp16)
+            return (static_cast<uint32_t>(__half_as_ushort(__float2half_rn(__uint_as_float(b)))) & ~1u) | tag;
         }
+        if (!nan) b += (b >> 1) & 1u;  // RNE to 22 stored bits (the low bit is cleared below)
+        return (b & ~1u) | tag;
     }
 };
 
-// Stage h_{s-1} (one batch tile) into shared memory.  Every thread owns up
-// to K 16-byte chunks per group (chunk c = thread + j * blockDim); all of them
-// are in flight at once, and chunks whose tags are stale are re-polled
-// together (one round trip per round, not per chunk).  The producers always
-// write whole chunks (an odd word count gets a tagged pad word), so a chunk is
-// valid iff both tags match.  Tag mode spins; grid-sync mode checks once.
-// ROW16 (dense tensor-core comparator): every unit gets a 16-byte hs row
-// (ldmatrix rows); with BT = 4 the upper 8 bytes stay zero.
+// Stage h_{s-1} (one batch tile) into shared memory, in two parts so the
+// first poll round is in flight while the caller does its other per-step
+// bookkeeping (the b' prefetch): issue() sends the loads of a thread's first
+// batch of K 16-byte chunks (chunk c = thread + j * nt); complete() checks
+// them, re-polls the stale ones together (one round trip per round, not per
+// chunk), stages them into hs and then handles any further batches.  Tag mode
+// spins; grid-sync mode checks once.  ROW16 (dense tensor-core comparator):
+// every unit gets a 16-byte hs row (ldmatrix rows); with BT = 4 a chunk holds
+// two units.
 template <bool F16, int BT, int K, bool ROW16 = false>
-__device__ __forceinline__ bool load_tile(const ulonglong2* __restrict__ src, unsigned char* hs, int n_words,
-                                          uint32_t want, bool spin, int32_t* status,
-                                          unsigned long long timeout_ns, uint32_t backoff_ns = 0,
-                                          int loaders = 0, int ps = 0) {
-    const int n_chunks = (n_words + 1) >> 1;
-    const int nt = loaders > 0 ? min(loaders, static_cast<int>(blockDim.x)) : static_cast<int>(blockDim.x);
-    Watchdog wd{0ull, 0u};
-    bool ok = true;
-    for (int base = threadIdx.x; base < n_chunks; base += K * nt) {
-        const ulonglong2* ptr = src + base;
-        ulonglong2 v[K];
-        uint32_t pend = 0u;
+struct Poller {
+    static constexpr unsigned long long M = Fmt<F16, BT>::TAGMASK;
+    ulonglong2 v[K];
+    uint32_t pend;
+
+    __device__ __forceinline__ void issue(const ulonglong2* __restrict__ src, int base, int n_chunks, int nt) {
+        pend = 0u;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
             if (base + j * nt < n_chunks) {
-                v[j] = ld_relaxed_v2(ptr + j * nt);
+                v[j] = ld_relaxed_v2(src + base + j * nt);
                 pend |= 1u << j;
             }
         }
-        while (true) {
+    }
+
+    __device__ __forceinline__ bool complete(const ulonglong2* __restrict__ src, unsigned char* hs, int n_chunks,
+                                             uint32_t tag, bool spin, int32_t* status, unsigned long long timeout_ns,
+                                             uint32_t backoff_ns, int nt, int* rounds, long long* t_first) {
+        const unsigned long long want = tag ? M : 0ull;
+        Watchdog wd{0ull, 0u};
+        for (int base = threadIdx.x; base < n_chunks; base += K * nt) {
+            if (base != static_cast<int>(threadIdx.x)) issue(src, base, n_chunks, nt);
+            while (true) {
 #pragma unroll
-            for (int j = 0; j < K; ++j) {
-                if ((pend >> j) & 1u) {
-                    if ((tag_of(v[j].x) == want) & (tag_of(v[j].y) == want)) {
-                        if (ROW16 && BT == 4)
-                            *reinterpret_cast<uint2*>(hs + 16 * (base + j * nt)) =
-                                make_uint2(static_cast<uint32_t>(v[j].x), static_cast<uint32_t>(v[j].y));
-                        else
-                            Fmt<F16, BT>::store(hs, base + j * nt, v[j].x, v[j].y, true, ps);
-                        pend &= ~(1u << j);
+                for (int j = 0; j < K; ++j) {
+                    if ((pend >> j) & 1u) {
+                        if ((((v[j].x & M) ^ want) | ((v[j].y & M) ^ want)) == 0ull) {
+                            const int c = base + j * nt;
+                            v[j].x &= ~M;  // strip the tags: the producer's rounded values
+                            v[j].y &= ~M;
+                            if (ROW16 && BT == 4) {
+                                *reinterpret_cast<unsigned long long*>(hs + 32 * c) = v[j].x;
+                                *reinterpret_cast<unsigned long long*>(hs + 32 * c + 16) = v[j].y;
+                            } else {
+                                *reinterpret_cast<ulonglong2*>(hs + 16 * c) = v[j];
+                            }
+                            pend &= ~(1u << j);
+                        }
                     }
                 }
-            }
-            if (pend == 0u) break;
-            if (!spin) {
-                atomicCAS(status, 0, -4 /* protocol violation -> SRNN_ERR_STATE */);
-                break;
-            }
-            if (watchdog_tick(wd, status, timeout_ns)) {
-                ok = false;
-                break;
-            }
-            if (backoff_ns) __nanosleep(backoff_ns);
+                if (rounds) {
+                    if (*rounds == 0 && t_first) *t_first = clock64();
+                    ++*rounds;
+                }
+                if (pend == 0u) break;
+                if (!spin) {
+                    atomicCAS(status, 0, -4 /* protocol violation -> SRNN_ERR_STATE */);
+                    return true;
+                }
+                if (watchdog_tick(wd, status, timeout_ns)) return false;
+                if (backoff_ns) __nanosleep(backoff_ns);
 #pragma unroll
-            for (int j = 0; j < K; ++j)
-                if ((pend >> j) & 1u) v[j] = ld_relaxed_v2(ptr + j * nt);
+                for (int j = 0; j < K; ++j)
+                    if ((pend >> j) & 1u) v[j] = ld_relaxed_v2(src + base + j * nt);
+            }
         }
-        if (!ok) break;
+        return true;
     }
-    return ok;
-}
+};
 
 // ---------------------------------------------------------------------------
 // Register-resident weights and the operate stage.
@@ -592,37 +608,6 @@ struct MaxThreadsBT {
     static constexpr int value =
         (F16 && BT == 16) ? (NP <= 4 ? 640 : NP <= 8 ? 512 : NP <= 16 ? 384 : 256) : MaxThreads<NP, F16>::value;
 };
-template <int NP, bool F16>
-struct LoadK {
-    static constexpr int value = F16 ? (NP <= 48 ? 8 : 4) : 4;
-};
-
-// Poll slots per thread (K chunks in flight in the unrolled loader).  Fewer slots mean a
-// shorter loop and fewer live registers; measured on B200 (A/B, same box):
-//   fp16 tiles of 4 (NP <= 24): K = 5 -- C2 2.334 -> 2.176 µs/step (K = 8), 2304 @ 10%
-//     2.252 -> 2.014, LSTM C4 2.071 -> 2.023; K = 4 / 3 / 6: 2.61 / 2.55 / 2.25
-//   fp16 tiles of 8 / 16: K = 6 -- C5 (5760, B = 64) 51.9 -> 43.9, B = 16 5.19 -> 4.96,
-//     B = 8 3.29 -> 3.26 (K = 5: 48.1 / 5.22 / 3.13)
-//   fp32 tiles: K = 5 -- C2 fp32 3.358 -> 3.108 (K = 3: 3.355)
-// A runtime choice between two K inside one kernel spills (48 bytes) and loses everything,
-// so K is fixed per compiled instance.  SRNN_LOADK_* override for experiments.
-#ifndef SRNN_LOADK_BT4
-#define SRNN_LOADK_BT4 5
-#endif
-#ifndef SRNN_LOADK_WIDE8
-#define SRNN_LOADK_WIDE8 6
-#endif
-#ifndef SRNN_LOADK_F32
-#define SRNN_LOADK_F32 5
-#endif
-template <int NP, bool F16, int BT>
-struct LoadKTile {
-    static constexpr int value = (F16 && BT == 4 && NP <= 24) ? SRNN_LOADK_BT4
-                                 : (F16 && BT >= 8)          ? SRNN_LOADK_WIDE8
-                                 : !F16                      ? SRNN_LOADK_F32
-                                                             : LoadK<NP, F16>::value;
-};
-
 __device__ __forceinline__ void cp_async_f32(float* dst_smem, const float* src) {
     const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst_smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
@@ -634,7 +619,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // MT = 0: the sparse kernel (NP register slots per lane); MT = -1: the same with 8 poll
-// slots per thread (fp16 tiles of 4 whose threads own > 5 chunks).  MT >= 1: the dense
+// slots per thread (plans whose threads own more chunks than poll_slots).  MT >= 1: the dense
 // tensor-core comparator (NP register A fragments per lane, MT row tiles).
 template <int NP, int BT, int G, bool F16, int MT = 0>
 __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16, BT>::value, 1)
@@ -662,11 +647,12 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
 
     const int L = DENSE ? 32 : p.lanes_per_row;
     const int n_w = DENSE ? 0 : p.warp_slots[cta * (p.threads >> 5) + warp];
-    const int n_words = H * F::WPR;
-    const int ps = H * 16;                      // BT = 16: second hs plane
-    const unsigned char* hs2 = hs + ps;
-    const int tile_stride = (n_words + 1) & ~1;
+    const int n_chunks = p.tile_bytes >> 4;     // 16-byte chunks of one exchange image
+    const unsigned char* hs2 = hs + H * 16;     // BT = 16: second hs plane
     const int GH = G * H;
+    // values after the last unit that pad the image to whole chunks (written by the last CTA)
+    const int n_pad = (cta == static_cast<int>(gridDim.x) - 1 && !(F16 && BT == 16))
+                          ? (p.tile_bytes - H * F::E) / F::VB : 0;
 
     // ---- prologue: weights HBM -> registers (once per forward) ----
     Weights<NP, BT, F16> W;
@@ -711,26 +697,50 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     const bool row_leader = (lane & (L - 1)) == 0 && krow < G * U;
     if (tid == 0) *s_abort = 0;
 
-    // Publish item e's h of (step s, tile k) as tagged words.  Called by all
-    // threads of the CTA (the fp16 pairing uses a shuffle); `ok` masks items.
+    // Publish item e's h of (step s, tile k) into the exchange image of parity
+    // s & 1 (one relaxed 16/32-bit store per item, tag (global step >> 1) & 1
+    // in the LSB, reading R16); `ok` masks items.  The first item round also
+    // writes the tagged pad values of the last CTA.
+    auto store_tagged = [&](unsigned char* img, int off, float h, uint32_t tag) {
+        if (F16)
+            st_relaxed_u16(img + off, F::encode(h, tag));
+        else
+            st_relaxed_u32(img + off, F::encode(h, tag));
+    };
+    const bool drop_cta = (p.flags & kFlagDropPublish) && cta == 0;  // test hook: lost exchange message
+    const bool jitter0 = (p.flags & kFlagJitter) && tid == 0;          // test hook: per-CTA delays
     auto publish = [&](int s, int k, int e, bool ok, float h) {
-        if ((p.flags & kFlagDropPublish) && cta == 0 && s == 2) return;  // fault injection (CTA-uniform)
-        unsigned long long* dst = p.xbuf + static_cast<size_t>((s & 1) * p.n_tiles + k) * tile_stride;
-        const uint32_t tag = p.epoch + static_cast<uint32_t>(s);
-        if ((n_words & 1) && cta == 0 && e == 0)  // keep every 16-byte chunk whole: tagged pad word
-            st_relaxed_u64(dst + n_words, static_cast<unsigned long long>(tag) << 32);
-        const int unit = u0 + e / BT, eb = e % BT;
-        if (!F16) {
-            if (ok) st_relaxed_u64(dst + unit * BT + eb, pack_tagged(h, tag));
-        } else {
-            const uint32_t hb = __half_as_ushort(__float2half_rn(h));
-            const uint32_t nb = __shfl_down_sync(0xffffffffu, hb, 1);
-            if (ok && (BT == 1 || (eb & 1) == 0)) {
-                const uint32_t lo = BT == 1 ? hb : (hb | (nb << 16));
-                st_relaxed_u64(dst + unit * F::WPR + (eb >> 1), (static_cast<unsigned long long>(tag) << 32) | lo);
+        if (drop_cta && s == 2) return;  // fault injection (CTA-uniform)
+        const uint32_t g = p.epoch + static_cast<uint32_t>(s);  // global step: parity g & 1, tag (g >> 1) & 1
+        unsigned char* dst = p.xbuf + static_cast<size_t>((g & 1u) * p.xbuf_tiles + k) * p.tile_bytes;
+        const uint32_t tag = (g >> 1) & 1u;
+#ifdef SRNN_PUB32
+        if (F16 && BT >= 2 && BT <= 8) {  // A/B: two samples per 32-bit store
+            const uint32_t v = F::encode(h, tag);
+            const uint32_t nb = __shfl_down_sync(0xffffffffu, v, 1);
+            if (ok && ((e % BT) & 1) == 0) st_relaxed_u32(dst + F::offset(H, u0 + e / BT, e % BT), v | (nb << 16));
+        } else
+#endif
+        if (ok) store_tagged(dst, F::offset(H, u0 + e / BT, e % BT), h, tag);
+        if (e < n_pad) store_tagged(dst, H * F::E + e * F::VB, 0.0f, tag);
+    };
+
+    // ---- exchange re-initialisation: the stale values of both parities must carry the
+    // tags of global steps epoch - 2 / epoch - 1 (the host asks for it when the buffers
+    // are fresh or were idle for some tiles; an aborted launch marks them dirty) ----
+    if (p.reinit || *reinterpret_cast<volatile int32_t*>(p.xdirty) != 0) {
+        for (int q = 0; q < 2; ++q) {
+            const uint32_t g = p.epoch + static_cast<uint32_t>(q);  // first step of this launch in parity g & 1
+            const uint32_t stale = ((g - 2u) >> 1) & 1u;
+            for (int k = 0; k < p.n_tiles; ++k) {
+                unsigned char* dst = p.xbuf + static_cast<size_t>((g & 1u) * p.xbuf_tiles + k) * p.tile_bytes;
+                for (int e = tid; e < n_items; e += nt) store_tagged(dst, F::offset(H, u0 + e / BT, e % BT), 0.0f, stale);
+                if (tid < n_pad) store_tagged(dst, H * F::E + tid * F::VB, 0.0f, stale);
             }
         }
-    };
+        cg::this_grid().sync();
+        if (cta == 0 && tid == 0) *p.xdirty = 0;  // every CTA read the flag before the grid barrier
+    }
 
     // ---- publish h_0 (tag = epoch) and initialise c ----
     for (int k = 0; k < p.n_tiles; ++k) {
@@ -755,12 +765,33 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     // pipelined host forward: b' arrives in chunks of steps and the ready counter only
     // grows, so each thread re-polls (acquire) only when its last observed value is behind
     uint32_t bp_seen = p.bp_ready_base;
+    bool bp_failed = false;  // the b' readiness wait timed out: abort at the next barrier
+    const bool bp_pipelined = p.bp_ready != nullptr;
+    // one item per thread (the common case): b' source of item e1 = tid hoisted out of the time loop
+    const float* const bp_e1 = p.bprime + static_cast<size_t>(e1_b) * GH + e1_unit;
     auto issue_bprime = [&](int s, int k, int b) {
         float* dstb = bpsb + b * G * umax_bt;
-        if (p.bp_ready != nullptr && tid < n_items && static_cast<int32_t>(bp_seen - p.bp_ready_base) < s) {
+        if (bp_pipelined && tid < n_items && static_cast<int32_t>(bp_seen - p.bp_ready_base) < s) {
             Watchdog wdb{0ull, 0u};
             while (static_cast<int32_t>((bp_seen = ld_acquire_u32(p.bp_ready)) - p.bp_ready_base) < s)
-                if (watchdog_tick(wdb, p.status, p.timeout_ns)) break;
+                if (watchdog_tick(wdb, p.status, p.timeout_ns)) {
+                    bp_failed = true;
+                    return;
+                }
+        }
+        if (item_rounds == 1) {
+            if (e1_ok) {
+                float* d = dstb + e1 * G;
+                if (k * BT + e1_b < p.B) {
+                    const float* src = bp_e1 + (static_cast<size_t>(s - 1) * p.B + k * BT) * GH;
+#pragma unroll
+                    for (int q = 0; q < G; ++q) cp_async_f32(d + q, src + q * H);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < G; ++q) d[q] = 0.0f;
+                }
+            }
+            return;
         }
         for (int j = 0; j < item_rounds; ++j) {
             const int e = tid + j * nt;
@@ -779,37 +810,66 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     int buf = 0;
     if (p.T >= 1) issue_bprime(1, 0, 0);
     cp_async_commit();
+#ifdef SRNN_PROFILE
+    const bool prof_on = (p.flags & kFlagProfile) && p.profile != nullptr;
+#endif
+    const int n_loaders = p.loader_threads > 0 ? min(p.loader_threads, nt) : nt;
+    Poller<F16, BT, poll_slots(NP, F16, BT, MT < 0), DENSE> poll;
 
     for (int s = 1; s <= p.T; ++s) {
         for (int k = 0; k < p.n_tiles; ++k) {
-            long long* prof = (p.flags & kFlagProfile) && p.profile != nullptr && tid == 0
-                                  ? p.profile + ((static_cast<size_t>(cta) * p.T + (s - 1)) * p.n_tiles + k) * 8
-                                  : nullptr;
-            if (prof) prof[0] = clock64();
-            // b' of the NEXT tile -> shared memory (cp.async, double-buffered):
-            // it lands during this whole tile; this tile's b' was issued one
-            // tile earlier.
+#ifdef SRNN_PROFILE
+            long long* prof_all = prof_on
+                                      ? p.profile + ((static_cast<size_t>(cta) * p.T + (s - 1)) * p.n_tiles + k) * 16
+                                      : nullptr;
+            long long* prof = tid == 0 ? prof_all : nullptr;
+            int rounds = 0;
+#endif
+            SRNN_STAMP(0, clock64());
+            // ---- load: h_{s-1} tile k -> hs; the first poll round goes out first ----
+            const uint32_t g_prev = p.epoch + static_cast<uint32_t>(s - 1);  // global step of h_{s-1}
+            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
+                p.xbuf + static_cast<size_t>((g_prev & 1u) * p.xbuf_tiles + k) * p.tile_bytes);
+            // fp16 tiles of <= 4 samples send the first poll round before the b' prefetch (the
+            // round trip hides the prefetch's address work); wider / fp32 tiles hold more chunks
+            // per thread, whose registers would stay live across it (measured: slower), so they
+            // poll after it
+            constexpr bool kEarlyPoll = F16 && BT <= 4;
+            if (kEarlyPoll && tid < n_loaders) poll.issue(src, tid, n_chunks, n_loaders);
+            // b' of the NEXT tile -> shared memory (cp.async, double-buffered) while the
+            // poll loads are in flight; it lands during this whole tile (this tile's b'
+            // was issued one tile earlier)
             {
                 const int ns = k + 1 < p.n_tiles ? s : s + 1, nk = k + 1 < p.n_tiles ? k + 1 : 0;
                 if (ns <= p.T) issue_bprime(ns, nk, buf ^ 1);
                 cp_async_commit();
             }
             float* bps = bpsb + buf * G * umax_bt;
-            // ---- load: h_{s-1} tile k -> hs ----
-            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
-                p.xbuf + static_cast<size_t>(((s - 1) & 1) * p.n_tiles + k) * tile_stride);
-            if (!load_tile<F16, BT, (MT < 0 ? 8 : LoadKTile<NP, F16, BT>::value), DENSE>(src, hs, n_words, p.epoch + static_cast<uint32_t>(s - 1),
-                                                            !grid_sync, p.status, p.timeout_ns, p.poll_backoff_ns,
-                                                            p.loader_threads, ps))
+            if (!kEarlyPoll && tid < n_loaders) poll.issue(src, tid, n_chunks, n_loaders);
+            if (tid < n_loaders &&
+                !poll.complete(src, hs, n_chunks, (g_prev >> 1) & 1u, !grid_sync, p.status, p.timeout_ns,
+                               p.poll_backoff_ns, n_loaders,
+#ifdef SRNN_PROFILE
+                               prof_all ? &rounds : nullptr, prof ? prof + 10 : nullptr
+#else
+                               nullptr, nullptr
+#endif
+                               ))
                 *s_abort = 1;
+            if (bp_failed) *s_abort = 1;
+#ifdef SRNN_PROFILE
+            if (prof_all) atomicMax(reinterpret_cast<unsigned long long*>(prof_all + 9), static_cast<unsigned long long>(rounds));
+#endif
             __syncthreads();
-            if (prof) prof[1] = clock64();
+            SRNN_STAMP(1, clock64());
+            SRNN_STAMP(8, rounds);
+            SRNN_STAMP(12, static_cast<long long>(globaltimer_ns()));
             if (*s_abort) goto done;
 
             // ---- operate + reduce ----
             if constexpr (DENSE) {
                 DW.operate(hs, reinterpret_cast<const uint4*>(ws), red, p.dense_kpw, dense_nf_reg, nt);
-                if (prof) prof[4] = clock64();
+                SRNN_STAMP(4, clock64());
                 __syncthreads();
                 // fixed-order sum of the 16 warps' partial tiles -> zs[local row][sample]
                 for (int e = tid; e < G * U * BT; e += nt) {
@@ -823,14 +883,14 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                     for (int w = 0; w < kDenseThreads / 32; ++w) z += v[w];
                     zs[e] = z;
                 }
-                if (prof) prof[5] = clock64();
+                SRNN_STAMP(5, clock64());
             } else {
                 float acc[BT];
 #pragma unroll
                 for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
                 W.operate(acc, hs, n_w, hs2);
                 if (n_w > NP) operate_smem_tier<BT, F16>(acc, hs, ws, NP, n_w, nt, hs2);
-                if (prof) prof[4] = clock64();
+                SRNN_STAMP(4, clock64());
                 // ---- reduce over the row's L lanes, fixed order ----
                 // L >= BT: log2(BT) halving levels (each lane keeps half of its
                 // samples and receives the partner's sums for them: BT-1
@@ -863,7 +923,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                         }
                     }
                 }
-                if (prof) prof[5] = clock64();
+                SRNN_STAMP(5, clock64());
                 if (L >= BT) {
                     if (zs_writer) zs[krow * BT + sbase] = acc[0];
                 } else if (row_leader) {
@@ -872,12 +932,12 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                 }
             }
             asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's b' (the newest group may pend)
-            if (prof) prof[6] = clock64();
+            SRNN_STAMP(6, clock64());
             __syncthreads();
-            if (prof) prof[2] = clock64();
+            SRNN_STAMP(2, clock64());
 
             // ---- epilogue: activation / gates, y, tagged publish of h_s ----
-            if ((p.flags & kFlagJitter) && tid == 0) {
+            if (jitter0) {
                 const uint32_t r = (static_cast<uint32_t>(cta) * 2654435761u) ^ (static_cast<uint32_t>(s * 40503 + k));
                 __nanosleep((r >> 7) & 2047u);
             }
@@ -932,13 +992,14 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                 }
                 publish(s, k, e, ok, h);
             }
-            if (prof) prof[3] = clock64();
+            SRNN_STAMP(3, clock64());
+            SRNN_STAMP(11, static_cast<long long>(globaltimer_ns()));
             if (grid_sync) cg::this_grid().sync();
             // Start polling for the next tile only once this CTA has published:
             // early pollers only add stale round trips and contend with the
             // epilogue warps for the LSU (measured: -6..10% step time).
             __syncthreads();
-            if (p.poll_delay_ns) __nanosleep(p.poll_delay_ns);
+            SRNN_STAMP(7, clock64());
             buf ^= 1;
             if (p.progress != nullptr && tid == 0 && k == p.n_tiles - 1 &&
                 (s % p.progress_every == 0 || s == p.T)) {
@@ -950,7 +1011,10 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
 done:
     // An aborted launch (watchdog / lost message) still releases the host pipeline's
     // y-copy waits on the progress counter (the host re-reads the counter on error).
-    if (*s_abort && p.progress != nullptr && tid == 0) atomicAdd(p.progress, 1u << 20);
+    if (*s_abort && tid == 0) {
+        atomicExch(p.xdirty, 1);  // the exchange buffers are inconsistent: the next launch re-initialises them
+        if (p.progress != nullptr) atomicAdd(p.progress, 1u << 20);
+    }
     return;
 }
 

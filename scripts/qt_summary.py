@@ -1,7 +1,19 @@
-import json, sys
-for l in open(sys.argv[1] if len(sys.argv) > 1 else 'gpurun_out/qt.log'):
-    if l.startswith('{'):
-        d = json.loads(l); i = d['info']; c = d['cfg']
-        print(f"H={c['H']} B={c['B']} d={c['d']} {c['cell']} {c['prec']} flags={c['flags']} | C={i['num_ctas']} L={i['lanes_per_row']} NP={i['pairs_per_lane']}/{i['slots_used']} thr={i['threads_per_cta']} regs={i['regs_per_thread']} wf={i['wavefronts_per_step_max']} | us/step={d['us_per_step']:.3f} gemm_ms={d['gemm_ms']:.3f}")
-    elif 'Error' in l:
-        print(l.strip()[:200])
+"""Print one line per quick_time / timeline JSON record in the given logs."""
+import json
+import sys
+
+for fn in sys.argv[1:]:
+    for line in open(fn):
+        try:
+            d = json.loads(line)
+        except Exception:
+            if line.strip():
+                print("  !", line.rstrip()[:200])
+            continue
+        c = d["cfg"]
+        key = f"H={c['H']} B={c['B']} d={c['d']} {c['prec']} {c.get('cell','rnn')} flags={c.get('flags',0)}"
+        if "us_per_step" in d:
+            print(f"{key:55s} us/step {d['us_per_step']:.3f} fwd {d['fwd_ms']:.3f} ms gemm {d['gemm_ms']*1e3:.1f} us")
+        else:
+            ph = {k: round(v["median"]) for k, v in d.items() if isinstance(v, dict) and "median" in v}
+            print(f"{key:55s} {ph}")

@@ -119,7 +119,7 @@ def test_bank_aware_layout_cuts_predicted_conflicts(B, prec, cut):
 
 
 @pytest.mark.parametrize("mutate,code", [
-    ("dup", -3), ("range", -3), ("monotone", -3), ("nnz", -3),
+    ("dup", -3), ("range", -3), ("monotone", -3), ("nnz", -3), ("rowptr_past_nnz", -3),
 ])
 def test_load_weights_rejects_bad_csr(mutate, code):
     prob = inputs.make_problem(64, 64, 1, 2, 0.2)
@@ -132,6 +132,9 @@ def test_load_weights_rejects_bad_csr(mutate, code):
         cl[3] = 64
     elif mutate == "monotone":
         rp[5], rp[6] = rp[6], rp[5] - 1
+    elif mutate == "rowptr_past_nnz":
+        # a middle row range far past the end of col: rejected before any column is read
+        rp[10] = nnz + 1_000_000
     m = SparseRNN(64, 64, 1, 2, 0.2, flags=FLAG_HOST_ONLY, prec="fp32")
     lib = load_library()
     from paper_1804_10223_b200._lib import _ptr
