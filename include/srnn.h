@@ -108,6 +108,12 @@ typedef enum { SRNN_PREC_FP32 = 0, SRNN_PREC_FP16W_FP32ACC = 1 } srnn_prec_t;
                                               leaves ~1.5e-8 * K relative error in b' (4.9e-5 at
                                               K = 2304 vs 6e-6 for SIMT), above the 1e-5 parity
                                               bound of the fp32 mode -- not the default        */
+#define SRNN_FLAG_Y_BATCH_MAJOR  (1u << 11) /* y is written batch-major, [B][T][H], instead of [T][B][H]:
+                                              the shards of a batch-partitioned run (SURVEY.md
+                                              Sec. 8(e)) are then contiguous blocks
+                                              of the global [B][T][H] y, so an all-gather needs no
+                                              re-layout.  srnn_forward / srnn_recurrence /
+                                              srnn_forward_host (the latter unpipelined)         */
 #define SRNN_FLAG_DENSE_TC       (1u << 8) /* comparator: the DENSE persistent
                                               RNN of PAPER.md:51-71 (Sec. 3.2, Diamos et al.)
                                               re-done for sm_100a tensor cores.  U_r is densified
@@ -166,6 +172,8 @@ typedef struct {
     int32_t dense_kblocks_per_warp; /* 16-column k-blocks of U_r per warp                      */
     int32_t dense_frags_reg;   /* A fragments per lane held in registers (compiled instance) */
     int32_t dense_frags_smem;  /* A fragments per lane held in shared memory                 */
+    int32_t spill_bytes;       /* local memory (register spills / stack) per thread of the
+                                  chosen compiled instance; 0 for a spill-free instance  (L) */
 } srnn_plan_info_t;
 
 /* Create a plan for the layer described by *cfg.
@@ -198,7 +206,8 @@ srnn_status_t srnn_load_weights(srnn_plan_t plan, const int32_t *wh_rowptr, cons
 /* Whole hot path on device buffers:
  * input projection GEMM into the plan's b' workspace, then the persistent
  * recurrent kernel.  x: device [T][B][I]; h0, c0: device [B][H] or NULL (=0;
- * c0 only for LSTM); y: device [T][B][H] (may be NULL if hT is wanted only);
+ * c0 only for LSTM); y: device [T][B][H] ([B][T][H] with SRNN_FLAG_Y_BATCH_MAJOR;
+ * may be NULL if hT is wanted only);
  * hT, cT: device [B][H] or NULL.  0 <= T <= T_max, 1 <= B <= B_max.
  * T == 0 copies h0 (or zeros) to hT.
  * Errors: SRNN_ERR_STATE (no weights loaded, or host-only plan),

@@ -32,6 +32,7 @@ FLAG_RESERVE_SMS = 1 << 7
 FLAG_DENSE_TC = 1 << 8
 FLAG_DEBUG_DROP_PUBLISH = 1 << 9
 FLAG_FP32_TC_GEMM = 1 << 10
+FLAG_Y_BATCH_MAJOR = 1 << 11
 
 EXPORTED = ["srnn_plan_create", "srnn_plan_query", "srnn_load_weights", "srnn_forward", "srnn_input_projection",
             "srnn_recurrence", "srnn_forward_host", "srnn_plan_status", "srnn_plan_export_layout",
@@ -62,7 +63,7 @@ class PlanInfo(ctypes.Structure):
                  "wavefronts_per_step_ideal", "conflict_wavefronts", "smem_weight_bytes_per_cta",
                  "image_slots_per_lane", "model_cycles_per_step")] + \
                [(n, ctypes.c_int32) for n in
-                ("dense_m_tiles", "dense_kblocks_per_warp", "dense_frags_reg", "dense_frags_smem")]
+                ("dense_m_tiles", "dense_kblocks_per_warp", "dense_frags_reg", "dense_frags_smem", "spill_bytes")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -135,6 +136,7 @@ class SparseRNN:
         self.G = {"rnn": 1, "lstm": 4, "gru": 3}[cell]
         self.cell, self.prec = cell, prec
         self.device = device
+        self.flags = flags
         h = ctypes.c_void_p()
         _check("srnn_plan_create", self.lib.srnn_plan_create(ctypes.byref(self.cfg), ctypes.byref(h)))
         self.handle = h
@@ -204,13 +206,16 @@ class SparseRNN:
         if tuple(t.shape) != tuple(shape):
             raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
 
+    def _yshape(self, T, B):
+        return (B, T, self.H) if self.flags & FLAG_Y_BATCH_MAJOR else (T, B, self.H)
+
     def forward(self, x, h0=None, c0=None, y=None, hT=None, cT=None, stream=None):
-        """srnn_forward: x [T,B,I] -> y [T,B,H] (allocated if None), hT [B,H]."""
+        """srnn_forward: x [T,B,I] -> y [T,B,H] ([B,T,H] with FLAG_Y_BATCH_MAJOR; allocated if None), hT [B,H]."""
         import torch
         T, B = int(x.shape[0]), int(x.shape[1])
         dev = x.device
         if y is None:
-            y = torch.empty((T, B, self.H), dtype=torch.float32, device=dev)
+            y = torch.empty(self._yshape(T, B), dtype=torch.float32, device=dev)
         if hT is None:
             hT = torch.empty((B, self.H), dtype=torch.float32, device=dev)
         if self.G == 4 and cT is None:
@@ -218,7 +223,7 @@ class SparseRNN:
         self._check_dev(x, (T, B, self.I), "x")
         self._check_dev(h0, (B, self.H), "h0")
         self._check_dev(c0, (B, self.H), "c0")
-        self._check_dev(y, (T, B, self.H), "y")
+        self._check_dev(y, self._yshape(T, B), "y")
         self._check_dev(hT, (B, self.H), "hT")
         self._check_dev(cT, (B, self.H), "cT")
         _check("srnn_forward", self.lib.srnn_forward(self.handle, T, B, _ptr(x), _ptr(h0), _ptr(c0), _ptr(y),
@@ -241,12 +246,13 @@ class SparseRNN:
         T, B = int(bprime.shape[0]), int(bprime.shape[1])
         dev = bprime.device
         if y is None:
-            y = torch.empty((T, B, self.H), dtype=torch.float32, device=dev)
+            y = torch.empty(self._yshape(T, B), dtype=torch.float32, device=dev)
         if hT is None:
             hT = torch.empty((B, self.H), dtype=torch.float32, device=dev)
         if self.G == 4 and cT is None:
             cT = torch.empty((B, self.H), dtype=torch.float32, device=dev)
         self._check_dev(bprime, (T, B, self.G * self.H), "bprime")
+        self._check_dev(y, self._yshape(T, B), "y")
         _check("srnn_recurrence", self.lib.srnn_recurrence(self.handle, T, B, _ptr(bprime), _ptr(h0), _ptr(c0),
                                                            _ptr(y), _ptr(hT), _ptr(cT), self._stream(stream)))
         return (y, hT, cT) if self.G == 4 else (y, hT)
@@ -255,7 +261,7 @@ class SparseRNN:
         """srnn_forward_host on numpy (or pinned torch CPU) buffers; synchronous."""
         T, B = int(x.shape[0]), int(x.shape[1])
         if y is None:
-            y = np.empty((T, B, self.H), np.float32)
+            y = np.empty(self._yshape(T, B), np.float32)
         if hT is None:
             hT = np.empty((B, self.H), np.float32)
         if self.G == 4 and cT is None:

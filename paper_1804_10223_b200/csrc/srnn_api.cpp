@@ -39,6 +39,7 @@ struct srnn_plan {
     double model_cost = 0;  // planner cost-model estimate of one timestep (SM cycles)
     int ns_slots = 0;  // shared-memory tier slots per lane
     int regs = 0;
+    int spill_bytes = 0;  // local memory per thread of the compiled instance (0 = no spills)
     size_t smem_bytes = 0;
     int64_t nnz = 0;
     // device buffers
@@ -498,6 +499,7 @@ srnn_status_t srnn_plan_query(srnn_plan_t p, srnn_plan_info_t* out) {
         for (int c = 0; c < l.num_ctas; ++c) umax = std::max(umax, l.cta_unit0[c + 1] - l.cta_unit0[c]);
         out->units_per_cta_max = umax;
         out->regs_per_thread = p->regs;
+        out->spill_bytes = p->spill_bytes;
         out->packed_registers = p->f16 ? 1 : 0;
         out->nnz = p->nnz;
         out->slots_total = l.slots_total;
@@ -823,13 +825,14 @@ search_again:
         RecParams rp{};
         rp.threads = l.threads;
         rp.k8 = p->k8 ? 1 : 0;
-        int regs = 0, maxb = 0;
+        int regs[2] = {0, 0}, maxb = 0;
         int le = p->dense ? launch_dense(p->dense_inst, p->dense_mt, p->BT, G, rp, l.num_ctas, p->smem_bytes, nullptr,
-                                         true, &regs, &maxb)
+                                         true, regs, &maxb)
                           : launch_recurrent(p->np_inst, p->BT, G, p->f16 ? 1 : 0, rp, l.num_ctas, p->smem_bytes,
-                                             nullptr, true, &regs, &maxb);
+                                             nullptr, true, regs, &maxb);
         if (le != 0) return SRNN_ERR_CUDA;
-        p->regs = regs;
+        p->regs = regs[0];
+        p->spill_bytes = regs[1];
         if (maxb < 1) return SRNN_ERR_NOT_ON_CHIP;
         if (preload_projection_kernels() != 0 || preload_gemm_f32() != 0) return SRNN_ERR_CUDA;
         if (cudaDeviceSynchronize() != cudaSuccess) return SRNN_ERR_CUDA;  // uploads visible to every stream
@@ -944,6 +947,9 @@ static srnn_status_t recurrence_impl(srnn_plan_t p, int32_t T, int32_t B, const 
     rp.c0 = p->G == 4 ? c0 : nullptr;
     rp.bias_hn = p->G == 3 ? p->d_bhn : nullptr;
     rp.y = y;
+    const bool batch_major = (p->cfg.flags & SRNN_FLAG_Y_BATCH_MAJOR) != 0;
+    rp.y_bstride = batch_major ? static_cast<int64_t>(T) * p->cfg.hidden : p->cfg.hidden;
+    rp.y_tstride = batch_major ? p->cfg.hidden : static_cast<int64_t>(B) * p->cfg.hidden;
     rp.hT = hT;
     rp.cT = p->G == 4 ? cT : nullptr;
     rp.xbuf = p->d_xbuf;
@@ -1056,7 +1062,9 @@ srnn_status_t srnn_forward_host(srnn_plan_t p, int32_t T, int32_t B, const float
     cudaStream_t st = p->stream;
     const size_t hb = static_cast<size_t>(B) * H * 4;
     cudaError_t e = cudaSuccess;
-    const bool pipelined = T >= 2 && p->lay.num_ctas < p->sm_count && stream_mem_ops();
+    // the pipelined path returns y in chunks of steps: [T][B][H] only
+    const bool pipelined = T >= 2 && p->lay.num_ctas < p->sm_count && stream_mem_ops() &&
+                           (p->cfg.flags & SRNN_FLAG_Y_BATCH_MAJOR) == 0;
     if (!pipelined) {  // plain: H2D, forward, D2H on one stream
         const size_t xb = static_cast<size_t>(T) * B * I * 4, yb = static_cast<size_t>(T) * B * H * 4;
         if (T > 0) e = cudaMemcpyAsync(p->d_x, x_host, xb, cudaMemcpyHostToDevice, st);

@@ -42,7 +42,9 @@ struct RecParams {
     const float* h0;      // [B][H] or null
     const float* c0;      // [B][H] or null
     const float* bias_hn; // GRU: [H] recurrent bias of the n gate (inside r * (.)), or null
-    float* y;             // [T][B][H] or null
+    float* y;             // element (t, b, unit) at b * y_bstride + t * y_tstride + unit, or null
+    int64_t y_bstride;    // [T][B][H]: H;      batch-major [B][T][H]: T * H
+    int64_t y_tstride;    // [T][B][H]: B * H;  batch-major: H
     float* hT;            // [B][H] or null
     float* cT;            // [B][H] or null
     unsigned char* xbuf;  // exchange images [2 global-step parities][xbuf_tiles][tile_bytes] (= the hs layout, tag in each LSB)
@@ -79,7 +81,8 @@ struct GemmParams {
     float* C;            // [M][N]
 };
 
-// Launch helpers implemented in the .cu files. Return cudaError_t as int.
+// Launch helpers implemented in the .cu files. Return cudaError_t as int.  regs_out, if
+// given, is int[2]: compiled registers per thread and local-memory (spill) bytes per thread.
 int launch_recurrent(int np, int bt, int g, int f16, const RecParams& p, int num_ctas,
                      size_t smem_bytes, void* stream, bool query_only, int* regs_out,
                      int* max_blocks_per_sm_out);

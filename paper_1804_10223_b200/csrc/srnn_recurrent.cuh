@@ -693,7 +693,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     const int e1 = tid, e1_b = tid % BT, e1_unit = u0 + tid / BT;
     const bool e1_ok = tid < n_items;
     const float* zs_e1 = zs + e1;
-    float* const y_e1 = (p.y != nullptr && e1_ok) ? p.y + static_cast<size_t>(e1_b) * H + e1_unit : nullptr;
+    float* const y_e1 = (p.y != nullptr && e1_ok) ? p.y + e1_b * p.y_bstride + e1_unit : nullptr;
     const bool row_leader = (lane & (L - 1)) == 0 && krow < G * U;
     if (tid == 0) *s_abort = 0;
 
@@ -948,7 +948,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                     h = activation<F16>(act, zs_e1[0] + bps[e1]);
                     const int bg = k * BT + e1_b;
                     if (bg < p.B) {
-                        if (y_e1 != nullptr) y_e1[(static_cast<size_t>(s - 1) * p.B + k * BT) * H] = h;
+                        if (y_e1 != nullptr) y_e1[(s - 1) * p.y_tstride + k * BT * p.y_bstride] = h;
                         if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + e1_unit] = h;
                     }
                 }
@@ -986,7 +986,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                         if (s == p.T && p.cT != nullptr && bg < p.B) p.cT[static_cast<size_t>(bg) * H + unit] = c;
                     }
                     if (bg < p.B) {
-                        if (p.y != nullptr) p.y[(static_cast<size_t>(s - 1) * p.B + bg) * H + unit] = h;
+                        if (p.y != nullptr) p.y[bg * p.y_bstride + (s - 1) * p.y_tstride + unit] = h;
                         if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + unit] = h;
                     }
                 }
@@ -1028,7 +1028,10 @@ static int launch_one(const RecParams& p, int num_ctas, size_t smem, void* strea
         cudaFuncAttributes attr;
         e = cudaFuncGetAttributes(&attr, fn);
         if (e != cudaSuccess) return static_cast<int>(e);
-        if (regs_out) *regs_out = attr.numRegs;
+        if (regs_out) {  // int[2]: registers per thread, local-memory (spill/stack) bytes per thread
+            regs_out[0] = attr.numRegs;
+            regs_out[1] = static_cast<int>(attr.localSizeBytes);
+        }
         if (max_blocks_out) {
             int nb = 0;
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, p.threads, smem);

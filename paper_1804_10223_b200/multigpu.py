@@ -55,8 +55,45 @@ def gather_batch(y_local, group=None, global_batch=None):
     return y
 
 
-def forward_partitioned(local_forward, x_global, group=None):
-    """Run `local_forward(x_shard) -> y_shard` on this rank's slice of x [T, B, I], all-gather y."""
+def gather_batch_major(y_local, group=None, global_batch=None, out=None):
+    """All-gather batch-major per-rank outputs [B_r, T, H] into the global [B, T, H].
+
+    With SRNN_FLAG_Y_BATCH_MAJOR every rank's y is one contiguous block of the global
+    batch-major y, so equal shards go straight into the collective's output buffer
+    (no permute, no staging copy -- ``out`` may be preallocated); unequal shards are
+    padded to the largest for the collective and compacted after.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    b_r, T, H = y_local.shape
+    if global_batch is not None and global_batch % world == 0 and b_r * world == global_batch:
+        if out is None:
+            out = torch.empty((global_batch, T, H), dtype=y_local.dtype, device=y_local.device)
+        if hasattr(dist, "all_gather_into_tensor") and y_local.is_cuda:
+            dist.all_gather_into_tensor(out, y_local.contiguous(), group=group)
+        else:
+            dist.all_gather(list(out.chunk(world)), y_local.contiguous(), group=group)
+        return out
+    sizes = torch.tensor([b_r], dtype=torch.int64, device=y_local.device)
+    all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
+    dist.all_gather(all_sizes, sizes, group=group)
+    all_sizes = [int(v.item()) for v in all_sizes]
+    bmax = max(all_sizes)
+    send = torch.zeros((bmax, T, H), dtype=y_local.dtype, device=y_local.device)
+    send[:b_r] = y_local
+    recv = torch.empty((world * bmax, T, H), dtype=y_local.dtype, device=y_local.device)
+    dist.all_gather(list(recv.chunk(world)), send, group=group)
+    y = torch.cat([recv[r * bmax:r * bmax + all_sizes[r]] for r in range(world)], 0)
+    if global_batch is not None and y.shape[0] != global_batch:
+        raise RuntimeError(f"gathered batch {y.shape[0]} != expected {global_batch}")
+    return y
+
+
+def forward_partitioned(local_forward, x_global, group=None, batch_major=False):
+    """Run `local_forward(x_shard) -> y_shard` on this rank's slice of x [T, B, I], all-gather y
+    ([T, B, H]; batch_major: local outputs and the result are [B_r, T, H] / [B, T, H])."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
@@ -64,6 +101,8 @@ def forward_partitioned(local_forward, x_global, group=None):
     T, B, _ = x_global.shape
     start, count = shard(B, world, rank)
     y_local = local_forward(x_global[:, start:start + count].contiguous())
+    if batch_major:  # local_forward returns [B_r, T, H] (SRNN_FLAG_Y_BATCH_MAJOR)
+        return gather_batch_major(y_local, group=group, global_batch=B)
     return gather_batch(y_local, group=group, global_batch=B)
 
 

@@ -22,6 +22,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 namespace cg = cooperative_groups;
@@ -127,6 +128,57 @@ __global__ void k_a2a_bulk(Args a) {
                         pend &= ~(1u << j);
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
+                    if (pend >> j & 1) v[j] = ld_relaxed_v2(src + base + j * blockDim.x);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// The product's exchange (srnn_recurrent.cuh, R16): every CTA publishes its
+// units' values as 16-bit words carrying the 1-bit step tag in the LSB (one relaxed store
+// per value), then a CTA barrier, then every thread polls K 16-byte chunks of the whole
+// image at once, re-polling stale ones, and stages them into shared memory; a second
+// barrier ends the step.  vals = units_per_cta * BT values per CTA.
+template <int K>
+__global__ void k_a2a_lsb(Args a) {
+    extern __shared__ __align__(16) unsigned char hs[];
+    const int n = gridDim.x;
+    const int vals = a.upc * a.wpu;  // wpu reused as values per unit (BT)
+    const int total = n * vals;      // 16-bit values per image
+    const int chunks = (total * 2 + 15) / 16;
+    unsigned short* img = reinterpret_cast<unsigned short*>(a.words);
+    for (int s = 1; s <= a.steps; ++s) {
+        unsigned short* dst = img + static_cast<size_t>(s & 1) * (chunks * 8);
+        const unsigned tag = (s >> 1) & 1u;
+        for (int i = threadIdx.x; i < vals; i += blockDim.x) {
+            const unsigned short v = static_cast<unsigned short>((0x3c00u + i) & ~1u) | tag;
+            asm volatile("st.relaxed.gpu.global.b16 [%0], %1;" ::"l"(dst + blockIdx.x * vals + i), "h"(v) : "memory");
+        }
+        if (blockIdx.x == n - 1)  // pad values of the last chunk
+            for (int i = total + threadIdx.x; i < chunks * 8; i += blockDim.x)
+                asm volatile("st.relaxed.gpu.global.b16 [%0], %1;" ::"l"(dst + i), "h"(static_cast<unsigned short>(tag)) : "memory");
+        __syncthreads();
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(dst);
+        const unsigned long long M = 0x0001000100010001ull, want = tag ? M : 0ull;
+        for (int base = threadIdx.x; base < chunks; base += K * blockDim.x) {
+            ulonglong2 v[K];
+            unsigned pend = 0;
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+                if (base + j * static_cast<int>(blockDim.x) < chunks) {
+                    v[j] = ld_relaxed_v2(src + base + j * blockDim.x);
+                    pend |= 1u << j;
+                }
+            while (pend) {
+#pragma unroll
+                for (int j = 0; j < K; ++j)
+                    if ((pend >> j & 1) && ((((v[j].x & M) ^ want) | ((v[j].y & M) ^ want)) == 0ull)) {
+                        *reinterpret_cast<ulonglong2*>(hs + 16 * (base + j * blockDim.x)) = v[j];
+                        pend &= ~(1u << j);
+                    }
+#pragma unroll
+                for (int j = 0; j < K; ++j)
                     if (pend >> j & 1) v[j] = ld_relaxed_v2(src + base + j * blockDim.x);
             }
         }
@@ -446,7 +498,42 @@ static float run(void* fn, Args a, int grid, int block) {
     return ms * 1000.0f / a.steps;
 }
 
+static float run_smem(void* fn, Args a, int grid, int block, size_t smem) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    void* args[] = {&a};
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(block), args, smem, nullptr);  // warm-up
+    cudaEventRecord(e0);
+    cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(block), args, smem, nullptr);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (cudaGetLastError() != cudaSuccess) return -1.f;
+    return 1000.f * ms / a.steps;
+}
+
 int main(int argc, char** argv) {
+    if (argc > 1 && std::string(argv[1]) == "--floor") {
+        // bench.py: the product-format exchange floor for H units x BT fp16 values on 148 CTAs
+        Args a;
+        const int H = argc > 2 ? atoi(argv[2]) : 2304, bt = argc > 3 ? atoi(argv[3]) : 4;
+        const int ncta = argc > 4 ? atoi(argv[4]) : 148, threads = argc > 5 ? atoi(argv[5]) : 512;
+        a.upc = (H + ncta - 1) / ncta;
+        a.wpu = bt;
+        a.steps = 4000;
+        a.delay_ns = 0;
+        const size_t img = static_cast<size_t>(ncta) * a.upc * bt * 2 + 16;
+        cudaMalloc(&a.words, 2 * img + 64);
+        cudaMemset(a.words, 0, 2 * img + 64);
+        cudaMalloc(&a.out, 64);
+        const float us = run_smem(reinterpret_cast<void*>(k_a2a_lsb<3>), a, ncta, threads, img + 64);
+        printf("{\"a2a_lsb_us_per_step\": %.4f, \"units_per_cta\": %d, \"bt\": %d, \"ctas\": %d, \"threads\": %d, "
+               "\"bytes_per_cta\": %zu}\n", us, a.upc, bt, ncta, threads, img - 16);
+        return us > 0 ? 0 : 1;
+    }
     Args a;
     a.upc = argc > 1 ? atoi(argv[1]) : 16;
     a.wpu = argc > 2 ? atoi(argv[2]) : 2;

@@ -42,7 +42,11 @@ def check(prob, prec, flags=0, **kw):
     assert err <= TOL[prec], (err, g["info"])
     assert errh <= TOL[prec]
     if prob["cell"] == "lstm":
-        assert np.abs(g["cT"].astype(np.float64) - o["cT"]).max() <= TOL[prec] * 2
+        # c is an unbounded running sum (c = f c + i g): its error scales with |c|, while
+        # h = o tanh(c) damps it (|tanh'| <= 1 and -> 0 where |c| is large), so the cell
+        # state is held to the north-star tolerance relative to max(1, |c|)
+        errc = np.abs(g["cT"].astype(np.float64) - o["cT"]) / np.maximum(1.0, np.abs(o["cT"]))
+        assert errc.max() <= TOL[prec], errc.max()
     return g, o, err
 
 
@@ -425,16 +429,20 @@ def test_stacked_chunked_wavefront(cuda_device, prec, cell):
         got = forward_stacked_chunked(steps, x, n)
         torch.cuda.synchronize()
         assert torch.equal(got, full), n
+    # each layer against the oracle on the input that layer actually received: layer 0 on
+    # x, layer 1 on the GPU's layer-0 output -- both at the north-star tolerance (layer 1's
+    # own error, not layer 0's error propagated through W_x)
+    y0 = forward_stacked_chunked(steps[:1], x, 1).cpu().numpy()
     for m in plans:
         m.status()
         m.close()
-    q0 = dict(p0)
-    o0 = oracle.forward(q0)
+    o0 = oracle.forward(dict(p0))
+    assert np.abs(y0.astype(np.float64) - o0["y"]).max() <= TOL[prec]
     q1 = dict(p1)
-    q1["x"] = o0["y"].astype(np.float32)
+    q1["x"] = y0.astype(np.float32)
     o1 = oracle.forward(q1)
     err = np.abs(full.cpu().numpy().astype(np.float64) - o1["y"]).max()
-    assert err <= 3 * TOL[prec], err
+    assert err <= TOL[prec], err
 
 
 @pytest.mark.parametrize("H,B,T,d", [
@@ -565,3 +573,165 @@ def test_tag_epoch_wrap(cuda_device, monkeypatch, prec):
         m.status()
         assert np.abs(y.cpu().numpy() - o["y"]).max() <= TOL[prec]
     m.close()
+
+
+# ---- round 2: the method's defining edge cases at the headline shape, NaN, full-T C5 ----
+
+def _oracle_samples(prob, samples, threads=None):
+    """Oracle outputs of selected batch samples (samples are independent, PAPER.md:43-49 per
+    sequence), run in parallel host threads (the oracle's C calls release the GIL)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(b):
+        q = dict(prob)
+        q["x"] = np.ascontiguousarray(prob["x"][:, b:b + 1])
+        q["B"] = 1
+        for k in ("h0", "c0"):
+            if prob.get(k) is not None:
+                q[k] = np.ascontiguousarray(prob[k][b:b + 1])
+        return b, oracle.forward(q)
+
+    with ThreadPoolExecutor(threads or max(1, os.cpu_count() or 1)) as ex:
+        return dict(ex.map(one, samples))
+
+
+@pytest.mark.parametrize("prec", ["fp16", "fp32"])
+@pytest.mark.parametrize("d", [0.0, 1.0])
+def test_C2_density_extremes(cuda_device, prec, d):
+    """C2 shape (H=2304, B=4, T=256) at density 0 (h_t = g(b'_t): no recurrent term,
+    PAPER.md:46 Eq. 2 with U_r = 0) and density 1 (the dense RNN the method reduces to,
+    PAPER.md:91/:100: padding and reordering do not change the result) through the
+    sparse kernel -- every output against the oracle.  A plan the chip cannot hold must
+    say so (SRNN_ERR_NOT_ON_CHIP), never fall back."""
+    from paper_1804_10223_b200 import SrnnError
+    cfg = {k: v for k, v in inputs.CONFIGS["C2"].items() if k != "prec"}
+    cfg["density"] = d
+    prob = inputs.make_problem(**cfg, h0="random")
+    try:
+        g, o, err = check(prob, prec)
+    except SrnnError as ex:
+        assert d == 1.0 and prec == "fp32" and ex.code == -2, ex
+        pytest.skip("fp32 pairs of a dense 2304 layer exceed the on-chip capacity (SRNN_ERR_NOT_ON_CHIP)")
+    if d == 0.0:
+        assert g["info"]["nnz"] == 0
+    print("C2 density", d, prec, "max-abs err", err, g["info"]["num_ctas"], g["info"]["batch_tile"])
+
+
+@pytest.mark.parametrize("cell,act,prec", [("rnn", "tanh", "fp16"), ("rnn", "tanh", "fp32"),
+                                           ("rnn", "relu", "fp16"), ("lstm", "tanh", "fp16")])
+def test_nan_propagates(cuda_device, cell, act, prec):
+    """A NaN in x (NaN inputs are propagated, not trapped): the poisoned
+    sample's outputs are NaN exactly where the oracle's are (from the poisoned step on,
+    every unit -- W_x is dense), the other samples are untouched and within tolerance.
+    ReLU absorbs NaN in both (g(NaN) = 0: u > 0 is false in the oracle, fmax in the kernel)."""
+    prob = inputs.make_problem(700, 700, 4, 12, 0.1, cell=cell, act=act, h0="random", c0="random")
+    prob["x"] = prob["x"].copy()
+    prob["x"][5, 2, 17] = np.nan
+    g = run_gpu(prob, prec)
+    o = oracle.forward(prob)
+    gy, oy = g["y"].astype(np.float64), o["y"]
+    assert np.array_equal(np.isnan(gy), np.isnan(oy))
+    if act != "relu" or cell == "lstm":
+        assert np.isnan(oy[5:, 2]).all() and not np.isnan(oy[:5]).any()
+    fin = ~np.isnan(oy)
+    assert np.abs(gy[fin] - oy[fin]).max() <= TOL[prec]
+    assert not np.isnan(gy[:, [0, 1, 3]]).any()
+
+
+def test_C5_full_T_sampled_per_shard(cuda_device):
+    """C5 (H=5760, d=10%, B=64, T=512, fp16) at its full length: the 8-way batch partition
+    of the bench (B/8 = 8 sequences per shard) is bit-identical to the full batch, and two
+    samples of every shard (its first and last) match the oracle over all 512 steps."""
+    import torch
+    from paper_1804_10223_b200.multigpu import shard
+    cfg = {k: v for k, v in inputs.CONFIGS["C5"].items() if k != "prec"}
+    prob = inputs.make_problem(**cfg)
+    m = from_problem(prob, prec="fp16")
+    x = torch.from_numpy(prob["x"]).cuda()
+    y, _ = m.forward(x)
+    torch.cuda.synchronize()
+    m.status()
+    samples = []
+    for r in range(8):
+        s0, c = shard(64, 8, r)
+        part = m.forward(x[:, s0:s0 + c].contiguous())[0]
+        torch.cuda.synchronize()
+        assert torch.equal(part, y[:, s0:s0 + c]), r
+        samples += [s0, s0 + c - 1]
+    yc = y.cpu().numpy().astype(np.float64)
+    for b, o in _oracle_samples(prob, samples).items():
+        err = np.abs(yc[:, b] - o["y"][:, 0]).max()
+        assert err <= TOL["fp16"], (b, err)
+
+
+def test_y_batch_major_layout(cuda_device):
+    """SRNN_FLAG_Y_BATCH_MAJOR writes y as [B][T][H]: the same bits as the default [T][B][H]
+    layout, transposed (ragged tiles included)."""
+    import torch
+    from paper_1804_10223_b200 import FLAG_Y_BATCH_MAJOR
+    prob = inputs.make_problem(777, 777, 11, 9, 0.1, act="tanh", h0="random")
+    x = torch.from_numpy(prob["x"]).cuda()
+    h0 = torch.from_numpy(prob["h0"]).cuda()
+    for prec in ("fp16", "fp32"):
+        a = from_problem(prob, prec=prec)
+        b = from_problem(prob, prec=prec, flags=FLAG_Y_BATCH_MAJOR)
+        ya, ha = a.forward(x, h0)
+        yb, hb = b.forward(x, h0)
+        torch.cuda.synchronize()
+        assert tuple(yb.shape) == (11, 9, 777)
+        assert torch.equal(ya.permute(1, 0, 2), yb) and torch.equal(ha, hb)
+        yh, _ = b.forward_host(prob["x"], prob["h0"])
+        assert np.array_equal(yh, yb.cpu().numpy())
+        a.close()
+        b.close()
+
+
+def test_plans_on_concurrent_host_threads(cuda_device):
+    """Distinct plans are independent (include/srnn.h): two host threads each drive their own
+    plan and stream at the same time (the per-launch shared-memory opt-in of the tcgen05
+    projection) and get the single-thread results bit for bit."""
+    import threading
+    import torch
+    probs = [inputs.make_problem(1152, 1152, 4, 20, 0.1, act="tanh", seed_offset=s) for s in (1, 2)]
+    ref = []
+    for p in probs:
+        m = from_problem(p, prec="fp16")
+        ref.append(m.forward(torch.from_numpy(p["x"]).cuda())[0].cpu())
+        m.close()
+    out = [None, None]
+
+    def run(i):
+        torch.cuda.set_device(0)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            m = from_problem(probs[i], prec="fp16")
+            for _ in range(3):
+                y = m.forward(torch.from_numpy(probs[i]["x"]).cuda(), stream=s)[0]
+            s.synchronize()
+            out[i] = y.cpu()
+            m.status()
+            m.close()
+
+    th = [threading.Thread(target=run, args=(i,)) for i in (0, 1)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for i in (0, 1):
+        assert torch.equal(out[i], ref[i])
+
+
+def test_plans_on_two_devices(cuda_device):
+    """One process, one plan per device (the per-device GEMM attribute)."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two visible GPUs (the round-end box has one)")
+    prob = inputs.make_problem(1152, 1152, 4, 16, 0.1, act="tanh")
+    ys = []
+    for dev in (0, 1):
+        m = from_problem(prob, prec="fp16", device=dev)
+        ys.append(m.forward(torch.from_numpy(prob["x"]).to(f"cuda:{dev}"))[0].cpu())
+        m.status()
+        m.close()
+    assert torch.equal(ys[0], ys[1])

@@ -121,3 +121,44 @@ def test_gloo_world2_layer_pipeline_equals_unchunked(tmp_path, cell, n_chunks):
         got = np.load(tmp_path / f"y{r}.npy")
         assert got.shape == ref.shape
         assert np.array_equal(got, ref)
+
+
+# ---- the C5 split (global batch 64 over ranks, batch-major y) ----
+
+def _c5_problem():
+    # C5's batch structure (B = 64, split evenly), small H / T so the CPU oracle stands in
+    # for each rank's local compute
+    return inputs.make_problem(40, 16, 64, 5, 0.1, act="relu")
+
+
+def _c5_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    prob = _c5_problem()
+    start, count = shard(64, world, rank)
+    assert count == 64 // world
+
+    def local_forward(x_shard):  # batch-major [B_r, T, H], like SRNN_FLAG_Y_BATCH_MAJOR
+        p = dict(prob)
+        p["x"] = x_shard.numpy()
+        p["B"] = x_shard.shape[1]
+        return torch.from_numpy(np.ascontiguousarray(oracle.forward(p)["y"].transpose(1, 0, 2)))
+
+    y = forward_partitioned(local_forward, torch.from_numpy(prob["x"]), batch_major=True)
+    np.save(os.path.join(out_dir, f"y{rank}.npy"), y.numpy())
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_c5_split_batch_major(tmp_path):
+    """B = 64 split 32 / 32 (the C5 shape at 2 GPUs): the batch-major all-gather of the
+    ranks' blocks is the global [B, T, H] y of the single-process run, bit for bit."""
+    port = _free_port()
+    mp.spawn(_c5_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    import oracle
+    ref = oracle.forward(_c5_problem())["y"].transpose(1, 0, 2)
+    for r in range(2):
+        got = np.load(tmp_path / f"y{r}.npy")
+        assert got.shape == ref.shape == (64, 5, 40)
+        assert np.array_equal(got, ref)
