@@ -114,6 +114,12 @@ typedef enum { SRNN_PREC_FP32 = 0, SRNN_PREC_FP16W_FP32ACC = 1 } srnn_prec_t;
                                               of the global [B][T][H] y, so an all-gather needs no
                                               re-layout.  srnn_forward / srnn_recurrence /
                                               srnn_forward_host (the latter unpipelined)         */
+#define SRNN_FLAG_CLASS_BALANCE  (1u << 12) /* class-based load balancing: hidden units are
+                                              bucketed into classes by their nonzero count and dealt
+                                              over the CTAs so every CTA gets the same class mix and
+                                              warps get rows of similar length; the exchange and hs
+                                              use the resulting unit order (results unchanged up to
+                                              fp reassociation)                                  */
 #define SRNN_FLAG_DENSE_TC       (1u << 8) /* comparator: the DENSE persistent
                                               RNN of PAPER.md:51-71 (Sec. 3.2, Diamos et al.)
                                               re-done for sm_100a tensor cores.  U_r is densified

@@ -33,6 +33,7 @@ FLAG_DENSE_TC = 1 << 8
 FLAG_DEBUG_DROP_PUBLISH = 1 << 9
 FLAG_FP32_TC_GEMM = 1 << 10
 FLAG_Y_BATCH_MAJOR = 1 << 11
+FLAG_CLASS_BALANCE = 1 << 12
 
 EXPORTED = ["srnn_plan_create", "srnn_plan_query", "srnn_load_weights", "srnn_forward", "srnn_input_projection",
             "srnn_recurrence", "srnn_forward_host", "srnn_plan_status", "srnn_plan_export_layout",

@@ -45,6 +45,9 @@ struct srnn_plan {
     // device buffers
     void* d_img = nullptr;          // uint2 (fp32) or uint32 (fp16) image
     int32_t* d_unit0 = nullptr;
+    int32_t* d_perm = nullptr;            // class balancing: unit of each exchange position
+    int32_t* d_piece0 = nullptr;          // class balancing: pieces of heavy rows (Layout::piece0)
+    std::vector<int32_t> unit_of_pos, pos_of_unit;  // chosen layout's permutation (empty = identity)
     int32_t* d_wslots = nullptr;
     float* d_wx = nullptr;
     // fp16 mode tensor-core GEMM: W_x and x rounded to fp16, K padded to a multiple of 8
@@ -116,9 +119,10 @@ int inst_for(int slots, bool f16, int bt) {
 
 int elem_bytes(bool f16, int bt) { return f16 ? 2 * bt : 4 * bt; }
 
-size_t smem_for(const srnn_plan* p, int units_max, int bt, int n_tiles) {
+size_t smem_for(const srnn_plan* p, int units_max, int bt, int n_tiles, int vrows = 0) {
     size_t s = (static_cast<size_t>(p->cfg.hidden) * elem_bytes(p->f16, bt) + 15) & ~static_cast<size_t>(15);
-    s += 3 * static_cast<size_t>(p->G) * units_max * bt * 4;  // zs + double-buffered b' staging
+    const size_t zrows = std::max<size_t>(static_cast<size_t>(p->G) * units_max, vrows);  // zs: (virtual) rows
+    s += zrows * bt * 4 + 2 * static_cast<size_t>(p->G) * units_max * bt * 4;  // zs + double-buffered b'
     if (p->G >= 3) s += static_cast<size_t>(n_tiles) * units_max * bt * 4;  // LSTM c / GRU fp32 h
     return s + 16;
 }
@@ -126,6 +130,8 @@ size_t smem_for(const srnn_plan* p, int units_max, int bt, int n_tiles) {
 void free_device(srnn_plan* p) {
     cudaFree(p->d_img);
     cudaFree(p->d_unit0);
+    cudaFree(p->d_perm);
+    cudaFree(p->d_piece0);
     cudaFree(p->d_wslots);
     cudaFree(p->d_wx);
     cudaFree(p->d_wx16);
@@ -592,9 +598,32 @@ search_again:
     const int P = p->E >= 4 ? 128 / p->E : 32;  // lanes per shared-memory phase
     const bool plan_log = std::getenv("SRNN_PLAN_LOG") != nullptr;  // diagnostics: every candidate to stderr
     // Evaluate one (CTAs, lanes per row, slot budget) candidate.
+    const bool class_balance = (p->cfg.flags & SRNN_FLAG_CLASS_BALANCE) != 0 && !in.naive;
+    if (class_balance) {  // heavy rows (> 1.25 x the mean length) are handled as several pieces
+        const double mean = static_cast<double>(nnz) / std::max(1, R);
+        in.piece_cap = std::max(32, static_cast<int>(std::ceil(1.25 * mean)));
+    }
+    std::vector<std::vector<int32_t>> perm_uop, perm_pou;  // per candidate CTA count
+    std::vector<int> perm_c;
+    auto use_perm = [&](int C) {
+        if (!class_balance) return;
+        size_t i = 0;
+        while (i < perm_c.size() && perm_c[i] != C) ++i;
+        if (i == perm_c.size()) {
+            perm_c.push_back(C);
+            perm_uop.emplace_back();
+            perm_pou.emplace_back();
+            class_balanced_units(in, C, 8, &perm_uop.back(), &perm_pou.back());
+        }
+        in.unit_of_pos = perm_uop[i].data();
+        in.pos_of_unit = perm_pou[i].data();
+    };
+    int best_perm_c = -1;
     auto try_layout = [&](int C, int L, int np, int reg_cap, int64_t ns_cap) {
         Layout lay;
+        use_perm(C);
         if (!pack_layout(in, C, L, np, &lay)) return;
+        if (lay.threads > 1024) return;
         const int su = std::max(1, lay.slots_used);
         int inst = inst_for(su, p->f16, p->BT);
         int ns = 0;
@@ -602,6 +631,15 @@ search_again:
             inst = reg_cap;
             ns = ((su - reg_cap) + 3) & ~3;
             if (ns > ns_cap) return;
+        }
+        if (lay.vrows_max > G * ((H + C - 1) / C)) {  // pieces: more zs rows (and maybe threads)
+            int um = 0;
+            for (int c = 0; c < C; ++c) um = std::max(um, lay.cta_unit0[c + 1] - lay.cta_unit0[c]);
+            if (lay.threads > max_threads_for(inst, p->f16, p->BT) ||
+                smem_for(p, um, p->BT, p->n_tiles_max, lay.vrows_max) + 16 +
+                        static_cast<size_t>(ns) * lay.threads * (p->f16 ? 4 : 8) >
+                    static_cast<size_t>(p->smem_optin))
+                return;
         }
         double cst = cost_model(lay, p->BT, H, p->n_tiles_max, p->f16, inst);
         if (ns > 0) cst += static_cast<double>(ns) * lay.warps * 2.0;  // weight LDS + issue per smem slot
@@ -615,6 +653,7 @@ search_again:
             best = std::move(lay);
             best_inst = inst;
             best_ns = ns;
+            best_perm_c = C;
             any = true;
         }
     };
@@ -700,7 +739,7 @@ search_again:
     }
     int umax = 0;
     for (int c = 0; c < fin.num_ctas; ++c) umax = std::max(umax, fin.cta_unit0[c + 1] - fin.cta_unit0[c]);
-    p->smem_bytes = smem_for(p, umax, p->BT, p->n_tiles_max) + 16 +
+    p->smem_bytes = smem_for(p, umax, p->BT, p->n_tiles_max, fin.vrows_max) + 16 +
                     static_cast<size_t>(best_ns) * fin.threads * pair_bytes;
     p->np_inst = best_inst;
     // A plan whose threads own more exchange chunks than the default instance polls at once
@@ -711,6 +750,15 @@ search_again:
         const int64_t chunks = exchange_tile_bytes(H, p->f16, p->BT) / 16;  // 16-byte chunks per tile
         const int64_t c = (chunks + best.threads - 1) / best.threads;       // per thread
         p->k8 = k8_compiled(best_inst, p->f16, p->BT) && ksmall < 8 && (c + 7) / 8 < (c + ksmall - 1) / ksmall;
+    }
+    p->unit_of_pos.clear();
+    p->pos_of_unit.clear();
+    if (class_balance) {
+        for (size_t i = 0; i < perm_c.size(); ++i)
+            if (perm_c[i] == best_perm_c) {
+                p->unit_of_pos = perm_uop[i];
+                p->pos_of_unit = perm_pou[i];
+            }
     }
     p->model_cost = best_cost;
     p->ns_slots = best_ns;
@@ -739,22 +787,40 @@ search_again:
             std::vector<uint4>().swap(p->dense_img);
         } else if (p->f16) {
             std::vector<uint32_t> img(n);
-            for (size_t i = 0; i < n; ++i)
-                img[i] = (static_cast<uint32_t>(p->BT >= 8 ? l.col[i] : l.col[i] * p->E) << 16) |
-                         float_to_half_rne(l.val[i]);
+            const bool perm = !p->pos_of_unit.empty();
+            for (size_t i = 0; i < n; ++i) {
+                const int32_t pos = perm ? p->pos_of_unit[l.col[i]] : l.col[i];  // hs position of the column
+                img[i] = (static_cast<uint32_t>(p->BT >= 8 ? pos : pos * p->E) << 16) | float_to_half_rne(l.val[i]);
+            }
             e = cudaMalloc(&p->d_img, n * 4);
             if (e == cudaSuccess) e = cudaMemcpy(p->d_img, img.data(), n * 4, cudaMemcpyHostToDevice);
         } else {
             std::vector<uint2> img(n);
+            const bool perm = !p->pos_of_unit.empty();
             for (size_t i = 0; i < n; ++i) {
                 uint32_t b;
                 std::memcpy(&b, &l.val[i], 4);
-                img[i] = make_uint2(static_cast<uint32_t>(l.col[i] * p->E), b);
+                const int32_t pos = perm ? p->pos_of_unit[l.col[i]] : l.col[i];
+                img[i] = make_uint2(static_cast<uint32_t>(pos * p->E), b);
             }
             e = cudaMalloc(&p->d_img, n * 8);
             if (e == cudaSuccess) e = cudaMemcpy(p->d_img, img.data(), n * 8, cudaMemcpyHostToDevice);
         }
         const size_t wx_n = static_cast<size_t>(R) * p->cfg.input;
+        cudaFree(p->d_perm);
+        cudaFree(p->d_piece0);
+        p->d_perm = nullptr;
+        p->d_piece0 = nullptr;
+        if (e == cudaSuccess && !l.piece0.empty()) {
+            e = cudaMalloc(&p->d_piece0, l.piece0.size() * 4);
+            if (e == cudaSuccess)
+                e = cudaMemcpy(p->d_piece0, l.piece0.data(), l.piece0.size() * 4, cudaMemcpyHostToDevice);
+        }
+        if (e == cudaSuccess && !p->unit_of_pos.empty()) {
+            e = cudaMalloc(&p->d_perm, p->unit_of_pos.size() * 4);
+            if (e == cudaSuccess)
+                e = cudaMemcpy(p->d_perm, p->unit_of_pos.data(), p->unit_of_pos.size() * 4, cudaMemcpyHostToDevice);
+        }
         if (e == cudaSuccess) e = cudaMalloc(&p->d_unit0, l.cta_unit0.size() * 4);
         if (e == cudaSuccess) e = cudaMemcpy(p->d_unit0, l.cta_unit0.data(), l.cta_unit0.size() * 4, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMalloc(&p->d_wslots, l.warp_slots.size() * 4);
@@ -941,6 +1007,9 @@ static srnn_status_t recurrence_impl(srnn_plan_t p, int32_t T, int32_t B, const 
     else
         rp.img_f32 = static_cast<const uint2*>(p->d_img);
     rp.cta_unit0 = p->d_unit0;
+    rp.unit_perm = p->dense ? nullptr : p->d_perm;
+    rp.piece0 = p->dense ? nullptr : p->d_piece0;
+    rp.vrows_max = p->lay.vrows_max;
     rp.warp_slots = p->d_wslots;
     rp.bprime = bprime;
     rp.h0 = h0;

@@ -35,7 +35,10 @@ struct RecParams {
     // packed weights: [cta][slot][thread]
     const uint2* img_f32;      // fp32 mode: {hs byte offset, float bits}
     const uint32_t* img_f16;   // fp16 mode: (hs byte offset << 16) | half bits
-    const int32_t* cta_unit0;  // [num_ctas + 1] first unit of each CTA
+    const int32_t* cta_unit0;  // [num_ctas + 1] first exchange position of each CTA
+    const int32_t* unit_perm;  // [H] hidden unit at each exchange position (class balancing), or null = identity
+    const int32_t* piece0;     // [cta][G*units_max + 1] first virtual row of each local row (split heavy rows), or null
+    int32_t vrows_max;         // virtual rows of the largest CTA (zs rows)
     const int32_t* warp_slots; // [num_ctas][warps] slots used by each warp (warp-uniform)
     // data
     const float* bprime;  // [T][B][G*H]

@@ -90,7 +90,10 @@ float half_to_float(uint16_t h) {
 
 namespace {
 
-inline int32_t global_row(int k, int U, int u0, int H) { return (k / U) * H + u0 + (k % U); }
+inline int32_t global_row(int k, int U, int u0, int H, const int32_t* unit_of_pos) {
+    const int pos = u0 + (k % U);
+    return (k / U) * H + (unit_of_pos ? unit_of_pos[pos] : pos);
+}
 
 struct RowState {
     int32_t grow = -1;                       // global row
@@ -105,6 +108,7 @@ struct RowState {
 int min_np(const PackInput& in, int L) {
     int64_t mx = 0;
     for (int r = 0; r < in.G * in.H; ++r) mx = std::max<int64_t>(mx, in.rowptr[r + 1] - in.rowptr[r]);
+    if (in.piece_cap > 0) mx = std::min<int64_t>(mx, in.piece_cap);  // longer rows are split into pieces
     return static_cast<int>((mx + L - 1) / L);
 }
 
@@ -117,7 +121,11 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
     const int E = in.E;
     const int P = E >= 4 ? 128 / E : 32;
     const int ng = 32 / P;  // phase groups per warp instruction
-    auto key = [E](int32_t c) { return E >= 4 ? c : (c >> 1); };
+    const int32_t* pos_of = in.pos_of_unit;  // bank model on hs positions (class balancing permutes them)
+    auto key = [E, pos_of](int32_t c) {
+        const int32_t q = pos_of ? pos_of[c] : c;
+        return E >= 4 ? q : (q >> 1);
+    };
     const int rpw = 32 / L;
     Layout& lay = *out;
     lay = Layout();
@@ -128,8 +136,32 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
     int umax = 0;
     for (int c = 0; c <= C; ++c) lay.cta_unit0[c] = static_cast<int32_t>((static_cast<int64_t>(c) * H) / C);
     for (int c = 0; c < C; ++c) umax = std::max(umax, lay.cta_unit0[c + 1] - lay.cta_unit0[c]);
-    const int rows_max = G * umax;
+    // virtual rows: pieces of rows longer than piece_cap (contiguous CSR sub-ranges)
+    struct VRow {
+        int32_t grow;
+        int64_t b, e;
+    };
+    auto pieces_of = [&](int64_t len) -> int64_t {
+        return (in.piece_cap > 0 && len > in.piece_cap) ? (len + in.piece_cap - 1) / in.piece_cap : 1;
+    };
+    int vmax = 0;
+    bool split = false;
+    for (int c = 0; c < C; ++c) {
+        const int u0 = lay.cta_unit0[c], U = lay.cta_unit0[c + 1] - u0;
+        int v = 0;
+        for (int k = 0; k < G * U; ++k) {
+            const int32_t gr = global_row(k, U, u0, H, in.unit_of_pos);
+            const int64_t np = pieces_of(in.rowptr[gr + 1] - in.rowptr[gr]);
+            split |= np > 1;
+            v += static_cast<int>(np);
+        }
+        vmax = std::max(vmax, v);
+    }
+    lay.vrows_max = vmax;
+    const int rows_max = vmax;
     lay.warps = std::max(1, (rows_max + rpw - 1) / rpw);
+    if (split) lay.piece0.assign(static_cast<size_t>(C) * (G * umax + 1), 0);
+    std::vector<VRow> vrows;
     lay.threads = lay.warps * 32;
     const size_t n_img = static_cast<size_t>(C) * NP * lay.threads;
     lay.col.assign(n_img, 0);
@@ -143,7 +175,16 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
     for (int c = 0; c < C; ++c) {
         const int u0 = lay.cta_unit0[c];
         const int U = lay.cta_unit0[c + 1] - u0;
-        const int n_rows = G * U;
+        vrows.clear();
+        for (int k = 0; k < G * U; ++k) {
+            const int32_t gr = global_row(k, U, u0, H, in.unit_of_pos);
+            const int64_t b0 = in.rowptr[gr], len = in.rowptr[gr + 1] - b0, np = pieces_of(len);
+            if (!lay.piece0.empty()) lay.piece0[static_cast<size_t>(c) * (G * umax + 1) + k] = static_cast<int32_t>(vrows.size());
+            for (int64_t j = 0; j < np; ++j) vrows.push_back({gr, b0 + (len * j) / np, b0 + (len * (j + 1)) / np});
+        }
+        const int n_rows = static_cast<int>(vrows.size());
+        if (!lay.piece0.empty())
+            for (int k = G * U; k <= G * umax; ++k) lay.piece0[static_cast<size_t>(c) * (G * umax + 1) + k] = n_rows;
         int64_t wf_cta = 0, issue_cta = 0, pairs_cta = 0, conf_cta = 0;
         for (int w = 0; w < lay.warps; ++w) {
             const int k0 = w * rpw;
@@ -156,8 +197,8 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
                 rs.bucket.assign(P, {});
                 rs.head.assign(P, 0);
                 if (q >= nr) continue;
-                rs.grow = global_row(k0 + q, U, u0, H);
-                const int64_t b = in.rowptr[rs.grow], e = in.rowptr[rs.grow + 1];
+                rs.grow = vrows[k0 + q].grow;
+                const int64_t b = vrows[k0 + q].b, e = vrows[k0 + q].e;
                 rs.remaining = e - b;
                 pairs_cta += e - b;
                 if (e - b > static_cast<int64_t>(L) * NP) return false;
@@ -192,7 +233,7 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
                             const int q = lane / L;
                             if (q >= nr) continue;
                             const int64_t k = static_cast<int64_t>(i) * L + (lane - rows[q].lane0);
-                            const int64_t b = in.rowptr[rows[q].grow], e = in.rowptr[rows[q].grow + 1];
+                            const int64_t b = vrows[k0 + q].b, e = vrows[k0 + q].e;
                             if (b + k < e) {
                                 place(q, lane, b + k);
                                 lane_used[lane - gl0] = 1;
@@ -300,6 +341,49 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
         lay.issue_max_cta = std::max(lay.issue_max_cta, issue_cta);
     }
     return true;
+}
+
+void class_balanced_units(const PackInput& in, int C, int classes, std::vector<int32_t>* unit_of_pos,
+                          std::vector<int32_t>* pos_of_unit) {
+    const int H = in.H, G = in.G;
+    std::vector<int64_t> len(H, 0);
+    for (int u = 0; u < H; ++u)
+        for (int q = 0; q < G; ++q) len[u] += in.rowptr[q * H + u + 1] - in.rowptr[q * H + u];
+    std::vector<int32_t> order(H);
+    for (int u = 0; u < H; ++u) order[u] = u;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return len[a] > len[b]; });
+    classes = std::max(1, std::min(classes, H));
+    std::vector<int32_t> cap(C), load_units(C, 0), cls_of(H);
+    std::vector<int64_t> load(C, 0);
+    for (int c = 0; c < C; ++c)
+        cap[c] = static_cast<int32_t>((static_cast<int64_t>(c + 1) * H) / C - (static_cast<int64_t>(c) * H) / C);
+    std::vector<std::vector<int32_t>> members(C);
+    for (int k = 0; k < classes; ++k) {
+        const int i0 = static_cast<int>((static_cast<int64_t>(k) * H) / classes);
+        const int i1 = static_cast<int>((static_cast<int64_t>(k + 1) * H) / classes);
+        for (int i = i0; i < i1; ++i) {  // heaviest first: least-loaded CTA with room
+            const int32_t u = order[i];
+            cls_of[u] = k;
+            int best = -1;
+            for (int c = 0; c < C; ++c)
+                if (load_units[c] < cap[c] && (best < 0 || load[c] < load[best])) best = c;
+            members[best].push_back(u);
+            load[best] += len[u];
+            ++load_units[best];
+        }
+    }
+    unit_of_pos->assign(H, 0);
+    pos_of_unit->assign(H, 0);
+    int pos = 0;
+    for (int c = 0; c < C; ++c) {
+        std::stable_sort(members[c].begin(), members[c].end(),
+                         [&](int32_t a, int32_t b) { return cls_of[a] < cls_of[b]; });
+        for (int32_t u : members[c]) {
+            (*unit_of_pos)[pos] = u;
+            (*pos_of_unit)[u] = pos;
+            ++pos;
+        }
+    }
 }
 
 }  // namespace srnn

@@ -15,7 +15,25 @@ struct PackInput {
     int32_t BT = 4;                   // batch tile (samples per staged h row)
     int32_t E = 16;                   // bytes per staged h row (4*BT fp32, 2*BT fp16): one LDS per pair
     bool naive = false;               // CSR-order lane-strided layout (PAPER.md:91 baseline)
+    // Unit permutation (class-based load balancing): exchange/hs position i holds
+    // unit unit_of_pos[i]; CTA c owns positions [cta_unit0[c], cta_unit0[c+1]).  nullptr = identity.
+    const int32_t* unit_of_pos = nullptr;
+    const int32_t* pos_of_unit = nullptr;  // inverse (column -> hs position)
+    // Rows longer than piece_cap nonzeros are split into near-equal pieces ("virtual rows")
+    // packed like rows; the epilogue sums a row's pieces (class-based balancing of heavy
+    // rows).  0 = never split.
+    int32_t piece_cap = 0;
 };
+
+// Class-based assignment of units to CTAs ("define a number of classes for
+// different amounts of sparsity and handle each class separately, assigning each row to one
+// class or another based on its sparsity"): units are bucketed into `classes` quantile classes
+// of their nonzero count (all G gate rows), every class is dealt over the C CTAs heaviest-first
+// to the least-loaded CTA with room (equal unit counts per CTA as before), and inside a CTA
+// units are ordered by class so a warp's rows have similar lengths.  Writes unit_of_pos /
+// pos_of_unit (size H).
+void class_balanced_units(const PackInput& in, int C, int classes, std::vector<int32_t>* unit_of_pos,
+                          std::vector<int32_t>* pos_of_unit);
 
 struct Layout {
     int32_t num_ctas = 0, lanes_per_row = 0, threads = 0, warps = 0;
@@ -32,6 +50,10 @@ struct Layout {
     int64_t conflicts_max_cta = 0;     // sum over (slot, phase) of (wavefronts - 1) in that CTA
     int64_t issue_max_cta = 0;         // warp-slot instructions of the busiest CTA
     int64_t slots_total = 0;
+    // pieces (PackInput::piece_cap): per CTA the first virtual row of each local row k
+    // (k = gate * U + unit, G*units_max + 1 entries per CTA, prefix sums); empty = no split
+    std::vector<int32_t> piece0;
+    int32_t vrows_max = 0;  // virtual rows of the largest CTA (= G * units when nothing splits)
     size_t idx(int c, int i, int t) const {
         return (static_cast<size_t>(c) * np_budget + i) * threads + t;
     }

@@ -639,7 +639,10 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     unsigned char* hs = smem;
     const size_t hs_bytes = DENSE ? static_cast<size_t>(p.hs_rows) * 16 : static_cast<size_t>(H) * F::E;
     float* zs = reinterpret_cast<float*>(smem + ((hs_bytes + 15) & ~static_cast<size_t>(15)));
-    float* bpsb = zs + G * umax_bt;                          // b' double buffer: [2][item][G]
+    // zs: one BT-row of reduced sums per (virtual) row -- heavy rows split into pieces
+    // (class balancing) have several, summed in the epilogue
+    const int zrows = max(G * p.units_max, p.vrows_max);
+    float* bpsb = zs + zrows * BT;                           // b' double buffer: [2][item][G]
     float* cs = bpsb + 2 * G * umax_bt;                      // LSTM c / GRU fp32 h_{t-1}: [n_tiles][item]
     int* s_abort = reinterpret_cast<int*>(cs + (G >= 3 ? p.n_tiles * umax_bt : 0));
     unsigned char* ws = reinterpret_cast<unsigned char*>(
@@ -688,13 +691,25 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     const int lg_l = __ffs(L) - 1;  // L is a power of two: shifts, no per-step integer division
     const int krow = (warp << (5 - lg_l)) + (lane >> lg_l);  // local row of this lane
     // lane of the row that stores sample sbase (L >= BT), hoisted out of the time loop
-    const bool zs_writer = (lane & (L - 1)) < BT && krow < G * U;
+    const int* pc = p.piece0 != nullptr ? p.piece0 + cta * (G * p.units_max + 1) : nullptr;
+    const int n_vrows = pc != nullptr ? __ldg(pc + G * U) : G * U;  // (virtual) rows of this CTA
+    const bool zs_writer = (lane & (L - 1)) < BT && krow < n_vrows;
+    // reduced sum of local row k (gate * U + unit), sample b: the sum of its pieces
+    auto zval = [&](int k, int b) -> float {
+        if (pc == nullptr) return zs[k * BT + b];
+        const int v1 = __ldg(pc + k + 1);
+        float z = 0.0f;
+        for (int v = __ldg(pc + k); v < v1; ++v) z += zs[v * BT + b];
+        return z;
+    };
     // epilogue fast path (one item per thread): item e1 = tid -> (unit, sample)
-    const int e1 = tid, e1_b = tid % BT, e1_unit = u0 + tid / BT;
+    // exchange positions vs hidden units: the same unless the plan balances classes (unit_perm)
+    auto real_unit = [&](int pos) { return p.unit_perm != nullptr ? __ldg(p.unit_perm + pos) : pos; };
+    const int e1 = tid, e1_b = tid % BT, e1_unit = (tid < U * BT) ? real_unit(u0 + tid / BT) : 0;
     const bool e1_ok = tid < n_items;
     const float* zs_e1 = zs + e1;
     float* const y_e1 = (p.y != nullptr && e1_ok) ? p.y + e1_b * p.y_bstride + e1_unit : nullptr;
-    const bool row_leader = (lane & (L - 1)) == 0 && krow < G * U;
+    const bool row_leader = (lane & (L - 1)) == 0 && krow < n_vrows;
     if (tid == 0) *s_abort = 0;
 
     // Publish item e's h of (step s, tile k) into the exchange image of parity
@@ -747,7 +762,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
         for (int j = 0; j < item_rounds; ++j) {
             const int e = tid + j * nt;
             const bool ok = e < n_items;
-            const int unit = u0 + e / BT, bg = k * BT + e % BT;
+            const int unit = ok ? real_unit(u0 + e / BT) : 0, bg = k * BT + e % BT;
             float h = 0.0f;
             if (ok) {
                 h = (p.h0 != nullptr && bg < p.B) ? p.h0[static_cast<size_t>(bg) * H + unit] : 0.0f;
@@ -796,7 +811,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
         for (int j = 0; j < item_rounds; ++j) {
             const int e = tid + j * nt;
             if (e < n_items) {
-                const int unit = u0 + e / BT, bg = k * BT + e % BT;
+                const int unit = real_unit(u0 + e / BT), bg = k * BT + e % BT;
 #pragma unroll
                 for (int q = 0; q < G; ++q) {
                     if (bg < p.B)
@@ -945,7 +960,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                 // fast path (one item per thread, RNN): addresses hoisted out of the time loop
                 float h = 0.0f;
                 if (e1_ok) {
-                    h = activation<F16>(act, zs_e1[0] + bps[e1]);
+                    h = activation<F16>(act, (pc == nullptr ? zs_e1[0] : zval(e1 / BT, e1_b)) + bps[e1]);
                     const int bg = k * BT + e1_b;
                     if (bg < p.B) {
                         if (y_e1 != nullptr) y_e1[(s - 1) * p.y_tstride + k * BT * p.y_bstride] = h;
@@ -959,26 +974,24 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                 const bool ok = e < n_items;
                 float h = 0.0f;
                 if (ok) {
-                    const int unit = u0 + e / BT, bg = k * BT + e % BT;
+                    const int unit = real_unit(u0 + e / BT), bg = k * BT + e % BT;
                     if (G == 1) {
-                        h = activation<F16>(p.act, zs[e] + bps[e]);
+                        h = activation<F16>(p.act, zval(e / BT, e % BT) + bps[e]);
                     } else if (G == 3) {
                         // GRU (R15): r, z from the product; the reset gate scales the
                         // n-gate product + b_hn; the previous h of this item stays in fp32 in cs
-                        const int ub = U * BT;
-                        const float r = sigmoid_g<F16>(zs[0 * ub + e] + bps[e * G + 0]);
-                        const float u = sigmoid_g<F16>(zs[1 * ub + e] + bps[e * G + 1 % G]);
+                        const float r = sigmoid_g<F16>(zval(0 * U + e / BT, e % BT) + bps[e * G + 0]);
+                        const float u = sigmoid_g<F16>(zval(1 * U + e / BT, e % BT) + bps[e * G + 1 % G]);
                         const float bhn = p.bias_hn != nullptr ? p.bias_hn[unit] : 0.0f;
-                        const float n = tanh_g<F16>(fmaf(r, zs[2 * ub + e] + bhn, bps[e * G + 2 % G]));
+                        const float n = tanh_g<F16>(fmaf(r, zval(2 * U + e / BT, e % BT) + bhn, bps[e * G + 2 % G]));
                         float* hp = &cs[k * umax_bt + e];
                         h = fmaf(u, *hp - n, n);  // (1 - u) n + u h_prev
                         *hp = h;
                     } else {
-                        const int ub = U * BT;
-                        const float zi = zs[0 * ub + e] + bps[e * G + 0];
-                        const float zf = zs[1 * ub + e] + bps[e * G + 1 % G];
-                        const float zg = zs[2 * ub + e] + bps[e * G + 2 % G];
-                        const float zo = zs[3 * ub + e] + bps[e * G + 3 % G];
+                        const float zi = zval(0 * U + e / BT, e % BT) + bps[e * G + 0];
+                        const float zf = zval(1 * U + e / BT, e % BT) + bps[e * G + 1 % G];
+                        const float zg = zval(2 * U + e / BT, e % BT) + bps[e * G + 2 % G];
+                        const float zo = zval(3 * U + e / BT, e % BT) + bps[e * G + 3 % G];
                         float* cp = &cs[k * umax_bt + e];
                         const float c = sigmoid_g<F16>(zf) * (*cp) + sigmoid_g<F16>(zi) * tanh_g<F16>(zg);
                         *cp = c;

@@ -58,6 +58,21 @@ def sparse_pattern(R, H, density, pattern="unstructured", seed_offset=0):
         for r in range(R):
             col[r * k:(r + 1) * k] = np.sort(rng.choice(H, size=k, replace=False))
         counts = np.full(R, k, dtype=np.int64)
+    elif pattern == "skewed":
+        # non-uniform row sparsity (the load-imbalance case of PAPER.md:91/:188): row lengths
+        # proportional to lognormal(0, 0.5) draws, scaled to nnz = round(d * R * H), <= H each
+        nnz = int(round(density * R * H))
+        wts = rng.lognormal(0.0, 0.5, size=R)
+        counts = np.minimum(np.floor(wts / wts.sum() * nnz).astype(np.int64), H)
+        short = nnz - int(counts.sum())
+        for r in np.argsort(-wts):
+            if short <= 0:
+                break
+            if counts[r] < H:
+                counts[r] += 1
+                short -= 1
+        col = np.concatenate([np.sort(rng.choice(H, size=int(k), replace=False)) if k else np.zeros(0, np.int64)
+                              for k in counts]).astype(np.int32)
     else:
         raise ValueError(f"unknown pattern {pattern!r}")
     rowptr = np.zeros(R + 1, dtype=np.int64)

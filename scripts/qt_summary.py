@@ -11,7 +11,7 @@ for fn in sys.argv[1:]:
                 print("  !", line.rstrip()[:200])
             continue
         c = d["cfg"]
-        key = f"H={c['H']} B={c['B']} d={c['d']} {c['prec']} {c.get('cell','rnn')} flags={c.get('flags',0)}"
+        key = f"H={c['H']} B={c['B']} d={c['d']} {c['prec']} {c.get('cell','rnn')} {c.get('pattern','')} flags={c.get('flags',0)}"
         if "us_per_step" in d:
             print(f"{key:55s} us/step {d['us_per_step']:.3f} fwd {d['fwd_ms']:.3f} ms gemm {d['gemm_ms']*1e3:.1f} us")
         else:

@@ -243,3 +243,33 @@ def test_gru_plan_host_only_and_dense_unsupported():
     with pytest.raises(SrnnError) as e:
         SparseRNN(96, 16, 4, 3, 0.2, cell="gru", prec="fp16", flags=FLAG_HOST_ONLY | FLAG_DENSE_TC)
     assert e.value.code == -7
+
+
+# ---- class-based load balancing ----
+
+@pytest.mark.parametrize("pattern,cell,prec", [("skewed", "rnn", "fp16"), ("unstructured", "lstm", "fp32"),
+                                               ("skewed", "gru", "fp16")])
+def test_class_balance_layout_reconstructs_and_balances(pattern, cell, prec):
+    """SRNN_FLAG_CLASS_BALANCE permutes hidden units over the CTAs by nonzero class: the
+    packed layout still reconstructs U_r exactly (every pair once, real rows / columns), and
+    the busiest CTA's pairs drop toward the mean on non-uniform rows."""
+    from paper_1804_10223_b200 import FLAG_CLASS_BALANCE
+    prob = inputs.make_problem(600, 600, 4, 4, 0.08, cell=cell, pattern=pattern)
+    plain = host_plan(prob, prec, num_ctas=148)
+    bal = host_plan(prob, prec, num_ctas=148, flags=FLAG_CLASS_BALANCE)
+    for m in (plain, bal):
+        dense, cnt, _ = reconstruct(m, prob)
+        ref = csr_dense(prob, np.asarray(prob["val"], np.float32).astype(np.float16).astype(np.float64)
+                        if prec == "fp16" else None)
+        assert np.array_equal(dense, ref)
+        assert cnt.max() <= 1
+    _, _, (col, val, row) = reconstruct(plain, prob)
+    _, _, (colb, valb, rowb) = reconstruct(bal, prob)
+
+    def max_cta_pairs(row, val):
+        return int(((row >= 0) & (val != 0)).reshape(148, -1).sum(1).max())
+
+    mean = prob["nnz"] / 148
+    assert max_cta_pairs(rowb, valb) <= max_cta_pairs(row, val)
+    if pattern == "skewed":
+        assert max_cta_pairs(rowb, valb) - mean < 0.5 * (max_cta_pairs(row, val) - mean)

@@ -735,3 +735,25 @@ def test_plans_on_two_devices(cuda_device):
         m.status()
         m.close()
     assert torch.equal(ys[0], ys[1])
+
+
+@pytest.mark.parametrize("prec,cell,pattern,B", [("fp16", "rnn", "skewed", 4), ("fp32", "rnn", "skewed", 3),
+                                                 ("fp16", "lstm", "skewed", 4), ("fp16", "gru", "unstructured", 5),
+                                                 ("fp16", "rnn", "skewed", 16)])
+def test_class_balance_parity(cuda_device, prec, cell, pattern, B):
+    """SRNN_FLAG_CLASS_BALANCE: units dealt over the CTAs by nonzero class, the
+    exchange in the permuted order, outputs back in unit order -- every output vs the oracle."""
+    from paper_1804_10223_b200 import FLAG_CLASS_BALANCE
+    prob = inputs.make_problem(1000, 600, B, 12, 0.1, cell=cell, act="tanh", pattern=pattern, h0="random",
+                               c0="random", seed_offset=B)
+    check(prob, prec, flags=FLAG_CLASS_BALANCE)
+
+
+def test_class_balance_integer_exact(cuda_device):
+    """Integer-exact inputs: any summation order is exact, so the permuted plan equals the
+    oracle (and the unpermuted plan) bit for bit."""
+    from paper_1804_10223_b200 import FLAG_CLASS_BALANCE
+    prob = inputs.make_integer_problem(200, 48, 4, 5, 0.02, act="identity")
+    o = oracle.forward(prob)
+    a = run_gpu(prob, "fp32", flags=FLAG_CLASS_BALANCE)
+    assert np.array_equal(a["y"].astype(np.float64), o["y"])
