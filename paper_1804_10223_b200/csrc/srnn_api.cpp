@@ -94,6 +94,7 @@ struct srnn_plan {
     int dense_mt = 0, dense_kpw = 0, dense_nf = 0, dense_inst = 0, hs_rows = 0;
     std::vector<uint4> dense_img;  // host image [cta][frag][thread] (freed after upload)
     bool k8 = false;               // sparse fp16 tile-of-4 plan that needs 8 poll slots per thread
+    std::vector<std::pair<int, bool>> spill_cache;  // (instance key, spills?) of queried instances
 };
 
 namespace {
@@ -453,8 +454,9 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     // (H * E <= 65536), 16-byte units for BT = 8 (the column index, any H)
     const int umax_guess = (c.hidden + p->sm_count - 1) / p->sm_count;
     while (bt > 1 && smem_for(p, umax_guess, bt, (c.batch + bt - 1) / bt) > static_cast<size_t>(p->smem_optin)) bt /= 2;
-    while (p->f16 && bt > 1 && bt < 8 && static_cast<int64_t>(c.hidden) * elem_bytes(true, bt) > 65536) bt /= 2;
-    if (p->f16 && bt < 8 && static_cast<int64_t>(c.hidden) * elem_bytes(true, bt) > 65536) {
+    // register pairs carry 16-bit hs byte offsets (fp16 tiles <= 4 and fp32): hs <= 64 KB
+    while (bt > 1 && (!p->f16 || bt < 8) && static_cast<int64_t>(c.hidden) * elem_bytes(p->f16, bt) > 65536) bt /= 2;
+    if ((!p->f16 || bt < 8) && static_cast<int64_t>(c.hidden) * elem_bytes(p->f16, bt) > 65536) {
         delete p;
         return SRNN_ERR_UNSUPPORTED;
     }
@@ -571,6 +573,7 @@ srnn_status_t srnn_load_weights(srnn_plan_t p, const int32_t* rowptr, const int3
         p->nnz = nnz;
     } else {
     // ---- search (num_ctas, lanes_per_row, slot budget) ----
+    bool spill_strict = true;
 search_again:
     std::vector<int> cands_c;
     if (p->cfg.num_ctas > 0) {
@@ -619,6 +622,23 @@ search_again:
         in.pos_of_unit = perm_pou[i].data();
     };
     int best_perm_c = -1;
+    // Compiled instances whose registers spill are avoided (SURVEY Sec. 8 d-vi: 0 spill bytes):
+    // the search takes the next wider register instance that fits, and only if no spill-free
+    // plan exists at all does it accept a spilling one (second pass).
+    auto spills = [&](int inst, bool k8) -> bool {
+        if (p->host_only) return false;
+        const int key = inst * 64 + p->BT * 4 + (k8 ? 2 : 0) + (p->f16 ? 1 : 0);
+        for (auto& kv : p->spill_cache)
+            if (kv.first == key) return kv.second;
+        RecParams q{};
+        q.threads = 32;
+        q.k8 = k8 ? 1 : 0;
+        int regs[2] = {0, 0};
+        const bool sp = launch_recurrent(inst, p->BT, G, p->f16 ? 1 : 0, q, 1, 0, nullptr, true, regs, nullptr) == 0 &&
+                        regs[1] > 0;
+        p->spill_cache.emplace_back(key, sp);
+        return sp;
+    };
     auto try_layout = [&](int C, int L, int np, int reg_cap, int64_t ns_cap) {
         Layout lay;
         use_perm(C);
@@ -631,6 +651,17 @@ search_again:
             inst = reg_cap;
             ns = ((su - reg_cap) + 3) & ~3;
             if (ns > ns_cap) return;
+        }
+        if (spill_strict && spills(inst, false)) {  // next wider spill-free instance under the thread cap
+            int alt = -1;
+            for (int i = 0; i < kNumNP; ++i)
+                if (kNPList[i] > inst && kNPList[i] <= reg_cap && !spills(kNPList[i], false)) {
+                    alt = kNPList[i];
+                    break;
+                }
+            if (alt < 0) return;
+            inst = alt;
+            ns = su > inst ? ((su - inst) + 3) & ~3 : 0;
         }
         if (lay.vrows_max > G * ((H + C - 1) / C)) {  // pieces: more zs rows (and maybe threads)
             int um = 0;
@@ -712,6 +743,10 @@ search_again:
         in.E = 16;
         goto search_again;
     }
+    if (!any && spill_strict && !p->host_only) {  // only spilling instances fit: accept them
+        spill_strict = false;
+        goto search_again;
+    }
     if (!any) return SRNN_ERR_NOT_ON_CHIP;
     // Re-pack at the chosen instance width so the image has np_inst slots.
     Layout fin;
@@ -750,6 +785,7 @@ search_again:
         const int64_t chunks = exchange_tile_bytes(H, p->f16, p->BT) / 16;  // 16-byte chunks per tile
         const int64_t c = (chunks + best.threads - 1) / best.threads;       // per thread
         p->k8 = k8_compiled(best_inst, p->f16, p->BT) && ksmall < 8 && (c + 7) / 8 < (c + ksmall - 1) / ksmall;
+        if (p->k8 && spills(best_inst, true) && !spills(best_inst, false)) p->k8 = false;  // spill-free first
     }
     p->unit_of_pos.clear();
     p->pos_of_unit.clear();

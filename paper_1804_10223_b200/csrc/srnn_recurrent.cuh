@@ -261,19 +261,41 @@ struct Weights;
 // warp-uniform slot count n_w is checked once per group.  Slots between n_w
 // and the end of a group hold zero weights reading column 0 (a broadcast),
 // exactly like the paper's <index, 0> padding pairs.
+#ifndef SRNN_GS_F32_BT4
+#define SRNN_GS_F32_BT4 4
+#endif
+#ifndef SRNN_GS_F32
+#define SRNN_GS_F32 8
+#endif
 template <int NP, int BT>
 struct Weights<NP, BT, false> {
-    static constexpr int GS = BT == 4 ? 4 : 8;
-    uint32_t off[NP];
+    static constexpr int GS = BT == 4 ? SRNN_GS_F32_BT4 : SRNN_GS_F32;
+    // fp32 values, and the hs byte offsets of two slots per register (hs <= 64 KB in fp32
+    // mode, host-checked): 1.5 registers per pair instead of 2, the difference between a
+    // spill-free and a spilling instance at 128 registers (e.g. NP = 24, the C2 fp32 plan)
+#ifndef SRNN_F32_UNPACKED
+    uint32_t offp[(NP + 1) / 2];
+    __device__ __forceinline__ uint32_t off(int i) const {
+        return (i & 1) ? (offp[i >> 1] >> 16) : (offp[i >> 1] & 0xffffu);
+    }
+#else  // A/B: one offset register per pair
+    uint32_t offp[NP];
+    __device__ __forceinline__ uint32_t off(int i) const { return offp[i]; }
+#endif
     float w[NP];
     __device__ __forceinline__ void load(const RecParams& p, size_t img0, int n_w) {
 #pragma unroll
+        for (int i = 0; i < static_cast<int>(sizeof(offp) / 4); ++i) offp[i] = 0u;
+#pragma unroll
         for (int i = 0; i < NP; ++i) {
-            off[i] = 0u;
             w[i] = 0.0f;
             if (i < n_w) {
                 const uint2 e = p.img_f32[img0 + static_cast<size_t>(i) * p.threads];
-                off[i] = e.x;
+#ifndef SRNN_F32_UNPACKED
+                offp[i >> 1] |= e.x << (16 * (i & 1));
+#else
+                offp[i] = e.x;
+#endif
                 w[i] = __uint_as_float(e.y);
             }
         }
@@ -287,7 +309,7 @@ struct Weights<NP, BT, false> {
                     float4 h[GS];
 #pragma unroll
                     for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) h[j] = *reinterpret_cast<const float4*>(hs + off[i0 + j]);
+                        if (i0 + j < NP) h[j] = *reinterpret_cast<const float4*>(hs + off(i0 + j));
 #pragma unroll
                     for (int j = 0; j < GS; ++j) {
                         if (i0 + j < NP) {
@@ -302,7 +324,7 @@ struct Weights<NP, BT, false> {
                     float2 h[GS];
 #pragma unroll
                     for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) h[j] = *reinterpret_cast<const float2*>(hs + off[i0 + j]);
+                        if (i0 + j < NP) h[j] = *reinterpret_cast<const float2*>(hs + off(i0 + j));
 #pragma unroll
                     for (int j = 0; j < GS; ++j) {
                         if (i0 + j < NP) {
@@ -314,7 +336,7 @@ struct Weights<NP, BT, false> {
                     float h[GS];
 #pragma unroll
                     for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) h[j] = *reinterpret_cast<const float*>(hs + off[i0 + j]);
+                        if (i0 + j < NP) h[j] = *reinterpret_cast<const float*>(hs + off(i0 + j));
 #pragma unroll
                     for (int j = 0; j < GS; ++j)
                         if (i0 + j < NP) acc[0] = fmaf(w[i0 + j], h[j], acc[0]);

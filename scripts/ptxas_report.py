@@ -15,8 +15,9 @@ for line in log:
         st, sp = int(m.group(1)), int(m.group(2))
     m = re.search(r"Used (\d+) registers", line)
     if m and cur:
-        k = re.search(r"srnn_persistent_kernelILi(\d+)ELi(\d+)ELi(\d+)ELb(\d)", cur)
-        name = f"rec NP={k.group(1)} BT={k.group(2)} G={k.group(3)} f16={k.group(4)}" if k else cur[:60]
+        k = re.search(r"srnn_persistent_kernelILi(\d+)ELi(\d+)ELi(\d+)ELb(\d)ELi(n?\d+)E", cur)
+        name = (f"rec NP={k.group(1)} BT={k.group(2)} G={k.group(3)} f16={k.group(4)} MT={k.group(5).replace('n', '-')}"
+                if k else cur[:60])
         rows.append((name, int(m.group(1)), st, sp))
         cur = None
 bad = [r for r in rows if r[2] or r[3]]
