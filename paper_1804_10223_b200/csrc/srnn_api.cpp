@@ -454,6 +454,17 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     // (H * E <= 65536), 16-byte units for BT = 8 (the column index, any H)
     const int umax_guess = (c.hidden + p->sm_count - 1) / p->sm_count;
     while (bt > 1 && smem_for(p, umax_guess, bt, (c.batch + bt - 1) / bt) > static_cast<size_t>(p->smem_optin)) bt /= 2;
+    // Register budget for the expected pairs: two registers per pair in the hoisted
+    // format, at most ~75% of each SM's 64K registers.  Checked before the offset-format
+    // limit below: a layer that cannot be on-chip at all is NOT_ON_CHIP, not UNSUPPORTED.
+    const double exp_pairs = static_cast<double>(c.density) * p->G * c.hidden * static_cast<double>(c.hidden);
+    // plus the shared-memory weight tier (up to ~60% of shared memory)
+    const double reg_capacity_pairs =
+        (0.75 * 65536.0 / (p->f16 ? 1.0 : 2.0) + 0.6 * p->smem_optin / (p->f16 ? 4.0 : 8.0)) * p->sm_count;
+    if (exp_pairs > reg_capacity_pairs) {
+        delete p;
+        return SRNN_ERR_NOT_ON_CHIP;
+    }
     // register pairs carry 16-bit hs byte offsets (fp16 tiles <= 4 and fp32): hs <= 64 KB
     while (bt > 1 && (!p->f16 || bt < 8) && static_cast<int64_t>(c.hidden) * elem_bytes(p->f16, bt) > 65536) bt /= 2;
     if ((!p->f16 || bt < 8) && static_cast<int64_t>(c.hidden) * elem_bytes(p->f16, bt) > 65536) {
@@ -466,16 +477,6 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     if (smem_for(p, umax_guess, bt, p->n_tiles_max) > static_cast<size_t>(p->smem_optin)) {
         delete p;
         return SRNN_ERR_NOT_ON_CHIP;  // h staging alone exceeds shared memory
-    }
-    // Register budget for the expected pairs: two registers per pair in the
-    // hoisted format, at most ~75% of each SM's 64K registers.
-    const double exp_pairs = static_cast<double>(c.density) * p->G * c.hidden * static_cast<double>(c.hidden);
-    // plus the shared-memory weight tier (up to ~60% of shared memory)
-    const double reg_capacity_pairs =
-        (0.75 * 65536.0 / (p->f16 ? 1.0 : 2.0) + 0.6 * p->smem_optin / (p->f16 ? 4.0 : 8.0)) * p->sm_count;
-    if (exp_pairs > reg_capacity_pairs) {
-        delete p;
-        return SRNN_ERR_NOT_ON_CHIP;
     }
     if (!p->host_only) {
         DeviceGuard g(c.device);
