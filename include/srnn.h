@@ -120,6 +120,17 @@ typedef enum { SRNN_PREC_FP32 = 0, SRNN_PREC_FP16W_FP32ACC = 1 } srnn_prec_t;
                                               warps get rows of similar length; the exchange and hs
                                               use the resulting unit order (results unchanged up to
                                               fp reassociation)                                  */
+#define SRNN_FLAG_COLUMN_SPLIT   (1u << 13) /* column split ("split one row among multiple
+                                              blocks"): CTAs run as 2-CTA thread-block clusters; both
+                                              CTAs of a pair hold every row of the pair's units, each
+                                              only the nonzeros of one half of the columns, so each
+                                              stages and fetches only half of h_{t-1} per step; the
+                                              two partial row sums are added through distributed
+                                              shared memory (fixed order: deterministic).  Halves the
+                                              h staging and exchange ingress per SM: larger H on chip
+                                              (the 16-bit staged offsets cover twice the columns) and
+                                              a faster load phase at large H.  RNN / LSTM / GRU cells,
+                                              batch tiles <= 8; not with CLASS_BALANCE / DENSE_TC  */
 #define SRNN_FLAG_DENSE_TC       (1u << 8) /* comparator: the DENSE persistent
                                               RNN of PAPER.md:51-71 (Sec. 3.2, Diamos et al.)
                                               re-done for sm_100a tensor cores.  U_r is densified
@@ -180,6 +191,8 @@ typedef struct {
     int32_t dense_frags_smem;  /* A fragments per lane held in shared memory                 */
     int32_t spill_bytes;       /* local memory (register spills / stack) per thread of the
                                   chosen compiled instance; 0 for a spill-free instance  (L) */
+    int32_t column_split;      /* 1: SRNN_FLAG_COLUMN_SPLIT plan (2-CTA clusters)             */
+    int32_t column_half;       /* column split: first column of the second half (units)      */
 } srnn_plan_info_t;
 
 /* Create a plan for the layer described by *cfg.

@@ -34,6 +34,7 @@ FLAG_DEBUG_DROP_PUBLISH = 1 << 9
 FLAG_FP32_TC_GEMM = 1 << 10
 FLAG_Y_BATCH_MAJOR = 1 << 11
 FLAG_CLASS_BALANCE = 1 << 12
+FLAG_COLUMN_SPLIT = 1 << 13
 
 EXPORTED = ["srnn_plan_create", "srnn_plan_query", "srnn_load_weights", "srnn_forward", "srnn_input_projection",
             "srnn_recurrence", "srnn_forward_host", "srnn_plan_status", "srnn_plan_export_layout",
@@ -64,7 +65,8 @@ class PlanInfo(ctypes.Structure):
                  "wavefronts_per_step_ideal", "conflict_wavefronts", "smem_weight_bytes_per_cta",
                  "image_slots_per_lane", "model_cycles_per_step")] + \
                [(n, ctypes.c_int32) for n in
-                ("dense_m_tiles", "dense_kblocks_per_warp", "dense_frags_reg", "dense_frags_smem", "spill_bytes")]
+                ("dense_m_tiles", "dense_kblocks_per_warp", "dense_frags_reg", "dense_frags_smem", "spill_bytes",
+                 "column_split", "column_half")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

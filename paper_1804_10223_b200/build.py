@@ -44,7 +44,10 @@ def _flags_stamp(extra):
 
 def _compile(src, verbose=False, obj_dir=OBJ, variant_flags=()):
     obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
-    extra = list(variant_flags) + os.environ.get("SRNN_NVCC_FLAGS", "").split()  # A/B experiments (e.g. -DSRNN_LOADK_BT4=3)
+    extra = list(variant_flags)
+    only = os.environ.get("SRNN_NVCC_FLAGS_ONLY", "")  # comma list of source-name substrings the flags apply to
+    if not only or any(t and t in os.path.basename(src) for t in only.split(",")):
+        extra += os.environ.get("SRNN_NVCC_FLAGS", "").split()  # A/B experiments (e.g. -DSRNN_LOADK_BT4=3)
     stamp = _flags_stamp(extra)
     newest_dep = max([os.path.getmtime(src)] + [os.path.getmtime(d) for d in _deps()])
     try:

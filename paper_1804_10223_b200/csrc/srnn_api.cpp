@@ -94,6 +94,16 @@ struct srnn_plan {
     int dense_mt = 0, dense_kpw = 0, dense_nf = 0, dense_inst = 0, hs_rows = 0;
     std::vector<uint4> dense_img;  // host image [cta][frag][thread] (freed after upload)
     bool k8 = false;               // sparse fp16 tile-of-4 plan that needs 8 poll slots per thread
+    // column split (SRNN_FLAG_COLUMN_SPLIT): 2-CTA clusters, each CTA one column half
+    bool csplit = false;
+    int hsplit = 0;                       // first column of the second half (units, multiple of 8)
+    std::vector<int32_t> unit0_real;      // [num_ctas + 1] units each CTA finalises / publishes
+    int32_t* d_vunit0 = nullptr;          // lay.cta_unit0 (virtual: the pair's units per CTA)
+    // b' by TMA windows (RecParams::bp_map, a kernel parameter): re-encoded when the call's
+    // (b' pointer, T, B) differ from the last one
+    alignas(64) CUtensorMap bp_map;
+    const float* bpmap_ptr = nullptr;
+    int32_t bpmap_T = 0, bpmap_B = 0;
     std::vector<std::pair<int, bool>> spill_cache;  // (instance key, spills?) of queried instances
 };
 
@@ -120,17 +130,46 @@ int inst_for(int slots, bool f16, int bt) {
 
 int elem_bytes(bool f16, int bt) { return f16 ? 2 * bt : 4 * bt; }
 
+// b' can come by TMA windows: one batch tile, no unit permutation, 16-byte b' row pitch
+bool bp_tma_ok(const srnn_plan* p, int n_tiles, int units_max) {
+    return !p->dense && p->G == 1 && n_tiles == 1 && p->cfg.hidden % 4 == 0 && bp_box_units(units_max) <= 256 &&
+           (p->cfg.flags & SRNN_FLAG_CLASS_BALANCE) == 0 && std::getenv("SRNN_NO_BP_TMA") == nullptr;
+}
+
 size_t smem_for(const srnn_plan* p, int units_max, int bt, int n_tiles, int vrows = 0) {
-    size_t s = (static_cast<size_t>(p->cfg.hidden) * elem_bytes(p->f16, bt) + 15) & ~static_cast<size_t>(15);
+    const int hs_units = p->csplit ? p->hsplit : p->cfg.hidden;  // column split: one half of h staged
+    size_t s = (static_cast<size_t>(hs_units) * elem_bytes(p->f16, bt) + 15) & ~static_cast<size_t>(15);
+    if (p->csplit && vrows == 0) vrows = 2 * p->G * units_max;  // a CTA holds the rows of its pair's units
     const size_t zrows = std::max<size_t>(static_cast<size_t>(p->G) * units_max, vrows);  // zs: (virtual) rows
-    s += zrows * bt * 4 + 2 * static_cast<size_t>(p->G) * units_max * bt * 4;  // zs + double-buffered b'
+    s += (p->csplit ? 2 : 1) * zrows * bt * 4 + 2 * static_cast<size_t>(p->G) * units_max * bt * 4;  // zs + b'
     if (p->G >= 3) s += static_cast<size_t>(n_tiles) * units_max * bt * 4;  // LSTM c / GRU fp32 h
+    if (bp_tma_ok(p, n_tiles, units_max)) s += static_cast<size_t>(bp_tma_smem_bytes(p->G, bt, units_max));  // TMA b' windows
     return s + 16;
+}
+
+// 3-D tensor map over b' [T][B][G*H] fp32: box {boxu units, bt samples, kBpWin steps}
+bool encode_bprime_map(CUtensorMap* map, const float* bprime, int64_t GH, int B, int T, int boxu, int bt) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(GH), static_cast<cuuint64_t>(B), static_cast<cuuint64_t>(T)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(GH) * 4, static_cast<cuuint64_t>(GH) * 4 * B};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(boxu), static_cast<cuuint32_t>(bt), static_cast<cuuint32_t>(kBpWin)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(bprime), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 void free_device(srnn_plan* p) {
     cudaFree(p->d_img);
     cudaFree(p->d_unit0);
+    cudaFree(p->d_vunit0);
     cudaFree(p->d_perm);
     cudaFree(p->d_piece0);
     cudaFree(p->d_wslots);
@@ -439,21 +478,46 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     p->f16 = c.prec == SRNN_PREC_FP16W_FP32ACC && (c.flags & SRNN_FLAG_FP32_STAGING) == 0;
     p->dense = (c.flags & SRNN_FLAG_DENSE_TC) != 0;
     if (p->dense) return create_dense(p, out);
-    // Batch tile: the paper's wide load interleaves 4 samples.
-    int bt = c.batch >= 4 ? 4 : (c.batch >= 2 ? 2 : 1);
-    if (p->f16 && c.batch >= 8) bt = 8;    // fp16: 8 samples per LDS.128 (one exchange round for B = 8)
-    if (p->f16 && c.batch >= 16) bt = 16;  // fp16: two planes of 8 (every extra tile costs a whole exchange)
-    if (c.batch_tile == 1 || c.batch_tile == 2 || c.batch_tile == 4 || ((c.batch_tile == 8 || c.batch_tile == 16) && p->f16))
-        bt = c.batch_tile;
-    if (const char* e = std::getenv("SRNN_BT")) {  // experiment override: batch tile width
-        const int v = std::atoi(e);
-        if (v == 1 || v == 2 || v == 4 || ((v == 8 || v == 16) && p->f16)) bt = v;
-    }
-    while (bt > 1 && bt > c.batch) bt /= 2;
-    // fp16 register pairs carry the hs offset in 16 bits: bytes for BT <= 4
-    // (H * E <= 65536), 16-byte units for BT = 8 (the column index, any H)
+    // Batch tile: the paper's wide load interleaves 4 samples.  tile_for(split) is
+    // the widest tile that fits (h staging in shared memory; 16-bit staged offsets for fp16 tiles
+    // <= 4 and fp32: hs <= 64 KB, the staged half under the column split), 0 if none does.
     const int umax_guess = (c.hidden + p->sm_count - 1) / p->sm_count;
-    while (bt > 1 && smem_for(p, umax_guess, bt, (c.batch + bt - 1) / bt) > static_cast<size_t>(p->smem_optin)) bt /= 2;
+    const int hsplit = ((c.hidden + 1) / 2 + 7) & ~7;  // column split: the half boundary on a 16-byte chunk
+    auto tile_for = [&](bool split) -> int {
+        p->csplit = split;
+        p->hsplit = split ? hsplit : 0;
+        int bt = c.batch >= 4 ? 4 : (c.batch >= 2 ? 2 : 1);
+        if (p->f16 && c.batch >= 8) bt = 8;    // fp16: 8 samples per LDS.128 (one exchange round for B = 8)
+        if (p->f16 && c.batch >= 16) bt = 16;  // fp16: two planes of 8 (every extra tile costs a whole exchange)
+        if (c.batch_tile == 1 || c.batch_tile == 2 || c.batch_tile == 4 ||
+            ((c.batch_tile == 8 || c.batch_tile == 16) && p->f16))
+            bt = c.batch_tile;
+        if (const char* e = std::getenv("SRNN_BT")) {  // experiment override: batch tile width
+            const int v = std::atoi(e);
+            if (v == 1 || v == 2 || v == 4 || ((v == 8 || v == 16) && p->f16)) bt = v;
+        }
+        while (bt > 1 && bt > c.batch) bt /= 2;
+        if (split && bt > 8) bt = 8;  // the column split stages one plane of h
+        while (bt > 1 && smem_for(p, umax_guess, bt, (c.batch + bt - 1) / bt) > static_cast<size_t>(p->smem_optin)) bt /= 2;
+        const int64_t hs_units = split ? hsplit : c.hidden;
+        while (bt > 1 && (!p->f16 || bt < 8) && hs_units * elem_bytes(p->f16, bt) > 65536) bt /= 2;
+        if ((!p->f16 || bt < 8) && hs_units * elem_bytes(p->f16, bt) > 65536) return 0;
+        return bt;
+    };
+    // Column split (SRNN_FLAG_COLUMN_SPLIT, or automatically when the unsplit layer needs more batch
+    // tiles -- each a whole exchange round per step -- or does not fit the offset format at all)
+    const bool split_ok = !(c.flags & (SRNN_FLAG_CLASS_BALANCE | SRNN_FLAG_GRID_SYNC)) && hsplit < c.hidden &&
+                          p->sm_count >= 2 && !(c.num_ctas != 0 && (c.num_ctas & 1));
+    bool split = (c.flags & SRNN_FLAG_COLUMN_SPLIT) != 0;
+    if (split && !split_ok) {
+        delete p;
+        return SRNN_ERR_UNSUPPORTED;
+    }
+    if (!split && split_ok && c.hidden >= 2 * p->sm_count && std::getenv("SRNN_NO_AUTO_SPLIT") == nullptr) {
+        const int b0 = tile_for(false), b1 = tile_for(true);
+        split = b1 > 0 && (b0 == 0 || (c.batch + b1 - 1) / b1 < (c.batch + b0 - 1) / b0);
+    }
+    int bt = tile_for(split);
     // Register budget for the expected pairs: two registers per pair in the hoisted
     // format, at most ~75% of each SM's 64K registers.  Checked before the offset-format
     // limit below: a layer that cannot be on-chip at all is NOT_ON_CHIP, not UNSUPPORTED.
@@ -465,9 +529,7 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
         delete p;
         return SRNN_ERR_NOT_ON_CHIP;
     }
-    // register pairs carry 16-bit hs byte offsets (fp16 tiles <= 4 and fp32): hs <= 64 KB
-    while (bt > 1 && (!p->f16 || bt < 8) && static_cast<int64_t>(c.hidden) * elem_bytes(p->f16, bt) > 65536) bt /= 2;
-    if ((!p->f16 || bt < 8) && static_cast<int64_t>(c.hidden) * elem_bytes(p->f16, bt) > 65536) {
+    if (bt == 0) {  // the staged h does not fit the 16-bit offsets of the register pairs
         delete p;
         return SRNN_ERR_UNSUPPORTED;
     }
@@ -497,6 +559,8 @@ srnn_status_t srnn_plan_query(srnn_plan_t p, srnn_plan_info_t* out) {
     out->batch_tile = p->BT;
     out->num_batch_tiles = p->n_tiles_max;
     out->fits = 1;
+    out->column_split = p->csplit ? 1 : 0;
+    out->column_half = p->csplit ? p->hsplit : 0;
     if (p->loaded) {
         const Layout& l = p->lay;
         out->num_ctas = l.num_ctas;
@@ -504,8 +568,9 @@ srnn_status_t srnn_plan_query(srnn_plan_t p, srnn_plan_info_t* out) {
         out->lanes_per_row = l.lanes_per_row;
         out->pairs_per_lane = p->np_inst;
         out->slots_used = l.slots_used;
+        const std::vector<int32_t>& u0 = p->csplit ? p->unit0_real : l.cta_unit0;  // units a CTA publishes
         int umax = 0;
-        for (int c = 0; c < l.num_ctas; ++c) umax = std::max(umax, l.cta_unit0[c + 1] - l.cta_unit0[c]);
+        for (int c = 0; c < l.num_ctas; ++c) umax = std::max(umax, u0[c + 1] - u0[c]);
         out->units_per_cta_max = umax;
         out->regs_per_thread = p->regs;
         out->spill_bytes = p->spill_bytes;
@@ -588,6 +653,55 @@ search_again:
         const int cmax = std::max(1, std::min(p->sm_count - reserve, H));
         cands_c.push_back(cmax);
         for (int cc = cmax / 2; cc >= 1; cc /= 2) cands_c.push_back(cc);
+    }
+    // Column split: one even CTA count (pairs = clusters); the packer sees a virtual matrix whose
+    // units are (pair unit, column half): CTA 2q + r holds the rows of pair q's units restricted
+    // to the columns of half r, renumbered from the half's first column (its hs position).
+    std::vector<int32_t> v_rowptr, v_col, v_unit0;
+    std::vector<float> v_val;
+    if (p->csplit) {
+        int C = cands_c[0] & ~1;
+        if (C < 2 || H < C) return SRNN_ERR_UNSUPPORTED;
+        cands_c.assign(1, C);
+        const int NQ = C / 2, Hc = p->hsplit;
+        v_unit0.assign(C + 1, 0);
+        p->unit0_real.assign(C + 1, 0);
+        std::vector<int32_t> vreal(2 * static_cast<size_t>(H)), vhalf(2 * static_cast<size_t>(H));
+        for (int q = 0; q < NQ; ++q) {
+            const int q0 = static_cast<int>(static_cast<int64_t>(q) * H / NQ);
+            const int q1 = static_cast<int>(static_cast<int64_t>(q + 1) * H / NQ), UQ = q1 - q0;
+            v_unit0[2 * q] = 2 * q0;
+            v_unit0[2 * q + 1] = 2 * q0 + UQ;
+            p->unit0_real[2 * q] = q0;
+            p->unit0_real[2 * q + 1] = q0 + UQ / 2;
+            for (int r = 0; r < 2; ++r)
+                for (int i = 0; i < UQ; ++i) {
+                    vreal[2 * q0 + r * UQ + i] = q0 + i;
+                    vhalf[2 * q0 + r * UQ + i] = r;
+                }
+        }
+        v_unit0[C] = 2 * H;
+        p->unit0_real[C] = H;
+        v_rowptr.assign(static_cast<size_t>(G) * 2 * H + 1, 0);
+        v_col.reserve(nnz);
+        v_val.reserve(nnz);
+        for (int g = 0; g < G; ++g)
+            for (int v = 0; v < 2 * H; ++v) {
+                const int32_t rr = g * H + vreal[v], hf = vhalf[v];
+                for (int32_t i = rowptr[rr]; i < rowptr[rr + 1]; ++i) {
+                    const int32_t cc = col[i];
+                    if ((cc >= Hc) == (hf == 1)) {
+                        v_col.push_back(cc - hf * Hc);
+                        v_val.push_back(qval[i]);
+                    }
+                }
+                v_rowptr[static_cast<size_t>(g) * 2 * H + v + 1] = static_cast<int32_t>(v_col.size());
+            }
+        in.H = 2 * H;
+        in.rowptr = v_rowptr.data();
+        in.col = v_col.data();
+        in.val = v_val.data();
+        in.cta_unit0 = v_unit0.data();
     }
     std::vector<int> cands_l;
     if (p->cfg.lanes_per_row > 0)
@@ -673,7 +787,7 @@ search_again:
                     static_cast<size_t>(p->smem_optin))
                 return;
         }
-        double cst = cost_model(lay, p->BT, H, p->n_tiles_max, p->f16, inst);
+        double cst = cost_model(lay, p->BT, p->csplit ? p->hsplit : H, p->n_tiles_max, p->f16, inst);
         if (ns > 0) cst += static_cast<double>(ns) * lay.warps * 2.0;  // weight LDS + issue per smem slot
         cst += 2.0 * inst;  // tie-break toward the smaller register instance (code size)
         if (plan_log)
@@ -707,7 +821,7 @@ search_again:
         }
         if (any && static_cast<double>(pairs_max) / P * p->n_tiles_max > best_cost) continue;
         for (int L : cands_l) {
-            const int rows_max = G * umax;
+            const int rows_max = (p->csplit ? 2 : 1) * G * umax;  // column split: the pair's rows
             const int threads = ((rows_max * L + 31) / 32) * 32;
             if (threads > 1024) continue;
             int reg_cap = -1;  // largest register instance whose thread cap admits this CTA size
@@ -774,7 +888,10 @@ search_again:
         }
     }
     int umax = 0;
-    for (int c = 0; c < fin.num_ctas; ++c) umax = std::max(umax, fin.cta_unit0[c + 1] - fin.cta_unit0[c]);
+    {
+        const std::vector<int32_t>& u0 = p->csplit ? p->unit0_real : fin.cta_unit0;
+        for (int c = 0; c < fin.num_ctas; ++c) umax = std::max(umax, u0[c + 1] - u0[c]);
+    }
     p->smem_bytes = smem_for(p, umax, p->BT, p->n_tiles_max, fin.vrows_max) + 16 +
                     static_cast<size_t>(best_ns) * fin.threads * pair_bytes;
     p->np_inst = best_inst;
@@ -858,8 +975,16 @@ search_again:
             if (e == cudaSuccess)
                 e = cudaMemcpy(p->d_perm, p->unit_of_pos.data(), p->unit_of_pos.size() * 4, cudaMemcpyHostToDevice);
         }
-        if (e == cudaSuccess) e = cudaMalloc(&p->d_unit0, l.cta_unit0.size() * 4);
-        if (e == cudaSuccess) e = cudaMemcpy(p->d_unit0, l.cta_unit0.data(), l.cta_unit0.size() * 4, cudaMemcpyHostToDevice);
+        // units each CTA finalises and publishes (column split: its half of the pair's units; the
+        // packed layout's ranges are then the virtual (pair unit, half) ones)
+        const std::vector<int32_t>& u0v = p->csplit ? p->unit0_real : l.cta_unit0;
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_unit0, u0v.size() * 4);
+        if (e == cudaSuccess) e = cudaMemcpy(p->d_unit0, u0v.data(), u0v.size() * 4, cudaMemcpyHostToDevice);
+        cudaFree(p->d_vunit0);
+        p->d_vunit0 = nullptr;
+        if (e == cudaSuccess && p->csplit) e = cudaMalloc(&p->d_vunit0, l.cta_unit0.size() * 4);
+        if (e == cudaSuccess && p->csplit)
+            e = cudaMemcpy(p->d_vunit0, l.cta_unit0.data(), l.cta_unit0.size() * 4, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMalloc(&p->d_wslots, l.warp_slots.size() * 4);
         if (e == cudaSuccess) e = cudaMemcpy(p->d_wslots, l.warp_slots.data(), l.warp_slots.size() * 4, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMalloc(&p->d_wx, wx_n * 4);
@@ -928,6 +1053,7 @@ search_again:
         RecParams rp{};
         rp.threads = l.threads;
         rp.k8 = p->k8 ? 1 : 0;
+        rp.csplit = p->csplit ? 1 : 0;  // cluster co-residency check
         int regs[2] = {0, 0}, maxb = 0;
         int le = p->dense ? launch_dense(p->dense_inst, p->dense_mt, p->BT, G, rp, l.num_ctas, p->smem_bytes, nullptr,
                                          true, regs, &maxb)
@@ -1034,8 +1160,14 @@ static srnn_status_t recurrence_impl(srnn_plan_t p, int32_t T, int32_t B, const 
     rp.np_inst = p->np_inst;
     rp.smem_slots = p->ns_slots;
     int umax = 0;
-    for (int c = 0; c < p->lay.num_ctas; ++c) umax = std::max(umax, p->lay.cta_unit0[c + 1] - p->lay.cta_unit0[c]);
+    {
+        const std::vector<int32_t>& u0 = p->csplit ? p->unit0_real : p->lay.cta_unit0;
+        for (int c = 0; c < p->lay.num_ctas; ++c) umax = std::max(umax, u0[c + 1] - u0[c]);
+    }
     rp.units_max = umax;
+    rp.csplit = p->csplit ? 1 : 0;
+    rp.hsplit = p->hsplit;
+    rp.cta_vunit0 = p->d_vunit0;
     rp.epoch = p->epoch;
     rp.flags = p->cfg.flags;
     rp.k8 = p->k8 ? 1 : 0;
@@ -1065,6 +1197,19 @@ static srnn_status_t recurrence_impl(srnn_plan_t p, int32_t T, int32_t B, const 
     // 1-bit tags follow the global step (epoch + s, continuous across launches and
     // across the u32 wrap); tiles idle in the previous launch hold older steps
     rp.reinit = rp.n_tiles > p->xbuf_valid_tiles ? 1 : 0;
+    if (p->csplit) {
+        // the cluster launch has no grid-wide barrier for the in-kernel re-initialisation: the
+        // host fills both parities with the stale tags (cheap: 2 x tiles x H x E bytes) every call
+        auto pat = [&](uint32_t q) {
+            const uint32_t g = p->epoch + q, stale = ((g - 2u) >> 1) & 1u;  // tag of step g - 2
+            return p->f16 ? (stale | (stale << 16)) : stale;
+        };
+        const int64_t per = static_cast<int64_t>(p->n_tiles_max) * p->tile_bytes;
+        // parity of global step epoch is epoch & 1: buffer (epoch & 1) holds pattern q = 0
+        const uint32_t pa = (p->epoch & 1u) ? pat(1) : pat(0), pb = (p->epoch & 1u) ? pat(0) : pat(1);
+        if (launch_xbuf_fill(p->d_xbuf, per, pa, pb, stream) != 0) return SRNN_ERR_CUDA;
+        rp.reinit = 0;
+    }
     rp.status = p->d_status;
     rp.timeout_ns = p->timeout_ns;
     if (const char* d = std::getenv("SRNN_POLL_BACKOFF_NS")) rp.poll_backoff_ns = static_cast<uint32_t>(std::atoi(d));
@@ -1082,6 +1227,21 @@ static srnn_status_t recurrence_impl(srnn_plan_t p, int32_t T, int32_t B, const 
     }
     rp.bp_ready = pa.bp_ready;
     rp.bp_ready_base = pa.bp_ready_base;
+    // b' by TMA windows when the plan reserved them and b' is resident (not the pipelined host forward)
+    if (!p->dense && pa.bp_ready == nullptr && rp.n_tiles == 1 && bp_tma_ok(p, p->n_tiles_max, umax) &&
+        (reinterpret_cast<uintptr_t>(bprime) & 15) == 0) {
+        const int boxu = bp_box_units(umax);
+        if (p->bpmap_ptr != bprime || p->bpmap_T != T || p->bpmap_B != B) {
+            if (!encode_bprime_map(&p->bp_map, bprime, static_cast<int64_t>(p->G) * p->cfg.hidden, B, T, boxu, p->BT))
+                return SRNN_ERR_CUDA;
+            p->bpmap_ptr = bprime;
+            p->bpmap_T = T;
+            p->bpmap_B = B;
+        }
+        rp.bp_map = p->bp_map;
+        rp.bp_tma = 1;
+        rp.bp_boxu = boxu;
+    }
     rp.progress = pa.progress;
     rp.progress_every = pa.every > 0 ? pa.every : 1;
     int e;

@@ -1,3 +1,4 @@
+#include <algorithm>
 // Dispatch (NP, BT, G, precision) -> compiled instance of the persistent kernel.
 #include <cuda_runtime.h>
 
@@ -34,4 +35,21 @@ int launch_recurrent(int np, int bt, int g, int f16, const RecParams& p, int num
     }
 #undef SRNN_NP
 }
+// Exchange re-initialisation from the host side (column-split plans, whose cluster launch does
+// not use the kernel's grid-wide barrier): every exchanged 16/32-bit value of parity q gets
+// the stale tag of the step that parity last held (pattern pat_q), i.e. "not yet written".
+__global__ void xbuf_fill_kernel(uint32_t* buf, int64_t words_per_parity, uint32_t pat0, uint32_t pat1) {
+    const int64_t n = 2 * words_per_parity;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        buf[i] = i < words_per_parity ? pat0 : pat1;
+}
+
+int launch_xbuf_fill(void* buf, int64_t bytes_per_parity, uint32_t pat0, uint32_t pat1, void* stream) {
+    const int64_t w = bytes_per_parity / 4;
+    const int blocks = static_cast<int>(std::min<int64_t>(1024, (2 * w + 255) / 256));
+    xbuf_fill_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<uint32_t*>(buf), w, pat0, pat1);
+    return static_cast<int>(cudaGetLastError());
+}
+
 }  // namespace srnn

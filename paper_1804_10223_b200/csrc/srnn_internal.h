@@ -1,6 +1,8 @@
 // srnn_internal.h -- shared between the host planner (srnn_api.cpp) and the
 // CUDA kernels of the product path.  Never included by oracle/.
 #pragma once
+#include <cuda.h>
+
 #include <cstdint>
 
 #ifdef __CUDACC__
@@ -18,6 +20,9 @@ namespace srnn {
 // Kernel arguments of the persistent recurrent kernel (one struct, passed by
 // value through cudaLaunchCooperativeKernel).
 struct RecParams {
+    // b' tensor map (see bp_tma below): first member, so it sits at the 128-byte aligned start of
+    // the kernel's parameter buffer (__grid_constant__: the TMA unit reads it from param space)
+    alignas(128) CUtensorMap bp_map;
     // problem
     int32_t H;        // hidden units
     int32_t G;        // gates per unit (1 RNN, 4 LSTM)
@@ -67,6 +72,20 @@ struct RecParams {
     uint32_t* progress;        // +1 per CTA every progress_every steps (after y is stored), or null
     int32_t progress_every;
     int32_t k8;                // host-side instance choice: the 8-poll-slot instance (k8_compiled)
+    // b' by TMA (one batch tile, resident b'): CUtensorMap in device memory over b' [T][B][G*H]
+    // (3-D: units, samples, steps), box {bp_boxu, BT, kBpWin}; one thread loads the next window
+    // of kBpWin steps per gate while the current window is consumed (double buffer, mbarriers)
+    // column split (SRNN_FLAG_COLUMN_SPLIT): CTA pairs form 2-CTA clusters; both CTAs
+    // of cluster q hold all rows of the cluster's units, CTA rank r only the columns of half r
+    // ([0, hsplit) or [hsplit, H)), and stage only that half of h; partial row sums are added
+    // across the pair through distributed shared memory.  cta_unit0 then lists the units each
+    // CTA finalises and publishes (its half of the cluster's units), cta_vunit0 the cluster's
+    // units (2 * first unit, +UQ, ...: UQ = the pair's unit count, the CTA's row count / G).
+    int32_t csplit;
+    int32_t hsplit;
+    const int32_t* cta_vunit0;
+    int32_t bp_tma;            // 1: b' by TMA windows through bp_map; 0: per-step cp.async of b'
+    int32_t bp_boxu;           // units per box (bp_box_units(units_max))
     // SRNN_FLAG_DENSE_TC comparator (dense U_r as mma.sync A fragments)
     const uint4* img_dense;    // [cta][frag][thread] A fragments (4 x 2 fp16), frag = kk * MT + m
     int32_t dense_kpw;         // k-blocks (16 columns) per warp
@@ -104,10 +123,20 @@ int launch_f32_to_f16(const float* in, void* out, int64_t n, void* stream);
 int launch_gemm_tf32x3(const void* map_a_hi, const void* map_a_lo, const void* map_b_hi, const void* map_b_lo,
                        const float* bias, float* C, int M, int N, int K, void* stream, int m_off, int sms);
 int launch_split_tf32(const float* in, float* hi, float* lo, int64_t rows, int cols, int ld_out, void* stream);
+int launch_xbuf_fill(void* buf, int64_t bytes_per_parity, uint32_t pat0, uint32_t pat1, void* stream);
 int preload_projection_kernels();
 int preload_gemm_f32();
 int launch_f32_to_f16_padded(const float* in, void* out, int64_t rows, int cols, int ld_out, void* stream);
 
+// b' TMA window (steps per bulk tensor load) and the shared-memory bytes of its double buffer
+// plus two mbarriers (must match the kernel's carve-up).
+constexpr int kBpWin = 8;
+// units per b' box: a CTA's units start at any column, the box at the 16-byte aligned column
+// below it (TMA tile mode needs the innermost start coordinate 16-byte aligned): up to 3 more
+SRNN_HD constexpr int bp_box_units(int units_max) { return (units_max + 3 + 3) / 4 * 4; }
+SRNN_HD constexpr int64_t bp_tma_smem_bytes(int G, int bt, int units_max) {
+    return 2LL * G * kBpWin * bt * bp_box_units(units_max) * 4 + 16 + 128;  // + alignment of the TMA window
+}
 // Poll slots (16-byte exchange chunks in flight per loader thread) of each compiled
 // instance; the k8 instances (MT = -1 in srnn_recurrent.cuh) poll 8.  Measured on B200
 // (DESIGN.md Sec. 4 "exchange protocol"); SRNN_LOADK_* override for A/B builds.

@@ -134,7 +134,8 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
     lay.np_budget = NP;
     lay.cta_unit0.resize(C + 1);
     int umax = 0;
-    for (int c = 0; c <= C; ++c) lay.cta_unit0[c] = static_cast<int32_t>((static_cast<int64_t>(c) * H) / C);
+    for (int c = 0; c <= C; ++c)
+        lay.cta_unit0[c] = in.cta_unit0 ? in.cta_unit0[c] : static_cast<int32_t>((static_cast<int64_t>(c) * H) / C);
     for (int c = 0; c < C; ++c) umax = std::max(umax, lay.cta_unit0[c + 1] - lay.cta_unit0[c]);
     // virtual rows: pieces of rows longer than piece_cap (contiguous CSR sub-ranges)
     struct VRow {

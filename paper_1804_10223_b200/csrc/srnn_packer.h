@@ -23,6 +23,10 @@ struct PackInput {
     // packed like rows; the epilogue sums a row's pieces (class-based balancing of heavy
     // rows).  0 = never split.
     int32_t piece_cap = 0;
+    // Explicit unit ranges per CTA ([C+1], CTA c owns units [cta_unit0[c], cta_unit0[c+1])); nullptr =
+    // the even split c*H/C.  The column split (SRNN_FLAG_COLUMN_SPLIT) packs a virtual matrix whose
+    // units are (cluster unit, column half) and needs both CTAs of a pair to own equally many.
+    const int32_t* cta_unit0 = nullptr;
 };
 
 // Class-based assignment of units to CTAs ("define a number of classes for

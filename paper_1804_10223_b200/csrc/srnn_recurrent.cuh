@@ -256,6 +256,31 @@ __device__ __forceinline__ float fma_f16f16f32(uint32_t a_lo_half, uint32_t b_ha
 template <int NP, int BT, bool F16>
 struct Weights;
 
+// hs byte offset of a slot, extracted from its packed register at every use.  volatile: the
+// compiler would otherwise hoist all NP extractions out of the time loop and hold NP more
+// registers live (one shift per gather is free on the idle ALU pipe; the registers are not).
+#ifndef SRNN_HOIST_OFFSETS
+__device__ __forceinline__ uint32_t xoff_hi16(uint32_t w) {
+    uint32_t o;
+    asm volatile("shr.b32 %0, %1, 16;" : "=r"(o) : "r"(w));
+    return o;
+}
+__device__ __forceinline__ uint32_t xoff_lo16(uint32_t w) {
+    uint32_t o;
+    asm volatile("and.b32 %0, %1, 65535;" : "=r"(o) : "r"(w));
+    return o;
+}
+__device__ __forceinline__ uint32_t xoff_u16(uint32_t w) {  // 16-byte units in the high half -> bytes
+    uint32_t o;
+    asm volatile("{\n.reg .b32 t;\nshr.b32 t, %1, 12;\nand.b32 %0, t, 1048560;\n}" : "=r"(o) : "r"(w));
+    return o;
+}
+#else
+__device__ __forceinline__ uint32_t xoff_hi16(uint32_t w) { return w >> 16; }
+__device__ __forceinline__ uint32_t xoff_lo16(uint32_t w) { return w & 0xffffu; }
+__device__ __forceinline__ uint32_t xoff_u16(uint32_t w) { return (w >> 12) & 0xffff0u; }
+#endif
+
 // The operate loop runs in groups of GS slots: all GS shared-memory loads of
 // a group are issued before its FMAs (memory-level parallelism), and the
 // warp-uniform slot count n_w is checked once per group.  Slots between n_w
@@ -276,7 +301,7 @@ struct Weights<NP, BT, false> {
 #ifndef SRNN_F32_UNPACKED
     uint32_t offp[(NP + 1) / 2];
     __device__ __forceinline__ uint32_t off(int i) const {
-        return (i & 1) ? (offp[i >> 1] >> 16) : (offp[i >> 1] & 0xffffu);
+        return (i & 1) ? xoff_hi16(offp[i >> 1]) : xoff_lo16(offp[i >> 1]);
     }
 #else  // A/B: one offset register per pair
     uint32_t offp[NP];
@@ -368,7 +393,7 @@ struct Weights<NP, BT, true> {
 #pragma unroll
                     for (int j = 0; j < GS; ++j) {
                         if (i0 + j < NP) {
-                            const uint32_t o = (pw[i0 + j] >> 12) & 0xffff0u;
+                            const uint32_t o = xoff_u16(pw[i0 + j]);
                             ha[j] = *reinterpret_cast<const uint4*>(hs + o);
                             hb[j] = *reinterpret_cast<const uint4*>(hs2 + o);
                         }
@@ -389,7 +414,7 @@ struct Weights<NP, BT, true> {
                     uint4 h[GS];
 #pragma unroll
                     for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) h[j] = *reinterpret_cast<const uint4*>(hs + ((pw[i0 + j] >> 12) & 0xffff0u));
+                        if (i0 + j < NP) h[j] = *reinterpret_cast<const uint4*>(hs + (xoff_u16(pw[i0 + j])));
 #pragma unroll
                     for (int j = 0; j < GS; ++j) {
                         if (i0 + j < NP) {
@@ -408,7 +433,7 @@ struct Weights<NP, BT, true> {
                     uint2 h[GS];
 #pragma unroll
                     for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) h[j] = *reinterpret_cast<const uint2*>(hs + (pw[i0 + j] >> 16));
+                        if (i0 + j < NP) h[j] = *reinterpret_cast<const uint2*>(hs + xoff_hi16(pw[i0 + j]));
 #pragma unroll
                     for (int j = 0; j < GS; ++j) {
                         if (i0 + j < NP) {
@@ -423,7 +448,7 @@ struct Weights<NP, BT, true> {
                     uint32_t h[GS];
 #pragma unroll
                     for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) h[j] = *reinterpret_cast<const uint32_t*>(hs + (pw[i0 + j] >> 16));
+                        if (i0 + j < NP) h[j] = *reinterpret_cast<const uint32_t*>(hs + xoff_hi16(pw[i0 + j]));
 #pragma unroll
                     for (int j = 0; j < GS; ++j) {
                         if (i0 + j < NP) {
@@ -435,7 +460,7 @@ struct Weights<NP, BT, true> {
                     uint32_t h[GS];
 #pragma unroll
                     for (int j = 0; j < GS; ++j)
-                        if (i0 + j < NP) h[j] = *reinterpret_cast<const unsigned short*>(hs + (pw[i0 + j] >> 16));
+                        if (i0 + j < NP) h[j] = *reinterpret_cast<const unsigned short*>(hs + xoff_hi16(pw[i0 + j]));
 #pragma unroll
                     for (int j = 0; j < GS; ++j)
                         if (i0 + j < NP) acc[0] = fma_f16f16f32(pw[i0 + j], h[j], acc[0]);
@@ -645,7 +670,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // tensor-core comparator (NP register A fragments per lane, MT row tiles).
 template <int NP, int BT, int G, bool F16, int MT = 0>
 __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16, BT>::value, 1)
-    srnn_persistent_kernel(const RecParams p) {
+    srnn_persistent_kernel(const __grid_constant__ RecParams p) {
     using F = Fmt<F16, BT>;
     constexpr bool DENSE = MT > 0;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -659,20 +684,47 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     const int umax_bt = p.units_max * BT;
     // shared memory: hs [H][BT] at offset 0 (E bytes per unit), then fp32 areas
     unsigned char* hs = smem;
-    const size_t hs_bytes = DENSE ? static_cast<size_t>(p.hs_rows) * 16 : static_cast<size_t>(H) * F::E;
+    // (column split: only this CTA's column half is staged, hsplit units; must match smem_for)
+    const size_t hs_bytes = DENSE ? static_cast<size_t>(p.hs_rows) * 16
+                                  : static_cast<size_t>(p.csplit != 0 ? p.hsplit : H) * F::E;
     float* zs = reinterpret_cast<float*>(smem + ((hs_bytes + 15) & ~static_cast<size_t>(15)));
     // zs: one BT-row of reduced sums per (virtual) row -- heavy rows split into pieces
     // (class balancing) have several, summed in the epilogue
     const int zrows = max(G * p.units_max, p.vrows_max);
-    float* bpsb = zs + zrows * BT;                           // b' double buffer: [2][item][G]
+    const bool CS = !DENSE && p.csplit != 0;  // column split over a 2-CTA cluster
+    const int crank = cta & 1;                // rank in the cluster (column half) when CS
+    if (CS) {  // the column split needs the 2-CTA cluster launch (srnn_api.cpp / launch_one)
+        uint32_t ncl, rk;
+        asm("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncl));
+        asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rk));
+        if (ncl != 2u || rk != static_cast<uint32_t>(crank)) {
+            if (threadIdx.x == 0) atomicCAS(p.status, 0, -4 /* SRNN_ERR_STATE */);
+            return;
+        }
+    }
+    const int zbuf = zrows * BT;                             // floats of one zs buffer (two when CS: step parity)
+    float* bpsb = zs + (CS ? 2 : 1) * zbuf;                  // b' double buffer: [2][item][G]
     float* cs = bpsb + 2 * G * umax_bt;                      // LSTM c / GRU fp32 h_{t-1}: [n_tiles][item]
-    int* s_abort = reinterpret_cast<int*>(cs + (G >= 3 ? p.n_tiles * umax_bt : 0));
+    // b' TMA windows [2][G][kBpWin][BT][boxu] + two mbarriers (only when the host passed a map)
+#ifdef SRNN_ABL_NO_BP_TMA
+    constexpr bool bp_tma = false;
+#else
+    const bool bp_tma = G == 1 && p.bp_tma != 0;  // RNN cells only (the gate cells keep cp.async: registers)
+#endif
+    const int boxu = p.bp_boxu;
+    float* bpw = reinterpret_cast<float*>(  // TMA destination: 128-byte aligned
+        (reinterpret_cast<uintptr_t>(cs + (G >= 3 ? p.n_tiles * umax_bt : 0)) + (bp_tma ? 127 : 0)) &
+        ~static_cast<uintptr_t>(bp_tma ? 127 : 0));
+    uint64_t* bp_mbar = reinterpret_cast<uint64_t*>(bpw + (bp_tma ? 2 * G * kBpWin * BT * boxu : 0));
+    int* s_abort = reinterpret_cast<int*>(bp_mbar + (bp_tma ? 2 : 0));
     unsigned char* ws = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(s_abort + 1) + 15) & ~static_cast<uintptr_t>(15));  // smem weight tier
 
     const int L = DENSE ? 32 : p.lanes_per_row;
     const int n_w = DENSE ? 0 : p.warp_slots[cta * (p.threads >> 5) + warp];
     const int n_chunks = p.tile_bytes >> 4;     // 16-byte chunks of one exchange image
+    const int c_lo = CS && crank ? (p.hsplit * F::E) >> 4 : 0;             // first chunk this CTA stages
+    const int n_ch = CS ? (crank ? n_chunks - c_lo : (p.hsplit * F::E) >> 4) : n_chunks;
     const unsigned char* hs2 = hs + H * 16;     // BT = 16: second hs plane
     const int GH = G * H;
     // values after the last unit that pad the image to whole chunks (written by the last CTA)
@@ -714,10 +766,29 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     const int krow = (warp << (5 - lg_l)) + (lane >> lg_l);  // local row of this lane
     // lane of the row that stores sample sbase (L >= BT), hoisted out of the time loop
     const int* pc = p.piece0 != nullptr ? p.piece0 + cta * (G * p.units_max + 1) : nullptr;
-    const int n_vrows = pc != nullptr ? __ldg(pc + G * U) : G * U;  // (virtual) rows of this CTA
+    // column split: this CTA's rows are all G * UQ rows of its cluster's units (its column half)
+    const int UQ = CS ? p.cta_vunit0[cta + 1] - p.cta_vunit0[cta] : U;
+    const int lu_off = CS && crank ? UQ - U : 0;  // cluster-local index of this CTA's first own unit
+    const int n_vrows = CS ? G * UQ : pc != nullptr ? __ldg(pc + G * U) : G * U;  // (virtual) rows of this CTA
     const bool zs_writer = (lane & (L - 1)) < BT && krow < n_vrows;
     // reduced sum of local row k (gate * U + unit), sample b: the sum of its pieces
+    float* zsp = zs;  // this step's zs buffer (column split: alternates with the step parity)
     auto zval = [&](int k, int b) -> float {
+        if (CS) {  // own partial + the peer's (DSMEM), always in the order half 0 + half 1
+            const int g = G == 1 ? 0 : k / U, u = G == 1 ? k : k - g * U;
+            const float* a = zsp + (g * UQ + lu_off + u) * BT + b;
+            const uint32_t la = static_cast<uint32_t>(__cvta_generic_to_shared(a));
+            uint32_t ra;
+            float peer;
+#ifdef SRNN_DBG_CS_NODSMEM
+            peer = 0.0f; (void)la; (void)ra;
+#else
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(crank ^ 1));
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(peer) : "r"(ra) : "memory");
+#endif
+            const float mine = *a;
+            return crank == 0 ? mine + peer : peer + mine;
+        }
         if (pc == nullptr) return zs[k * BT + b];
         const int v1 = __ldg(pc + k + 1);
         float z = 0.0f;
@@ -727,10 +798,13 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     // epilogue fast path (one item per thread): item e1 = tid -> (unit, sample)
     // exchange positions vs hidden units: the same unless the plan balances classes (unit_perm)
     auto real_unit = [&](int pos) { return p.unit_perm != nullptr ? __ldg(p.unit_perm + pos) : pos; };
-    const int e1 = tid, e1_b = tid % BT, e1_unit = (tid < U * BT) ? real_unit(u0 + tid / BT) : 0;
+    const int e1 = tid, e1_b = tid % BT;
     const bool e1_ok = tid < n_items;
+    const int e1_unit = e1_ok ? real_unit(u0 + e1 / BT) : 0;
     const float* zs_e1 = zs + e1;
     float* const y_e1 = (p.y != nullptr && e1_ok) ? p.y + e1_b * p.y_bstride + e1_unit : nullptr;
+    const float* const bp_e1 = p.bprime + static_cast<size_t>(e1_b) * GH + e1_unit;
+    const int xo_e1 = e1_ok ? F::offset(H, u0 + e1 / BT, e1_b) : 0;  // exchange offset of item e1 in a tile image
     const bool row_leader = (lane & (L - 1)) == 0 && krow < n_vrows;
     if (tid == 0) *s_abort = 0;
 
@@ -765,7 +839,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     // ---- exchange re-initialisation: the stale values of both parities must carry the
     // tags of global steps epoch - 2 / epoch - 1 (the host asks for it when the buffers
     // are fresh or were idle for some tiles; an aborted launch marks them dirty) ----
-    if (p.reinit || *reinterpret_cast<volatile int32_t*>(p.xdirty) != 0) {
+    if (!CS && (p.reinit || *reinterpret_cast<volatile int32_t*>(p.xdirty) != 0)) {  // CS: the host re-fills
         for (int q = 0; q < 2; ++q) {
             const uint32_t g = p.epoch + static_cast<uint32_t>(q);  // first step of this launch in parity g & 1
             const uint32_t stale = ((g - 2u) >> 1) & 1u;
@@ -795,6 +869,33 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
             publish(0, k, e, ok, h);
         }
     }
+    // b' windows by TMA: window w (steps w*kBpWin + 1 ..) lands in slot w & 1; phase (w >> 1) & 1
+    auto bp_issue = [&](int w) {
+        const int slot = w & 1;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // slot's previous generic reads
+        const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(bp_mbar + slot));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
+                     "r"(static_cast<uint32_t>(G * kBpWin * BT * boxu * 4))
+                     : "memory");
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+            const uint32_t dst = static_cast<uint32_t>(
+                __cvta_generic_to_shared(bpw + static_cast<size_t>(slot * G + q) * kBpWin * BT * boxu));
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                ::"r"(dst), "l"(&p.bp_map), "r"(q * H + (u0 & ~3)), "r"(0), "r"(w * kBpWin), "r"(mb)
+                : "memory");
+        }
+    };
+    if (bp_tma && tid == 0) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bp_mbar + i)))
+                         : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&p.bp_map) : "memory");
+        bp_issue(0);
+    }
     const bool grid_sync = (p.flags & kFlagGridSync) != 0u;
     if (grid_sync) cg::this_grid().sync();
     __syncthreads();
@@ -805,8 +906,11 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     bool bp_failed = false;  // the b' readiness wait timed out: abort at the next barrier
     const bool bp_pipelined = p.bp_ready != nullptr;
     // one item per thread (the common case): b' source of item e1 = tid hoisted out of the time loop
-    const float* const bp_e1 = p.bprime + static_cast<size_t>(e1_b) * GH + e1_unit;
     auto issue_bprime = [&](int s, int k, int b) {
+        if (bp_tma) {  // one thread loads window w + 1 during the first step of window w (s = that step + 1)
+            if (tid == 0 && (s - 2) % kBpWin == 0 && (s - 2 + kBpWin) < p.T) bp_issue((s - 2) / kBpWin + 1);
+            return;
+        }
         float* dstb = bpsb + b * G * umax_bt;
         if (bp_pipelined && tid < n_items && static_cast<int32_t>(bp_seen - p.bp_ready_base) < s) {
             Watchdog wdb{0ull, 0u};
@@ -865,26 +969,30 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
             SRNN_STAMP(0, clock64());
             // ---- load: h_{s-1} tile k -> hs; the first poll round goes out first ----
             const uint32_t g_prev = p.epoch + static_cast<uint32_t>(s - 1);  // global step of h_{s-1}
+            // column split: only the chunks of this CTA's column half [c_lo, c_lo + n_ch)
             const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
-                p.xbuf + static_cast<size_t>((g_prev & 1u) * p.xbuf_tiles + k) * p.tile_bytes);
+                p.xbuf + static_cast<size_t>((g_prev & 1u) * p.xbuf_tiles + k) * p.tile_bytes) + c_lo;
             // fp16 tiles of <= 4 samples send the first poll round before the b' prefetch (the
             // round trip hides the prefetch's address work); wider / fp32 tiles hold more chunks
             // per thread, whose registers would stay live across it (measured: slower), so they
             // poll after it
             constexpr bool kEarlyPoll = F16 && BT <= 4;
-            if (kEarlyPoll && tid < n_loaders) poll.issue(src, tid, n_chunks, n_loaders);
+            if (kEarlyPoll && tid < n_loaders) poll.issue(src, tid, n_ch, n_loaders);
             // b' of the NEXT tile -> shared memory (cp.async, double-buffered) while the
             // poll loads are in flight; it lands during this whole tile (this tile's b'
             // was issued one tile earlier)
             {
                 const int ns = k + 1 < p.n_tiles ? s : s + 1, nk = k + 1 < p.n_tiles ? k + 1 : 0;
+#ifndef SRNN_ABL_NO_BP
                 if (ns <= p.T) issue_bprime(ns, nk, buf ^ 1);
+#endif
                 cp_async_commit();
             }
-            float* bps = bpsb + buf * G * umax_bt;
-            if (!kEarlyPoll && tid < n_loaders) poll.issue(src, tid, n_chunks, n_loaders);
+
+            if (!kEarlyPoll && tid < n_loaders) poll.issue(src, tid, n_ch, n_loaders);
+            bool failed = bp_failed;
             if (tid < n_loaders &&
-                !poll.complete(src, hs, n_chunks, (g_prev >> 1) & 1u, !grid_sync, p.status, p.timeout_ns,
+                !poll.complete(src, hs, n_ch, (g_prev >> 1) & 1u, !grid_sync, p.status, p.timeout_ns,
                                p.poll_backoff_ns, n_loaders,
 #ifdef SRNN_PROFILE
                                prof_all ? &rounds : nullptr, prof ? prof + 10 : nullptr
@@ -892,17 +1000,24 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                                nullptr, nullptr
 #endif
                                ))
-                *s_abort = 1;
-            if (bp_failed) *s_abort = 1;
+                failed = true;
 #ifdef SRNN_PROFILE
             if (prof_all) atomicMax(reinterpret_cast<unsigned long long*>(prof_all + 9), static_cast<unsigned long long>(rounds));
 #endif
+            if (failed) *s_abort = 1;
             __syncthreads();
             SRNN_STAMP(1, clock64());
             SRNN_STAMP(8, rounds);
             SRNN_STAMP(12, static_cast<long long>(globaltimer_ns()));
-            if (*s_abort) goto done;
+            // abort check: the flag is read here, the branch is taken after the operate (its
+            // latency hides behind it; an aborted step computes on stale hs but never publishes)
+            const int aborted = *reinterpret_cast<volatile int*>(s_abort);
 
+#ifdef SRNN_ABL_EARLY_ABORT
+            if (aborted) goto done;
+#endif
+
+            if (CS) zsp = zs + (s & 1) * zbuf;
             // ---- operate + reduce ----
             if constexpr (DENSE) {
                 DW.operate(hs, reinterpret_cast<const uint4*>(ws), red, p.dense_kpw, dense_nf_reg, nt);
@@ -925,8 +1040,10 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                 float acc[BT];
 #pragma unroll
                 for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
+#ifndef SRNN_ABL_NO_OP  // A/B ablation builds only (scripts/abl.sh): phase costs
                 W.operate(acc, hs, n_w, hs2);
                 if (n_w > NP) operate_smem_tier<BT, F16>(acc, hs, ws, NP, n_w, nt, hs2);
+#endif
                 SRNN_STAMP(4, clock64());
                 // ---- reduce over the row's L lanes, fixed order ----
                 // L >= BT: log2(BT) halving levels (each lane keeps half of its
@@ -935,7 +1052,11 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                 // the row then holds the sum of sample bitrev(j mod BT).
                 // L < BT: plain xor butterfly, the row leader holds all samples.
                 int sbase = 0;
+#ifdef SRNN_ABL_NO_BFLY
+                if (false) {
+#else
                 if (L >= BT) {
+#endif
 #pragma unroll
                     for (int lvl = 0, half = BT / 2; half >= 1; ++lvl, half /= 2) {
                         const int m = 1 << lvl;
@@ -951,7 +1072,11 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
 #pragma unroll
                     for (int m = BT; m <= 16; m <<= 1)
                         if (m < L) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], m);
-                } else {
+                } else
+#ifdef SRNN_ABL_NO_BFLY
+                if (false)
+#endif
+                {
 #pragma unroll
                     for (int m = 16; m >= 1; m >>= 1) {
                         if (m < L) {  // warp-uniform
@@ -962,34 +1087,81 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                 }
                 SRNN_STAMP(5, clock64());
                 if (L >= BT) {
-                    if (zs_writer) zs[krow * BT + sbase] = acc[0];
+                    if (zs_writer) zsp[krow * BT + sbase] = acc[0];
                 } else if (row_leader) {
 #pragma unroll
-                    for (int b = 0; b < BT; ++b) zs[krow * BT + b] = acc[b];
+                    for (int b = 0; b < BT; ++b) zsp[krow * BT + b] = acc[b];
+                }
+            }
+            if (!CS && aborted) goto done;
+            if (bp_tma && (s - 1) % kBpWin == 0) {  // first step of a b' window: wait for its TMA load
+                const int w = (s - 1) / kBpWin;
+                const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(bp_mbar + (w & 1)));
+                Watchdog wdb{0ull, 0u};
+                uint32_t done_ = 0;
+                while (true) {
+                    asm volatile(
+                        "{\n.reg .pred P;\nmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\nselp.u32 %0, 1, 0, P;\n}"
+                        : "=r"(done_)
+                        : "r"(mb), "r"(static_cast<uint32_t>((w >> 1) & 1))
+                        : "memory");
+                    if (done_) break;
+                    if (watchdog_tick(wdb, p.status, p.timeout_ns)) break;  // the next poll aborts the launch
                 }
             }
             asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's b' (the newest group may pend)
             SRNN_STAMP(6, clock64());
-            __syncthreads();
+            if (CS) {
+                // both CTAs' partial sums are complete (release / acquire across the cluster); the
+                // pair takes the same abort decision (own flag or the peer's) so neither waits alone
+                asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+                const uint32_t la = static_cast<uint32_t>(__cvta_generic_to_shared(s_abort));
+                uint32_t ra;
+                int peer_ab;
+#ifdef SRNN_DBG_CS_NODSMEM
+                peer_ab = 0; (void)la; (void)ra;
+#else
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(crank ^ 1));
+                asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(peer_ab) : "r"(ra) : "memory");
+#endif
+                if (aborted | peer_ab) goto done;
+            } else {
+                __syncthreads();
+            }
             SRNN_STAMP(2, clock64());
 
             // ---- epilogue: activation / gates, y, tagged publish of h_s ----
+            // b' of this (step, tile): bps[e * G + q] (cp.async double buffer), or the TMA window
+            // element (q, j, b, unit) at bpt[q * kBpWin * BT * boxu + b * boxu + (u0 & 3) + unit] (the box
+            // starts at the 16-byte aligned column u0 & ~3)
+            const float* bps = bpsb + buf * G * umax_bt;
+            const float* bpt = bpw + static_cast<size_t>((((s - 1) / kBpWin) & 1) * G * kBpWin + (s - 1) % kBpWin) * BT * boxu;
+            auto bpv = [&](int e, int q) -> float {
+                return bp_tma ? bpt[q * kBpWin * BT * boxu + (e % BT) * boxu + (u0 & 3) + e / BT] : bps[e * G + q];
+            };
             if (jitter0) {
                 const uint32_t r = (static_cast<uint32_t>(cta) * 2654435761u) ^ (static_cast<uint32_t>(s * 40503 + k));
                 __nanosleep((r >> 7) & 2047u);
             }
             if (G == 1 && item_rounds == 1) {
-                // fast path (one item per thread, RNN): addresses hoisted out of the time loop
+                // fast path (one item per thread, RNN): hoisted offsets; the exchange store goes
+                // out first (it is the step's critical path), y / h_T after it
                 float h = 0.0f;
-                if (e1_ok) {
-                    h = activation<F16>(act, (pc == nullptr ? zs_e1[0] : zval(e1 / BT, e1_b)) + bps[e1]);
-                    const int bg = k * BT + e1_b;
-                    if (bg < p.B) {
-                        if (y_e1 != nullptr) y_e1[(s - 1) * p.y_tstride + k * BT * p.y_bstride] = h;
-                        if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(bg) * H + e1_unit] = h;
-                    }
+                const uint32_t g = p.epoch + static_cast<uint32_t>(s);  // parity g & 1, tag (g >> 1) & 1
+                if (e1_ok) h = activation<F16>(act, (pc == nullptr && !CS ? zs_e1[0] : zval(e1 / BT, e1_b)) + bpv(e1, 0));
+#ifdef SRNN_ABL_Y_FIRST
+                if (y_e1 != nullptr && k * BT + e1_b < p.B) y_e1[(s - 1) * p.y_tstride + k * BT * p.y_bstride] = h;
+#endif
+                if (e1_ok && !(drop_cta && s == 2))
+                    store_tagged(p.xbuf + static_cast<size_t>((g & 1u) * p.xbuf_tiles + k) * p.tile_bytes, xo_e1, h,
+                                 (g >> 1) & 1u);
+                publish(s, k, e1, false, 0.0f);  // only the pad values of the last chunk (last CTA)
+                if (e1_ok && k * BT + e1_b < p.B) {
+#if !defined(SRNN_ABL_NO_Y) && !defined(SRNN_ABL_Y_FIRST)
+                    if (y_e1 != nullptr) y_e1[(s - 1) * p.y_tstride + k * BT * p.y_bstride] = h;
+#endif
+                    if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(k * BT + e1_b) * H + e1_unit] = h;
                 }
-                publish(s, k, e1, e1_ok, h);
             } else
             for (int j = 0; j < item_rounds; ++j) {
                 const int e = tid + j * nt;
@@ -998,22 +1170,22 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                 if (ok) {
                     const int unit = real_unit(u0 + e / BT), bg = k * BT + e % BT;
                     if (G == 1) {
-                        h = activation<F16>(p.act, zval(e / BT, e % BT) + bps[e]);
+                        h = activation<F16>(p.act, zval(e / BT, e % BT) + bpv(e, 0));
                     } else if (G == 3) {
                         // GRU (R15): r, z from the product; the reset gate scales the
                         // n-gate product + b_hn; the previous h of this item stays in fp32 in cs
-                        const float r = sigmoid_g<F16>(zval(0 * U + e / BT, e % BT) + bps[e * G + 0]);
-                        const float u = sigmoid_g<F16>(zval(1 * U + e / BT, e % BT) + bps[e * G + 1 % G]);
+                        const float r = sigmoid_g<F16>(zval(0 * U + e / BT, e % BT) + bpv(e, 0));
+                        const float u = sigmoid_g<F16>(zval(1 * U + e / BT, e % BT) + bpv(e, 1 % G));
                         const float bhn = p.bias_hn != nullptr ? p.bias_hn[unit] : 0.0f;
-                        const float n = tanh_g<F16>(fmaf(r, zval(2 * U + e / BT, e % BT) + bhn, bps[e * G + 2 % G]));
+                        const float n = tanh_g<F16>(fmaf(r, zval(2 * U + e / BT, e % BT) + bhn, bpv(e, 2 % G)));
                         float* hp = &cs[k * umax_bt + e];
                         h = fmaf(u, *hp - n, n);  // (1 - u) n + u h_prev
                         *hp = h;
                     } else {
-                        const float zi = zval(0 * U + e / BT, e % BT) + bps[e * G + 0];
-                        const float zf = zval(1 * U + e / BT, e % BT) + bps[e * G + 1 % G];
-                        const float zg = zval(2 * U + e / BT, e % BT) + bps[e * G + 2 % G];
-                        const float zo = zval(3 * U + e / BT, e % BT) + bps[e * G + 3 % G];
+                        const float zi = zval(0 * U + e / BT, e % BT) + bpv(e, 0);
+                        const float zf = zval(1 * U + e / BT, e % BT) + bpv(e, 1 % G);
+                        const float zg = zval(2 * U + e / BT, e % BT) + bpv(e, 2 % G);
+                        const float zo = zval(3 * U + e / BT, e % BT) + bpv(e, 3 % G);
                         float* cp = &cs[k * umax_bt + e];
                         const float c = sigmoid_g<F16>(zf) * (*cp) + sigmoid_g<F16>(zi) * tanh_g<F16>(zg);
                         *cp = c;
@@ -1030,10 +1202,12 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
             SRNN_STAMP(3, clock64());
             SRNN_STAMP(11, static_cast<long long>(globaltimer_ns()));
             if (grid_sync) cg::this_grid().sync();
+#ifndef SRNN_ABL_NO_BAR3
             // Start polling for the next tile only once this CTA has published:
             // early pollers only add stale round trips and contend with the
             // epilogue warps for the LSU (measured: -6..10% step time).
             __syncthreads();
+#endif
             SRNN_STAMP(7, clock64());
             buf ^= 1;
             if (p.progress != nullptr && tid == 0 && k == p.n_tiles - 1 &&
@@ -1044,6 +1218,8 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
         }
     }
 done:
+    // column split: the pair leaves together (the peer may still read this CTA's zs / flag)
+    if (CS) asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     // An aborted launch (watchdog / lost message) still releases the host pipeline's
     // y-copy waits on the progress counter (the host re-reads the counter on error).
     if (*s_abort && tid == 0) {
@@ -1073,6 +1249,34 @@ static int launch_one(const RecParams& p, int num_ctas, size_t smem, void* strea
             if (e != cudaSuccess) return static_cast<int>(e);
             *max_blocks_out = p.threads > (MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16, BT>::value) ? 0 : nb;
         }
+    }
+    if (p.csplit) {  // column split: 2-CTA clusters, all co-resident (cooperative)
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(num_ctas);
+        lc.blockDim = dim3(p.threads);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = static_cast<cudaStream_t>(stream);
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeCooperative;
+        at[1].val.cooperative = 1;
+        lc.attrs = at;
+        lc.numAttrs = 2;
+        if (max_blocks_out != nullptr && *max_blocks_out > 0) {
+            int ncl = 0;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            e = cudaOccupancyMaxActiveClusters(&ncl, fn, &lc);
+            if (e != cudaSuccess) return static_cast<int>(e);
+            if (2 * ncl < num_ctas) *max_blocks_out = 0;  // the pairs do not all fit at once
+            lc.numAttrs = 2;
+        }
+        if (query_only) return 0;
+        e = cudaLaunchKernelEx(&lc, fn, p);
+        return static_cast<int>(e);
     }
     if (query_only) return 0;
     void* args[] = {const_cast<RecParams*>(&p)};

@@ -180,15 +180,20 @@ def test_plan_create_rejects_bad_config_and_state_errors():
     assert lib.srnn_forward(m.handle, 1, 1, None, None, None, None, None, None, None) == -4  # host-only -> STATE
 
 
-def test_not_on_chip_is_reported():
+def test_not_on_chip_is_reported(monkeypatch):
     # 65536 hidden at 50% density: ~2.1e9 pairs cannot be register-resident
     with pytest.raises(SrnnError) as e:
         SparseRNN(65536, 16, 1, 1, 0.5, flags=FLAG_HOST_ONLY, prec="fp32")
     assert e.value.code == -2
-    # fp16 register pairs hold the staged-h byte offset in 16 bits: H <= 32768
+    # fp16 register pairs hold the staged-h byte offset in 16 bits: H <= 32768 unsplit ...
+    monkeypatch.setenv("SRNN_NO_AUTO_SPLIT", "1")
     with pytest.raises(SrnnError) as e:
         SparseRNN(40000, 16, 1, 1, 0.001, flags=FLAG_HOST_ONLY, prec="fp16")
     assert e.value.code == -7
+    # ... and the planner takes the column split (each CTA stages half of h) by itself
+    monkeypatch.delenv("SRNN_NO_AUTO_SPLIT")
+    m = SparseRNN(40000, 16, 1, 1, 0.001, flags=FLAG_HOST_ONLY, prec="fp16")
+    assert m.info()["column_split"] == 1
 
 
 def test_density_zero_and_one_layouts():

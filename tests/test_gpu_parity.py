@@ -757,3 +757,78 @@ def test_class_balance_integer_exact(cuda_device):
     o = oracle.forward(prob)
     a = run_gpu(prob, "fp32", flags=FLAG_CLASS_BALANCE)
     assert np.array_equal(a["y"].astype(np.float64), o["y"])
+
+
+@pytest.mark.parametrize("prec,cell,H,B,T,d,act", [
+    ("fp16", "rnn", 1000, 4, 12, 0.3, "relu"),
+    ("fp32", "rnn", 1000, 4, 12, 0.3, "relu"),
+    ("fp16", "rnn", 777, 3, 20, 0.1, "tanh"),     # ragged H (odd halves), B < tile
+    ("fp32", "rnn", 513, 6, 9, 0.05, "identity"),  # two batch tiles
+    ("fp16", "rnn", 2304, 8, 10, 0.3, "relu"),    # one tile of 8 (LDS.128)
+    ("fp16", "lstm", 1024, 4, 10, 0.125, "tanh"),
+    ("fp16", "gru", 600, 5, 8, 0.1, "tanh"),
+    ("fp16", "rnn", 300, 1, 16, 0.1, "relu"),     # BT = 1
+])
+def test_column_split_parity(cuda_device, prec, cell, H, B, T, d, act):
+    """SRNN_FLAG_COLUMN_SPLIT ("split one row among multiple blocks"): 2-CTA clusters,
+    each CTA one column half, partial sums added through DSMEM -- every output vs the oracle."""
+    from paper_1804_10223_b200 import FLAG_COLUMN_SPLIT
+    prob = inputs.make_problem(H, H, B, T, d, cell=cell, act=act, h0="random", c0="random", seed_offset=H + B)
+    g, o, err = check(prob, prec, flags=FLAG_COLUMN_SPLIT)
+    assert g["info"]["column_split"] == 1 and g["info"]["num_ctas"] % 2 == 0
+
+
+def test_column_split_integer_exact(cuda_device):
+    """Integer-exact inputs: the split sums (half 0 + half 1) are exact, so the split plan equals
+    the oracle bit for bit, like the unsplit plan."""
+    from paper_1804_10223_b200 import FLAG_COLUMN_SPLIT
+    prob = inputs.make_integer_problem(500, 48, 4, 6, 0.02, act="identity")
+    o = oracle.forward(prob)
+    a = run_gpu(prob, "fp32", flags=FLAG_COLUMN_SPLIT)
+    assert np.array_equal(a["y"].astype(np.float64), o["y"])
+    # fp16 h rounds the growing integers (> 2^10) the same way in both plans: split == unsplit
+    b = run_gpu(prob, "fp16", flags=FLAG_COLUMN_SPLIT)
+    c = run_gpu(prob, "fp16")
+    assert np.array_equal(b["y"], c["y"])
+
+
+def test_column_split_jitter_deterministic(cuda_device):
+    """Random per-CTA delays change nothing (the pair's DSMEM sum has a fixed order)."""
+    from paper_1804_10223_b200 import FLAG_COLUMN_SPLIT
+    prob = inputs.make_problem(1152, 1152, 4, 24, 0.1, act="tanh", h0="random")
+    a = run_gpu(prob, "fp16", flags=FLAG_COLUMN_SPLIT)
+    b = run_gpu(prob, "fp16", flags=FLAG_COLUMN_SPLIT | FLAG_DEBUG_JITTER)
+    assert np.array_equal(a["y"], b["y"])
+
+
+def test_column_split_lost_message_watchdog(cuda_device, monkeypatch):
+    """A lost exchange message under the column split ends the launch through the watchdog (both
+    CTAs of every pair leave together: no cluster-barrier hang)."""
+    import torch
+    from paper_1804_10223_b200 import FLAG_COLUMN_SPLIT, SrnnError
+    from paper_1804_10223_b200._lib import FLAG_DEBUG_DROP_PUBLISH
+    monkeypatch.setenv("SRNN_TIMEOUT_MS", "200")
+    prob = inputs.make_problem(1000, 1000, 4, 8, 0.1, act="tanh")
+    m = from_problem(prob, prec="fp16", flags=FLAG_COLUMN_SPLIT | FLAG_DEBUG_DROP_PUBLISH)
+    m.forward(torch.from_numpy(prob["x"]).cuda())
+    torch.cuda.synchronize()
+    with pytest.raises(SrnnError) as e:
+        m.status()
+    assert e.value.code == -6
+    m.close()
+
+
+@pytest.mark.parametrize("H,d", [(36000, 0.0025), (41000, 0.0025)])
+def test_column_split_capacity_beyond_frontier(cuda_device, monkeypatch, H, d):
+    """(f)4: the column split stages half of h, so fp16 layers past the unsplit limit (16-bit
+    staged offsets: H <= 32768 at one sample per tile; host-only frontier 32680 @ 0.25%) run on
+    chip -- every output checked; the unsplit plan of the same layer is refused."""
+    from paper_1804_10223_b200 import FLAG_COLUMN_SPLIT, FLAG_HOST_ONLY, SrnnError
+    prob = inputs.make_problem(H, 64, 1, 5, d, act="tanh", h0="random")
+    monkeypatch.setenv("SRNN_NO_AUTO_SPLIT", "1")  # the unsplit plan is refused ...
+    with pytest.raises(SrnnError):
+        from_problem(prob, prec="fp16", flags=FLAG_HOST_ONLY)
+    monkeypatch.delenv("SRNN_NO_AUTO_SPLIT")  # ... the planner splits by itself, or on request
+    assert from_problem(prob, prec="fp16", flags=FLAG_HOST_ONLY).info()["column_split"] == 1
+    g, o, err = check(prob, "fp16", flags=FLAG_COLUMN_SPLIT)
+    print(H, d, g["info"])
