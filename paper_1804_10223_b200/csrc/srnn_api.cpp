@@ -96,6 +96,8 @@ struct srnn_plan {
     bool k8 = false;               // sparse fp16 tile-of-4 plan that needs 8 poll slots per thread
     // column split (SRNN_FLAG_COLUMN_SPLIT): 2-CTA clusters, each CTA one column half
     bool csplit = false;
+    bool auto_split = false;   // the planner chose the split (load_weights falls back if it does not fit)
+    int bt_unsplit = 0;        // tile width of the unsplit plan (0: the unsplit layer does not fit)
     int hsplit = 0;                       // first column of the second half (units, multiple of 8)
     std::vector<int32_t> unit0_real;      // [num_ctas + 1] units each CTA finalises / publishes
     int32_t* d_vunit0 = nullptr;          // lay.cta_unit0 (virtual: the pair's units per CTA)
@@ -132,7 +134,9 @@ int elem_bytes(bool f16, int bt) { return f16 ? 2 * bt : 4 * bt; }
 
 // b' can come by TMA windows: one batch tile, no unit permutation, 16-byte b' row pitch
 bool bp_tma_ok(const srnn_plan* p, int n_tiles, int units_max) {
+    // (the window buffer is capped at 8 KB of shared memory: at large H the weight tier needs it)
     return !p->dense && p->G == 1 && n_tiles == 1 && p->cfg.hidden % 4 == 0 && bp_box_units(units_max) <= 256 &&
+           bp_tma_smem_bytes(p->G, p->BT, units_max) <= 8192 + 144 &&
            (p->cfg.flags & SRNN_FLAG_CLASS_BALANCE) == 0 && std::getenv("SRNN_NO_BP_TMA") == nullptr;
 }
 
@@ -516,6 +520,8 @@ srnn_status_t srnn_plan_create(const srnn_config_t* cfg, srnn_plan_t* out) {
     if (!split && split_ok && c.hidden >= 2 * p->sm_count && std::getenv("SRNN_NO_AUTO_SPLIT") == nullptr) {
         const int b0 = tile_for(false), b1 = tile_for(true);
         split = b1 > 0 && (b0 == 0 || (c.batch + b1 - 1) / b1 < (c.batch + b0 - 1) / b0);
+        p->auto_split = split;
+        p->bt_unsplit = b0;
     }
     int bt = tile_for(split);
     // Register budget for the expected pairs: two registers per pair in the hoisted
@@ -742,12 +748,13 @@ search_again:
     // plan exists at all does it accept a spilling one (second pass).
     auto spills = [&](int inst, bool k8) -> bool {
         if (p->host_only) return false;
-        const int key = inst * 64 + p->BT * 4 + (k8 ? 2 : 0) + (p->f16 ? 1 : 0);
+        const int key = inst * 128 + p->BT * 4 + (k8 ? 2 : 0) + (p->f16 ? 1 : 0) + (p->csplit ? 64 : 0);
         for (auto& kv : p->spill_cache)
             if (kv.first == key) return kv.second;
         RecParams q{};
         q.threads = 32;
         q.k8 = k8 ? 1 : 0;
+        q.csplit = p->csplit ? 1 : 0;
         int regs[2] = {0, 0};
         const bool sp = launch_recurrent(inst, p->BT, G, p->f16 ? 1 : 0, q, 1, 0, nullptr, true, regs, nullptr) == 0 &&
                         regs[1] > 0;
@@ -862,6 +869,36 @@ search_again:
         spill_strict = false;
         goto search_again;
     }
+    if (!any && p->csplit && p->auto_split && p->bt_unsplit > 0) {
+        // the automatic column split doubles each CTA's rows: if its lanes cannot hold the half
+        // rows, plan the unsplit layer (more batch tiles) instead
+        p->csplit = p->auto_split = false;
+        p->hsplit = 0;
+        p->unit0_real.clear();
+        p->BT = p->bt_unsplit;
+        p->E = elem_bytes(p->f16, p->BT);
+        p->n_tiles_max = (p->cfg.batch + p->BT - 1) / p->BT;
+        p->tile_bytes = exchange_tile_bytes(H, p->f16, p->BT);
+        p->xbuf_valid_tiles = 0;
+        if (!p->host_only) {
+            DeviceGuard g(p->cfg.device);
+            cudaFree(p->d_xbuf);
+            p->d_xbuf = nullptr;
+            p->xbuf_bytes = 2 * static_cast<size_t>(p->n_tiles_max) * p->tile_bytes;
+            if (cudaMalloc(&p->d_xbuf, p->xbuf_bytes) != cudaSuccess ||
+                cudaMemset(p->d_xbuf, 0, p->xbuf_bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+                return SRNN_ERR_CUDA;
+        }
+        in.H = H;
+        in.rowptr = rowptr;
+        in.col = col;
+        in.val = qval.data();
+        in.cta_unit0 = nullptr;
+        in.BT = p->BT;
+        in.E = p->BT == 16 ? 16 : p->E;
+        spill_strict = true;
+        goto search_again;
+    }
     if (!any) return SRNN_ERR_NOT_ON_CHIP;
     // Re-pack at the chosen instance width so the image has np_inst slots.
     Layout fin;
@@ -902,7 +939,8 @@ search_again:
         const int ksmall = poll_slots(best_inst, p->f16, p->BT, false);
         const int64_t chunks = exchange_tile_bytes(H, p->f16, p->BT) / 16;  // 16-byte chunks per tile
         const int64_t c = (chunks + best.threads - 1) / best.threads;       // per thread
-        p->k8 = k8_compiled(best_inst, p->f16, p->BT) && ksmall < 8 && (c + 7) / 8 < (c + ksmall - 1) / ksmall;
+        p->k8 = !p->csplit && k8_compiled(best_inst, p->f16, p->BT) && ksmall < 8 &&
+                (c + 7) / 8 < (c + ksmall - 1) / ksmall;
         if (p->k8 && spills(best_inst, true) && !spills(best_inst, false)) p->k8 = false;  // spill-free first
     }
     p->unit_of_pos.clear();

@@ -382,12 +382,24 @@ struct Weights<NP, BT, true> {
 #pragma unroll
         for (int i = 0; i < NP; ++i) pw[i] = i < n_w ? p.img_f16[img0 + static_cast<size_t>(i) * p.threads] : 0u;
     }
-    // hs2: the second sample plane (BT = 16 only)
+    // hs2: the second sample plane (BT = 16 only).  A warp whose slots are all used (the common
+    // case of a balanced layout) runs the groups without the per-group slot-count checks, so the
+    // compiler may issue the next group's gathers under the current group's FMAs.
     __device__ __forceinline__ void operate(float (&acc)[BT], const unsigned char* hs, int n_w,
                                             const unsigned char* hs2 = nullptr) const {
+#ifdef SRNN_OPERATE_NOGUARD
+        if (n_w >= NP)
+            operate_groups<false>(acc, hs, n_w, hs2);
+        else
+#endif
+            operate_groups<true>(acc, hs, n_w, hs2);
+    }
+    template <bool GUARD>
+    __device__ __forceinline__ void operate_groups(float (&acc)[BT], const unsigned char* hs, int n_w,
+                                                   const unsigned char* hs2) const {
 #pragma unroll
         for (int i0 = 0; i0 < NP; i0 += GS) {
-            if (i0 < n_w) {
+            if (!GUARD || i0 < n_w) {
                 if (BT == 16) {
                     uint4 ha[GS], hb[GS];
 #pragma unroll
@@ -666,7 +678,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // MT = 0: the sparse kernel (NP register slots per lane); MT = -1: the same with 8 poll
-// slots per thread (plans whose threads own more chunks than poll_slots).  MT >= 1: the dense
+// slots per thread (plans whose threads own more chunks than poll_slots); MT = -2: the sparse
+// kernel of a column-split plan (2-CTA clusters; compiled separately so the other instances
+// carry none of its code).  MT >= 1: the dense
 // tensor-core comparator (NP register A fragments per lane, MT row tiles).
 template <int NP, int BT, int G, bool F16, int MT = 0>
 __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16, BT>::value, 1)
@@ -691,7 +705,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     // zs: one BT-row of reduced sums per (virtual) row -- heavy rows split into pieces
     // (class balancing) have several, summed in the epilogue
     const int zrows = max(G * p.units_max, p.vrows_max);
-    const bool CS = !DENSE && p.csplit != 0;  // column split over a 2-CTA cluster
+    constexpr bool CS = MT == -2;  // column split over a 2-CTA cluster (p.csplit)
     const int crank = cta & 1;                // rank in the cluster (column half) when CS
     if (CS) {  // the column split needs the 2-CTA cluster launch (srnn_api.cpp / launch_one)
         uint32_t ncl, rk;
@@ -783,8 +797,9 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
 #ifdef SRNN_DBG_CS_NODSMEM
             peer = 0.0f; (void)la; (void)ra;
 #else
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(crank ^ 1));
-            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(peer) : "r"(ra) : "memory");
+            // (no memory clobber: the cluster barrier before the epilogue orders these reads)
+            asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(crank ^ 1));
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(peer) : "r"(ra));
 #endif
             const float mine = *a;
             return crank == 0 ? mine + peer : peer + mine;
@@ -955,7 +970,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     const bool prof_on = (p.flags & kFlagProfile) && p.profile != nullptr;
 #endif
     const int n_loaders = p.loader_threads > 0 ? min(p.loader_threads, nt) : nt;
-    Poller<F16, BT, poll_slots(NP, F16, BT, MT < 0), DENSE> poll;
+    Poller<F16, BT, poll_slots(NP, F16, BT, MT == -1), DENSE> poll;
 
     for (int s = 1; s <= p.T; ++s) {
         for (int k = 0; k < p.n_tiles; ++k) {
@@ -1291,6 +1306,20 @@ int launch_np(int bt, int g, const RecParams& p, int num_ctas, size_t smem, void
 #define SRNN_CASE(BT_, G_)                                                                                    \
     if (bt == BT_ && g == G_)                                                                                 \
         return launch_one<NP, BT_, G_, F16>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out);
+    if (p.csplit) {  // column split (MT = -2): tiles of <= 8 samples
+#define SRNN_CS(BT_)                                                                                          \
+    if (bt == BT_) {                                                                                          \
+        if (g == 1) return launch_one<NP, BT_, 1, F16, -2>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out); \
+        if (g == 3) return launch_one<NP, BT_, 3, F16, -2>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out); \
+        if (g == 4) return launch_one<NP, BT_, 4, F16, -2>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out); \
+    }
+        SRNN_CS(1)
+        SRNN_CS(2)
+        SRNN_CS(4)
+        if constexpr (F16) { SRNN_CS(8) }
+#undef SRNN_CS
+        return static_cast<int>(cudaErrorInvalidValue);
+    }
     if constexpr (F16) {  // plans whose threads own more chunks than the default slots: 8 poll slots
         if (p.k8) {
 #define SRNN_K8(BT_)                                                                                          \

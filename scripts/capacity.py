@@ -38,7 +38,7 @@ def main():
                     help="Fig. 2b analogue (PAPER.md:151): largest on-chip H per density, one JSON line each")
     a = ap.parse_args()
     if a.curve:
-        for d in (0.01, 0.02, 0.05, 0.10, 0.20, 0.30, 0.50, 1.0):
+        for d in (0.0025, 0.005, 0.01, 0.02, 0.05, 0.10, 0.20, 0.30, 0.50, 1.0):
             lo, hi = 256, 65536
             if not fits(lo, d, a.B, a.prec, a.device):
                 print(json.dumps({"density": d, "H_max": None}), flush=True)
