@@ -126,7 +126,8 @@ def main():
                     rec["ours_us_per_step"] = 1000 * ms / T
                     rec["ours_eff_gflops"] = 2 * prob["nnz"] * B * T / (ms * 1e-3) / 1e9
                     rec["plan"] = {k: inf[k] for k in ("num_ctas", "threads_per_cta", "lanes_per_row", "pairs_per_lane",
-                                                       "image_slots_per_lane", "batch_tile", "num_batch_tiles")}
+                                                       "image_slots_per_lane", "batch_tile", "num_batch_tiles", "column_split")}
+                    rec["no_auto_split"] = os.environ.get("SRNN_NO_AUTO_SPLIT") is not None
                     m.close()
                 except SrnnError as e:
                     rec["ours"] = f"not on chip / unsupported: {e}"
