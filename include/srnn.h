@@ -131,6 +131,18 @@ typedef enum { SRNN_PREC_FP32 = 0, SRNN_PREC_FP16W_FP32ACC = 1 } srnn_prec_t;
                                               (the 16-bit staged offsets cover twice the columns) and
                                               a faster load phase at large H.  RNN / LSTM / GRU cells,
                                               batch tiles <= 8; not with CLASS_BALANCE / DENSE_TC  */
+#define SRNN_FLAG_STAGED         (1u << 14) /* partial progress ("the load stage can make
+                                              partial progress as values are marked complete, allowing
+                                              the operate stage to proceed before all values are
+                                              finished"): each warp's slots are packed in two stages,
+                                              the pairs whose column lies in the exchange chunks the
+                                              loaders fetch first, then the rest; the kernel stages the
+                                              early chunks, operates on the early slots while the late
+                                              chunks are still in flight, then completes the late stage.
+                                              fp16 mode, batch tiles of 4 / 8, register-resident plans
+                                              with one poll batch; ignored (plan_query staged = 0)
+                                              where it does not apply.  Results are identical up to fp
+                                              reassociation (a row's sum is taken in another order) */
 #define SRNN_FLAG_DENSE_TC       (1u << 8) /* comparator: the DENSE persistent
                                               RNN of PAPER.md:51-71 (Sec. 3.2, Diamos et al.)
                                               re-done for sm_100a tensor cores.  U_r is densified
@@ -193,6 +205,9 @@ typedef struct {
                                   chosen compiled instance; 0 for a spill-free instance  (L) */
     int32_t column_split;      /* 1: SRNN_FLAG_COLUMN_SPLIT plan (2-CTA clusters)             */
     int32_t column_half;       /* column split: first column of the second half (units)      */
+    int32_t staged;            /* 1: partial-progress plan (SRNN_FLAG_STAGED): each warp's slots
+                                  are ordered early chunks first, late chunks second     (L) */
+    int32_t early_chunks;      /* staged plans: 16-byte exchange chunks of the early stage   (L) */
 } srnn_plan_info_t;
 
 /* Create a plan for the layer described by *cfg.

@@ -35,6 +35,7 @@ FLAG_FP32_TC_GEMM = 1 << 10
 FLAG_Y_BATCH_MAJOR = 1 << 11
 FLAG_CLASS_BALANCE = 1 << 12
 FLAG_COLUMN_SPLIT = 1 << 13
+FLAG_STAGED = 1 << 14
 
 EXPORTED = ["srnn_plan_create", "srnn_plan_query", "srnn_load_weights", "srnn_forward", "srnn_input_projection",
             "srnn_recurrence", "srnn_forward_host", "srnn_plan_status", "srnn_plan_export_layout",
@@ -66,7 +67,7 @@ class PlanInfo(ctypes.Structure):
                  "image_slots_per_lane", "model_cycles_per_step")] + \
                [(n, ctypes.c_int32) for n in
                 ("dense_m_tiles", "dense_kblocks_per_warp", "dense_frags_reg", "dense_frags_smem", "spill_bytes",
-                 "column_split", "column_half")]
+                 "column_split", "column_half", "staged", "early_chunks")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

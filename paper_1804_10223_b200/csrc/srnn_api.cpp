@@ -49,6 +49,10 @@ struct srnn_plan {
     int32_t* d_piece0 = nullptr;          // class balancing: pieces of heavy rows (Layout::piece0)
     std::vector<int32_t> unit_of_pos, pos_of_unit;  // chosen layout's permutation (empty = identity)
     int32_t* d_wslots = nullptr;
+    // partial progress (SRNN_FLAG_STAGED): two-stage slot order, early-stage slots per warp
+    bool staged = false;
+    int early_chunks = 0;
+    int32_t* d_wearly = nullptr;
     float* d_wx = nullptr;
     // fp16 mode tensor-core GEMM: W_x and x rounded to fp16, K padded to a multiple of 8
     bool tc_gemm = false;
@@ -177,6 +181,7 @@ void free_device(srnn_plan* p) {
     cudaFree(p->d_perm);
     cudaFree(p->d_piece0);
     cudaFree(p->d_wslots);
+    cudaFree(p->d_wearly);
     cudaFree(p->d_wx);
     cudaFree(p->d_wx16);
     cudaFree(p->d_x16);
@@ -567,6 +572,8 @@ srnn_status_t srnn_plan_query(srnn_plan_t p, srnn_plan_info_t* out) {
     out->fits = 1;
     out->column_split = p->csplit ? 1 : 0;
     out->column_half = p->csplit ? p->hsplit : 0;
+    out->staged = p->staged ? 1 : 0;
+    out->early_chunks = p->staged ? p->early_chunks : 0;
     if (p->loaded) {
         const Layout& l = p->lay;
         out->num_ctas = l.num_ctas;
@@ -746,15 +753,17 @@ search_again:
     // Compiled instances whose registers spill are avoided (SURVEY Sec. 8 d-vi: 0 spill bytes):
     // the search takes the next wider register instance that fits, and only if no spill-free
     // plan exists at all does it accept a spilling one (second pass).
-    auto spills = [&](int inst, bool k8) -> bool {
+    auto spills = [&](int inst, bool k8, bool staged = false) -> bool {
         if (p->host_only) return false;
-        const int key = inst * 128 + p->BT * 4 + (k8 ? 2 : 0) + (p->f16 ? 1 : 0) + (p->csplit ? 64 : 0);
+        const int key = inst * 256 + p->BT * 4 + (k8 ? 2 : 0) + (p->f16 ? 1 : 0) + (p->csplit ? 64 : 0) + (staged ? 128 : 0);
         for (auto& kv : p->spill_cache)
             if (kv.first == key) return kv.second;
         RecParams q{};
         q.threads = 32;
         q.k8 = k8 ? 1 : 0;
         q.csplit = p->csplit ? 1 : 0;
+        static const int32_t dummy_early = 0;  // selects the staged instance (query only, never read)
+        q.warp_early = staged ? &dummy_early : nullptr;
         int regs[2] = {0, 0};
         const bool sp = launch_recurrent(inst, p->BT, G, p->f16 ? 1 : 0, q, 1, 0, nullptr, true, regs, nullptr) == 0 &&
                         regs[1] > 0;
@@ -900,6 +909,48 @@ search_again:
         goto search_again;
     }
     if (!any) return SRNN_ERR_NOT_ON_CHIP;
+    // Partial progress (SRNN_FLAG_STAGED): re-pack the chosen (CTAs, lanes per row)
+    // with each warp's slots in two stages -- the pairs whose column lies in the first
+    // early_chunks exchange chunks (the chunks every loader thread fetches first, j = 0), then
+    // the rest -- at the smallest slot budget that fits a compiled staged instance.
+    p->staged = false;
+    p->early_chunks = 0;
+    {
+        bool want = (p->cfg.flags & SRNN_FLAG_STAGED) != 0;
+        if (const char* es = std::getenv("SRNN_STAGED")) want = std::atoi(es) != 0;  // A/B override
+        const int64_t chunks = exchange_tile_bytes(H, p->f16, p->BT) / 16;
+        if (plan_log && want)
+            std::fprintf(stderr, "srnn plan staged: f16=%d BT=%d ns=%d csplit=%d chunks=%lld K=%d threads=%d\n", p->f16,
+                         p->BT, best_ns, p->csplit, static_cast<long long>(chunks), poll_slots(best_inst, true, p->BT, false),
+                         best.threads);
+        if (want && p->f16 && (p->BT == 4 || p->BT == 8) && best_ns == 0 && !p->csplit && !in.naive &&
+            chunks <= static_cast<int64_t>(poll_slots(best_inst, true, p->BT, false)) * best.threads) {
+            int64_t ec = std::min<int64_t>(best.threads, chunks / 2);
+            if (const char* e = std::getenv("SRNN_EARLY_CHUNKS")) ec = std::atoi(e);
+            if (ec > 0 && ec < chunks) {
+                use_perm(best_perm_c);
+                PackInput si = in;
+                si.early_pos = static_cast<int32_t>(ec * 16 / p->E);
+                si.early_align = operate_group_slots(true, p->BT);
+                for (int np = best.np_budget; np <= best.np_budget + 12; ++np) {
+                    Layout sl;
+                    if (!pack_layout(si, best.num_ctas, best.lanes_per_row, np, &sl)) continue;
+                    const int inst = inst_for(std::max(1, sl.slots_used), true, p->BT);
+                    if (plan_log)
+                        std::fprintf(stderr, "srnn plan staged: np=%d slots=%d inst=%d wf=%lld\n", np, sl.slots_used, inst,
+                                     static_cast<long long>(sl.wavefronts_max_cta));
+                    if (inst < 0 || !staged_compiled(inst, true, p->BT) ||
+                        sl.threads > max_threads_for(inst, true, p->BT) || (spill_strict && spills(inst, false, true)))
+                        break;
+                    best = std::move(sl);
+                    best_inst = inst;
+                    p->staged = true;
+                    p->early_chunks = static_cast<int>(ec);
+                    break;
+                }
+            }
+        }
+    }
     // Re-pack at the chosen instance width so the image has np_inst slots.
     Layout fin;
     {
@@ -939,7 +990,7 @@ search_again:
         const int ksmall = poll_slots(best_inst, p->f16, p->BT, false);
         const int64_t chunks = exchange_tile_bytes(H, p->f16, p->BT) / 16;  // 16-byte chunks per tile
         const int64_t c = (chunks + best.threads - 1) / best.threads;       // per thread
-        p->k8 = !p->csplit && k8_compiled(best_inst, p->f16, p->BT) && ksmall < 8 &&
+        p->k8 = !p->csplit && !p->staged && k8_compiled(best_inst, p->f16, p->BT) && ksmall < 8 &&
                 (c + 7) / 8 < (c + ksmall - 1) / ksmall;
         if (p->k8 && spills(best_inst, true) && !spills(best_inst, false)) p->k8 = false;  // spill-free first
     }
@@ -969,7 +1020,8 @@ search_again:
         cudaFree(p->d_wx);
         cudaFree(p->d_bias);
         p->d_img = nullptr;
-        p->d_unit0 = p->d_wslots = nullptr;
+        cudaFree(p->d_wearly);
+        p->d_unit0 = p->d_wslots = p->d_wearly = nullptr;
         p->d_wx = p->d_bias = nullptr;
         cudaError_t e = cudaSuccess;
         if (p->dense) {
@@ -1025,6 +1077,11 @@ search_again:
             e = cudaMemcpy(p->d_vunit0, l.cta_unit0.data(), l.cta_unit0.size() * 4, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMalloc(&p->d_wslots, l.warp_slots.size() * 4);
         if (e == cudaSuccess) e = cudaMemcpy(p->d_wslots, l.warp_slots.data(), l.warp_slots.size() * 4, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess && p->staged) {
+            e = cudaMalloc(&p->d_wearly, l.warp_early.size() * 4);
+            if (e == cudaSuccess)
+                e = cudaMemcpy(p->d_wearly, l.warp_early.data(), l.warp_early.size() * 4, cudaMemcpyHostToDevice);
+        }
         if (e == cudaSuccess) e = cudaMalloc(&p->d_wx, wx_n * 4);
         if (e == cudaSuccess) e = cudaMemcpy(p->d_wx, wx, wx_n * 4, cudaMemcpyHostToDevice);
         cudaFree(p->d_wx16);
@@ -1091,6 +1148,7 @@ search_again:
         RecParams rp{};
         rp.threads = l.threads;
         rp.k8 = p->k8 ? 1 : 0;
+        rp.warp_early = p->staged ? p->d_wearly : nullptr;  // the staged instance's registers
         rp.csplit = p->csplit ? 1 : 0;  // cluster co-residency check
         int regs[2] = {0, 0}, maxb = 0;
         int le = p->dense ? launch_dense(p->dense_inst, p->dense_mt, p->BT, G, rp, l.num_ctas, p->smem_bytes, nullptr,
@@ -1218,6 +1276,8 @@ static srnn_status_t recurrence_impl(srnn_plan_t p, int32_t T, int32_t B, const 
     rp.piece0 = p->dense ? nullptr : p->d_piece0;
     rp.vrows_max = p->lay.vrows_max;
     rp.warp_slots = p->d_wslots;
+    rp.warp_early = p->staged && !p->dense ? p->d_wearly : nullptr;
+    rp.early_chunks = p->early_chunks;
     rp.bprime = bprime;
     rp.h0 = h0;
     rp.c0 = p->G == 4 ? c0 : nullptr;

@@ -45,6 +45,10 @@ struct RecParams {
     const int32_t* piece0;     // [cta][G*units_max + 1] first virtual row of each local row (split heavy rows), or null
     int32_t vrows_max;         // virtual rows of the largest CTA (zs rows)
     const int32_t* warp_slots; // [num_ctas][warps] slots used by each warp (warp-uniform)
+    // staged instance (MT = -3): slots [0, warp_early) read only hs positions of the first
+    // early_chunks exchange chunks; the rest read the others
+    const int32_t* warp_early; // [num_ctas][warps], or null
+    int32_t early_chunks;
     // data
     const float* bprime;  // [T][B][G*H]
     const float* h0;      // [B][H] or null
@@ -156,6 +160,11 @@ SRNN_HD constexpr int poll_slots(int np, bool f16, int bt, bool k8) {
          : !f16                         ? SRNN_LOADK_F32
          : (np <= 48 ? 8 : 4);
 }
+// Slots per operate group of the fp16 kernel (all gathers of a group issue before its FMAs).
+SRNN_HD constexpr int operate_group_slots(bool f16, int bt) { return f16 ? (bt == 16 ? 2 : bt >= 4 ? 4 : 8) : (bt == 4 ? 4 : 8); }
+// Staged instance (MT = -3, partial progress): the operate of the early exchange
+// chunks overlaps the arrival of the late ones.  Compiled for fp16 tiles of 4 and 8 samples.
+SRNN_HD constexpr bool staged_compiled(int np, bool f16, int bt) { return f16 && (bt == 4 || bt == 8) && np <= 48; }
 // largest register instance compiled with the 16-sample tile (fp16, two hs planes)
 constexpr int kMaxNP16 = 48;
 // An 8-poll-slot instance exists for this (np, precision, tile)?  Must match launch_np.

@@ -169,6 +169,9 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
     lay.val.assign(n_img, 0.0f);
     lay.row.assign(n_img, -1);
     lay.warp_slots.assign(static_cast<size_t>(C) * lay.warps, 0);
+    const bool staged = in.early_pos > 0 && !in.naive;
+    if (staged) lay.warp_early.assign(static_cast<size_t>(C) * lay.warps, 0);
+    auto early = [&](int32_t c) -> bool { return (pos_of ? pos_of[c] : c) < in.early_pos; };
 
     std::vector<RowState> rows(rpw);
     std::vector<int32_t> gcol(P);       // column used per residue in current (slot, group); -1 none
@@ -193,23 +196,47 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
             for (int q = 0; q < rpw; ++q) {
                 RowState& rs = rows[q];
                 rs.grow = -1;
-                rs.remaining = 0;
                 rs.lane0 = q * L;
-                rs.bucket.assign(P, {});
-                rs.head.assign(P, 0);
                 if (q >= nr) continue;
                 rs.grow = vrows[k0 + q].grow;
                 const int64_t b = vrows[k0 + q].b, e = vrows[k0 + q].e;
-                rs.remaining = e - b;
                 pairs_cta += e - b;
                 if (e - b > static_cast<int64_t>(L) * NP) return false;
-                for (int64_t p = b; p < e; ++p) rs.bucket[key(in.col[p]) % P].push_back(p);
             }
-            // slot-major fill
+            // stages (PackInput::early_pos): the early stage takes slots [0, n_early) with the
+            // pairs of early columns only, the late stage the rest; one stage = [0, NP)
+            int n_early = 0;
+            if (staged) {
+                int64_t mx = 0;
+                for (int q = 0; q < nr; ++q) {
+                    int64_t n = 0;
+                    for (int64_t p = vrows[k0 + q].b; p < vrows[k0 + q].e; ++p) n += early(in.col[p]);
+                    mx = std::max(mx, n);
+                }
+                const int a = std::max(1, in.early_align);
+                n_early = (static_cast<int>((mx + L - 1) / L) + a - 1) / a * a;
+                if (n_early > NP) return false;
+            }
             int used_slots = 0;
             int64_t wf_warp = 0;
             std::vector<int64_t> wf_slot(NP, 0), conf_slot(NP, 0);
-            for (int i = 0; i < NP; ++i) {
+            for (int stage = 0; stage < (staged ? 2 : 1); ++stage) {
+            const int i_lo = stage == 0 ? 0 : n_early, i_hi = staged && stage == 0 ? n_early : NP;
+            for (int q = 0; q < rpw; ++q) {
+                RowState& rs = rows[q];
+                rs.remaining = 0;
+                rs.bucket.assign(P, {});
+                rs.head.assign(P, 0);
+                if (q >= nr) continue;
+                for (int64_t p = vrows[k0 + q].b; p < vrows[k0 + q].e; ++p) {
+                    if (staged && early(in.col[p]) != (stage == 0)) continue;
+                    rs.bucket[key(in.col[p]) % P].push_back(p);
+                    rs.remaining++;
+                }
+                if (rs.remaining > static_cast<int64_t>(L) * (i_hi - i_lo)) return false;
+            }
+            // slot-major fill
+            for (int i = i_lo; i < i_hi; ++i) {
                 bool any_real = false;
                 for (int g = 0; g < ng; ++g) {
                     const int gl0 = g * P, gl1 = gl0 + P;
@@ -278,7 +305,7 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
                             RowState& rs = rows[q];
                             const int lanes_later_groups =
                                 std::max(0, rs.lane0 + L - std::max(gl1, rs.lane0));  // lanes of q in groups > g
-                            int64_t quota = rs.remaining - (static_cast<int64_t>(NP - i - 1) * L + lanes_later_groups);
+                            int64_t quota = rs.remaining - (static_cast<int64_t>(i_hi - i - 1) * L + lanes_later_groups);
                             for (int l = std::max(gl0, rs.lane0); l < std::min(gl1, rs.lane0 + L) && quota > 0; ++l) {
                                 if (lane_used[l - gl0]) continue;
                                 int best = -1;
@@ -324,6 +351,11 @@ bool pack_layout(const PackInput& in, int C, int L, int NP, Layout* out) {
             }
             for (int q = 0; q < nr; ++q)
                 if (rows[q].remaining != 0) return false;
+            }  // stages
+            if (staged) {
+                used_slots = std::max(used_slots, n_early);  // the late stage starts at n_early
+                lay.warp_early[static_cast<size_t>(c) * lay.warps + w] = n_early;
+            }
             for (int i = 0; i < used_slots; ++i) {
                 wf_warp += wf_slot[i];
                 conf_cta += conf_slot[i];

@@ -27,6 +27,14 @@ struct PackInput {
     // the even split c*H/C.  The column split (SRNN_FLAG_COLUMN_SPLIT) packs a virtual matrix whose
     // units are (cluster unit, column half) and needs both CTAs of a pair to own equally many.
     const int32_t* cta_unit0 = nullptr;
+    // Partial progress ("the load stage can make partial progress as values are
+    // marked complete, allowing the operate stage to proceed before all values are finished"):
+    // > 0 = every warp's slots are ordered in two stages, first all pairs whose column sits at an
+    // hs position < early_pos (the exchange chunks the loaders fetch first), then the rest, so the
+    // kernel can operate on the early stage while the late chunks are still in flight.  The
+    // stage boundary is warp-uniform (Layout::warp_early).  0 = one stage.
+    int32_t early_pos = 0;
+    int32_t early_align = 1;  // the early stage's slot count is rounded up to this (operate group)
 };
 
 // Class-based assignment of units to CTAs ("define a number of classes for
@@ -45,6 +53,7 @@ struct Layout {
     int32_t slots_used = 0;  // max over warps of used slots
     std::vector<int32_t> cta_unit0;   // [num_ctas+1]
     std::vector<int32_t> warp_slots;  // [num_ctas*warps]
+    std::vector<int32_t> warp_early;  // [num_ctas*warps] slots of the early stage (PackInput::early_pos), or empty
     // per (cta, slot < np_budget, thread): column, value, owning global row (-1 idle)
     std::vector<int32_t> col;
     std::vector<float> val;

@@ -192,9 +192,12 @@ struct Poller {
         }
     }
 
+    // sel: the chunks j of the (single) batch to complete now (the staged instance completes the
+    // early chunks, operates on them, then completes the rest); ~0 = all
     __device__ __forceinline__ bool complete(const ulonglong2* __restrict__ src, unsigned char* hs, int n_chunks,
                                              uint32_t tag, bool spin, int32_t* status, unsigned long long timeout_ns,
-                                             uint32_t backoff_ns, int nt, int* rounds, long long* t_first) {
+                                             uint32_t backoff_ns, int nt, int* rounds, long long* t_first,
+                                             uint32_t sel = ~0u) {
         const unsigned long long want = tag ? M : 0ull;
         Watchdog wd{0ull, 0u};
         for (int base = threadIdx.x; base < n_chunks; base += K * nt) {
@@ -221,7 +224,16 @@ struct Poller {
                     if (*rounds == 0 && t_first) *t_first = clock64();
                     ++*rounds;
                 }
-                if (pend == 0u) break;
+                if ((pend & sel) == 0u) {
+                    // the selected chunks are staged; the other still-stale ones go out again
+                    // now so they are in flight during the caller's next work (staged instance)
+                    if (pend != 0u) {
+#pragma unroll
+                        for (int j = 0; j < K; ++j)
+                            if ((pend >> j) & 1u) v[j] = ld_relaxed_v2(src + base + j * nt);
+                    }
+                    break;
+                }
                 if (!spin) {
                     atomicCAS(status, 0, -4 /* protocol violation -> SRNN_ERR_STATE */);
                     return true;
@@ -376,7 +388,7 @@ struct Weights<NP, BT, false> {
 // 16-byte units for BT = 8 (E = 16: the column index itself, any H <= 65536).
 template <int NP, int BT>
 struct Weights<NP, BT, true> {
-    static constexpr int GS = BT == 16 ? 2 : BT >= 4 ? 4 : 8;
+    static constexpr int GS = operate_group_slots(true, BT);
     uint32_t pw[NP];
     __device__ __forceinline__ void load(const RecParams& p, size_t img0, int n_w) {
 #pragma unroll
@@ -389,17 +401,22 @@ struct Weights<NP, BT, true> {
                                             const unsigned char* hs2 = nullptr) const {
 #ifdef SRNN_OPERATE_NOGUARD
         if (n_w >= NP)
-            operate_groups<false>(acc, hs, n_w, hs2);
+            operate_groups<false>(acc, hs, 0, n_w, hs2);
         else
 #endif
-            operate_groups<true>(acc, hs, n_w, hs2);
+            operate_groups<true>(acc, hs, 0, n_w, hs2);
+    }
+    // Slots [lo, hi) only (the staged instance: lo and hi are multiples of GS, warp-uniform).
+    __device__ __forceinline__ void operate_span(float (&acc)[BT], const unsigned char* hs, int lo, int hi,
+                                                 const unsigned char* hs2 = nullptr) const {
+        operate_groups<true>(acc, hs, lo, hi, hs2);
     }
     template <bool GUARD>
-    __device__ __forceinline__ void operate_groups(float (&acc)[BT], const unsigned char* hs, int n_w,
+    __device__ __forceinline__ void operate_groups(float (&acc)[BT], const unsigned char* hs, int lo, int n_w,
                                                    const unsigned char* hs2) const {
 #pragma unroll
         for (int i0 = 0; i0 < NP; i0 += GS) {
-            if (!GUARD || i0 < n_w) {
+            if (!GUARD || (i0 >= lo && i0 < n_w)) {
                 if (BT == 16) {
                     uint4 ha[GS], hb[GS];
 #pragma unroll
@@ -971,6 +988,18 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
 #endif
     const int n_loaders = p.loader_threads > 0 ? min(p.loader_threads, nt) : nt;
     Poller<F16, BT, poll_slots(NP, F16, BT, MT == -1), DENSE> poll;
+    // staged instance (partial progress): this thread's early chunks (chunk
+    // tid + j * n_loaders < early_chunks; one poll batch, host-checked) and its warp's
+    // early slots [0, n_we)
+    constexpr bool STAGED = MT == -3;
+    uint32_t sel_early = 0u;
+    int n_we = 0;
+    if constexpr (STAGED) {
+#pragma unroll
+        for (int j = 0; j < poll_slots(NP, F16, BT, false); ++j)
+            if (tid + j * n_loaders < p.early_chunks) sel_early |= 1u << j;
+        n_we = p.warp_early[cta * (p.threads >> 5) + warp];
+    }
 
     for (int s = 1; s <= p.T; ++s) {
         for (int k = 0; k < p.n_tiles; ++k) {
@@ -1006,15 +1035,32 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
 
             if (!kEarlyPoll && tid < n_loaders) poll.issue(src, tid, n_ch, n_loaders);
             bool failed = bp_failed;
+            float acc_early[BT];  // staged instance: the early slots' partial sums
+#pragma unroll
+            for (int b = 0; b < BT; ++b) acc_early[b] = 0.0f;
+            if constexpr (STAGED) {
+                // early chunks -> hs, barrier, operate on the early slots while the late chunks
+                // (issued in the same poll batch) are still arriving, then complete those
+                if (tid < n_loaders && !poll.complete(src, hs, n_ch, (g_prev >> 1) & 1u, !grid_sync, p.status,
+                                                      p.timeout_ns, p.poll_backoff_ns, n_loaders, nullptr, nullptr,
+                                                      sel_early))
+                    failed = true;
+                __syncthreads();
+                SRNN_STAMP(13, clock64());
+#ifndef SRNN_ABL_NO_OP
+                W.operate_span(acc_early, hs, 0, n_we);
+#endif
+                SRNN_STAMP(14, clock64());
+            }
             if (tid < n_loaders &&
                 !poll.complete(src, hs, n_ch, (g_prev >> 1) & 1u, !grid_sync, p.status, p.timeout_ns,
                                p.poll_backoff_ns, n_loaders,
 #ifdef SRNN_PROFILE
-                               prof_all ? &rounds : nullptr, prof ? prof + 10 : nullptr
+                               prof_all ? &rounds : nullptr, prof ? prof + 10 : nullptr,
 #else
-                               nullptr, nullptr
+                               nullptr, nullptr,
 #endif
-                               ))
+                               STAGED ? ~sel_early : ~0u))
                 failed = true;
 #ifdef SRNN_PROFILE
             if (prof_all) atomicMax(reinterpret_cast<unsigned long long*>(prof_all + 9), static_cast<unsigned long long>(rounds));
@@ -1054,10 +1100,14 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
             } else {
                 float acc[BT];
 #pragma unroll
-                for (int b = 0; b < BT; ++b) acc[b] = 0.0f;
+                for (int b = 0; b < BT; ++b) acc[b] = acc_early[b];
 #ifndef SRNN_ABL_NO_OP  // A/B ablation builds only (scripts/abl.sh): phase costs
-                W.operate(acc, hs, n_w, hs2);
-                if (n_w > NP) operate_smem_tier<BT, F16>(acc, hs, ws, NP, n_w, nt, hs2);
+                if constexpr (STAGED) {
+                    W.operate_span(acc, hs, n_we, n_w);  // the late slots (no smem tier: host-checked)
+                } else {
+                    W.operate(acc, hs, n_w, hs2);
+                    if (n_w > NP) operate_smem_tier<BT, F16>(acc, hs, ws, NP, n_w, nt, hs2);
+                }
 #endif
                 SRNN_STAMP(4, clock64());
                 // ---- reduce over the row's L lanes, fixed order ----
@@ -1319,6 +1369,20 @@ int launch_np(int bt, int g, const RecParams& p, int num_ctas, size_t smem, void
         if constexpr (F16) { SRNN_CS(8) }
 #undef SRNN_CS
         return static_cast<int>(cudaErrorInvalidValue);
+    }
+    if constexpr (staged_compiled(NP, F16, 4)) {  // staged plans (partial progress): MT = -3
+        if (p.warp_early != nullptr) {
+#define SRNN_ST(BT_)                                                                                          \
+    if (bt == BT_) {                                                                                          \
+        if (g == 1) return launch_one<NP, BT_, 1, F16, -3>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out); \
+        if (g == 3) return launch_one<NP, BT_, 3, F16, -3>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out); \
+        if (g == 4) return launch_one<NP, BT_, 4, F16, -3>(p, num_ctas, smem, stream, query_only, regs_out, max_blocks_out); \
+    }
+            SRNN_ST(4)
+            SRNN_ST(8)
+#undef SRNN_ST
+            return static_cast<int>(cudaErrorInvalidValue);
+        }
     }
     if constexpr (F16) {  // plans whose threads own more chunks than the default slots: 8 poll slots
         if (p.k8) {

@@ -66,6 +66,10 @@ skew = pub - pub.min(axis=0, keepdims=True)
 # per step: latest publish of step s-1 -> this CTA's load end of step s
 lat = flat[:, 1:, 12] - pub.max(axis=0, keepdims=True)[:, :-1]
 period = flat[:, 1:, 0] - flat[:, :-1, 0]
+# staged plans (SRNN_FLAG_STAGED): early chunks staged (13), early slots operated (14)
+early_load = flat[:, :, 13] - flat[:, :, 0]
+early_op = flat[:, :, 14] - flat[:, :, 13]
+late_wait = flat[:, :, 1] - flat[:, :, 14]
 sk = 8 * nt
 res = {"cfg": vars(a), "plan": {k: inf[k] for k in ("num_ctas", "threads_per_cta", "lanes_per_row", "pairs_per_lane",
                                                      "slots_used", "batch_tile", "wavefronts_per_step_max")}}
@@ -73,6 +77,8 @@ for name, v in (("load", load[:, sk:]), ("operate", oper[:, sk:]), ("op_loop", o
                 ("butterfly", butterfly[:, sk:]), ("bprime_wait", bwait[:, sk:]), ("barrier2", bar2[:, sk:]), ("epilogue", epi[:, sk:]), ("gap", gap[:, sk:]), ("bar3", bar3[:, sk:]), ("loop", loop[:, sk:]),
                 ("first_round", first_round[:, sk:]), ("rounds0", rounds0[:, sk:]), ("rounds_max", rounds_max[:, sk:]),
                 ("pub_skew_ns", skew[:, sk:]), ("lastpub_to_loaded_ns", lat[:, sk:]),
-                ("tile_period", period[:, sk:])):
+                ("tile_period", period[:, sk:])) + (
+                (("early_load", early_load[:, sk:]), ("early_operate", early_op[:, sk:]), ("late_wait", late_wait[:, sk:]))
+                if inf.get("staged") else ()):
     res[name] = {"median": float(np.median(v)), "p10": float(np.percentile(v, 10)), "p90": float(np.percentile(v, 90))}
 print(json.dumps(res))

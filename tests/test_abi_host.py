@@ -278,3 +278,45 @@ def test_class_balance_layout_reconstructs_and_balances(pattern, cell, prec):
     assert max_cta_pairs(rowb, valb) <= max_cta_pairs(row, val)
     if pattern == "skewed":
         assert max_cta_pairs(rowb, valb) - mean < 0.5 * (max_cta_pairs(row, val) - mean)
+
+
+@pytest.mark.parametrize("H,B,d,cell,pattern", [
+    (2304, 4, 0.30, "rnn", "unstructured"),    # C2 headline shape
+    (1152, 4, 0.10, "rnn", "unstructured"),    # Table 1 shape
+    (1024, 4, 0.125, "lstm", "row_balanced"),  # C4 NMT LSTM
+    (2304, 8, 0.10, "rnn", "unstructured"),    # tile of 8
+    (301, 4, 0.2, "gru", "unstructured"),      # ragged
+])
+def test_staged_layout_orders_early_chunks_first(H, B, d, cell, pattern):
+    """SRNN_FLAG_STAGED (PAPER.md:103 partial progress): each warp's slots hold first only
+    pairs whose column lies in the early exchange chunks (hs position < early_chunks * 16 / E),
+    then only the others; the early stage ends at a multiple of the operate group (4 slots for
+    tiles of 4 / 8); the layout still reconstructs U_r exactly (PAPER.md:100 reordering)."""
+    from paper_1804_10223_b200 import FLAG_STAGED
+    prob = inputs.make_problem(H, H, B, 4, d, cell=cell, pattern=pattern)
+    m = host_plan(prob, "fp16", flags=FLAG_STAGED)
+    inf = m.info()
+    assert inf["staged"] == 1 and inf["early_chunks"] > 0
+    dense, cnt, (col, val, row) = reconstruct(m, prob)
+    q = prob["val"].astype(np.float16).astype(np.float64)
+    assert np.array_equal(dense, csr_dense(prob, q))
+    assert cnt.max() <= 1 and cnt.sum() == np.count_nonzero(q)  # (values that round to fp16 zero drop out)
+    E = 2 * inf["batch_tile"]
+    early_pos = inf["early_chunks"] * 16 // E
+    C, S, nt = col.shape
+    real = (row >= 0) & (val != 0)
+    w = col.reshape(C, S, nt // 32, 32)
+    rl = real.reshape(C, S, nt // 32, 32)
+    early = w < early_pos
+    slot = np.arange(S)[None, :, None, None]
+    # per (cta, warp): the last slot holding a real early pair < the first slot holding a real late pair
+    last_early = np.where(rl & early, slot, -1).max(axis=(1, 3))
+    first_late = np.where(rl & ~early, slot, S).min(axis=(1, 3))
+    assert (last_early < first_late).all()
+    # the late stage starts on an operate-group boundary (multiple of 4 slots)
+    has_late = first_late < S
+    assert (first_late[has_late] % 4 == 0).all()
+    # unstaged plan of the same problem: the staged one needs at most a few more slots
+    m0 = host_plan(prob, "fp16")
+    assert m0.info()["staged"] == 0
+    assert inf["slots_used"] <= m0.info()["slots_used"] + 8

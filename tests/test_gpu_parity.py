@@ -832,3 +832,61 @@ def test_column_split_capacity_beyond_frontier(cuda_device, monkeypatch, H, d):
     assert from_problem(prob, prec="fp16", flags=FLAG_HOST_ONLY).info()["column_split"] == 1
     g, o, err = check(prob, "fp16", flags=FLAG_COLUMN_SPLIT)
     print(H, d, g["info"])
+
+
+# ---- partial progress (SRNN_FLAG_STAGED) ----
+@pytest.mark.parametrize("cell,H,B,T,d,act,pattern", [
+    ("rnn", 2304, 4, 24, 0.30, "relu", "unstructured"),    # C2 shape, short T
+    ("rnn", 1152, 4, 40, 0.10, "tanh", "unstructured"),    # Table 1 shape
+    ("rnn", 1200, 4, 17, 0.05, "identity", "unstructured"),  # low density
+    ("lstm", 1024, 4, 20, 0.125, "tanh", "row_balanced"),  # C4 NMT shape
+    ("gru", 777, 4, 15, 0.2, "tanh", "unstructured"),      # ragged H
+    ("rnn", 2304, 8, 16, 0.30, "relu", "unstructured"),    # tile of 8
+    ("rnn", 1500, 13, 9, 0.1, "tanh", "unstructured"),     # several tiles, ragged (may fall back)
+])
+def test_staged_parity(cuda_device, cell, H, B, T, d, act, pattern):
+    """The staged plan (early chunks staged and operated on while the late chunks arrive) vs the
+    oracle on every output, and vs the one-stage plan (same values up to fp reassociation).  The
+    ragged multi-tile case may fall back to one stage (its staged instance spills: the planner
+    keeps the spill-free one); the rest must be staged."""
+    from paper_1804_10223_b200 import FLAG_STAGED
+    prob = inputs.make_problem(H, H, B, T, d, cell=cell, act=act, pattern=pattern, h0="random", c0="random",
+                               seed_offset=H + B)
+    g, o, err = check(prob, "fp16", flags=FLAG_STAGED)
+    assert g["info"]["staged"] == 1 or B == 13, g["info"]
+    g0 = run_gpu(prob, "fp16")
+    assert g0["info"]["staged"] == 0
+    assert np.abs(g["y"] - g0["y"]).max() <= TOL["fp16"]
+
+
+def test_staged_integer_exact_and_deterministic(cuda_device):
+    """Integer-exact inputs: the staged plan equals the oracle bit for bit, with and without
+    per-CTA jitter (the early/late barrier order cannot change a value)."""
+    from paper_1804_10223_b200 import FLAG_STAGED
+    prob = inputs.make_integer_problem(1200, 64, 4, 12, 0.05, act="identity")
+    o = oracle.forward(prob)
+    a = run_gpu(prob, "fp16", flags=FLAG_STAGED)
+    assert a["info"]["staged"] == 1
+    assert np.array_equal(a["y"].astype(np.float64), o["y"])
+    b = run_gpu(prob, "fp16", flags=FLAG_STAGED | FLAG_DEBUG_JITTER)
+    assert np.array_equal(a["y"], b["y"])
+
+
+def test_staged_lost_message_watchdog(cuda_device, monkeypatch):
+    """A lost exchange message under the staged plan: the early or late wait times out, the
+    launch reports SRNN_ERR_TIMEOUT instead of hanging, and a fresh staged plan is correct."""
+    import torch
+
+    from paper_1804_10223_b200 import FLAG_STAGED, SrnnError
+    from paper_1804_10223_b200._lib import FLAG_DEBUG_DROP_PUBLISH
+    monkeypatch.setenv("SRNN_TIMEOUT_MS", "200")
+    prob = inputs.make_problem(1152, 1152, 4, 8, 0.1, act="tanh")
+    m = from_problem(prob, prec="fp16", flags=FLAG_STAGED | FLAG_DEBUG_DROP_PUBLISH)
+    assert m.info()["staged"] == 1
+    m.forward(torch.from_numpy(prob["x"]).cuda())
+    torch.cuda.synchronize()
+    with pytest.raises(SrnnError) as e:
+        m.status()
+    assert e.value.code == -6
+    m.close()
+    check(prob, "fp16", flags=FLAG_STAGED)
