@@ -61,6 +61,8 @@ struct srnn_plan {
     void* d_x16 = nullptr;  // [T_max*B_max][k_pad]
     alignas(64) CUtensorMap map_x16;
     alignas(64) CUtensorMap map_wx16;
+    alignas(64) CUtensorMap map_wx16_32;  // W_x in 32 / 48-row boxes (the 4-CTA multicast clusters' B slices)
+    alignas(64) CUtensorMap map_wx16_48;
     // fp32 mode: 3xTF32 tensor-core GEMM on tf32 hi/lo splits of x and W_x, K padded to 4
     bool tf32x3 = false;
     int k_pad4 = 0;
@@ -1127,6 +1129,8 @@ search_again:
             if (e == cudaSuccess) e = cudaMalloc(&p->d_x16, xrows * p->k_pad * 2);
             // A (x) in 128-row boxes, B (W_x) in 64-row boxes (tile widths 128 / 192 / 256)
             if (e == cudaSuccess && (!encode_fp16_kmajor(&p->map_wx16, p->d_wx16, R, p->k_pad, 64) ||
+                                     !encode_fp16_kmajor(&p->map_wx16_32, p->d_wx16, R, p->k_pad, 32) ||
+                                     !encode_fp16_kmajor(&p->map_wx16_48, p->d_wx16, R, p->k_pad, 48) ||
                                      !encode_fp16_kmajor(&p->map_x16, p->d_x16, xrows, p->k_pad, 128)))
                 return SRNN_ERR_CUDA;
         }
@@ -1178,7 +1182,7 @@ static srnn_status_t project_rows(srnn_plan_t p, int64_t r0, int64_t M, const fl
                               : launch_f32_to_f16_padded(x + r0 * I, x16, M, I, p->k_pad, stream);
         if (e == 0)
             e = launch_gemm_tc(&p->map_x16, &p->map_wx16, p->d_bias, bprime, static_cast<int>(M), N, p->k_pad, stream,
-                               static_cast<int>(r0), 0, sms);
+                               static_cast<int>(r0), 0, sms, &p->map_wx16_32, &p->map_wx16_48);
         return e == 0 ? SRNN_OK : SRNN_ERR_CUDA;
     }
     if (p->tf32x3) {

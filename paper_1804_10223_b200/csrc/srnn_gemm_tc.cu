@@ -59,6 +59,19 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+// The same, multicast to every CTA of the cluster in cta_mask (same shared-memory offsets; each
+// destination's mbarrier at that offset receives the complete_tx bytes).
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t cta_mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, "
+        "%4}], [%2], %5;" ::"r"(su32(dst)),
+        "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "h"(cta_mask)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 // UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row groups 1024 B apart.
 __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
     const uint64_t addr = su32(p);
@@ -82,6 +95,7 @@ struct TcCfg {
     static constexpr uint32_t STAGE_BYTES = (X3 ? 2 : 1) * (TC_TILE_BYTES + B_BYTES);
     static constexpr int STAGES = static_cast<int>((200u * 1024u) / STAGE_BYTES);  // ~200 KB in flight
     static constexpr uint32_t TMEM_COLS = BN == 128 ? 256 : 512;  // two accumulators (power-of-2 allocation)
+    static constexpr uint32_t ACC_STRIDE = BN <= 128 ? 128 : 256;  // TMEM column of accumulator 1
     static constexpr size_t SMEM = STAGES * STAGE_BYTES + 1024 /* align */ + 256 /* barriers */;
 };
 
@@ -95,12 +109,30 @@ struct TcCfg {
 // and D += A_hi B_hi + A_hi B_lo + A_lo B_hi, dropping only A_lo B_lo (~2^-22 of
 // each product) -- fp32-level accuracy for the 1e-5 parity bound, with K in
 // steps of 8 tf32 elements (32 bytes, the same descriptor advance as fp16 K=16).
-template <int BN, bool X3 = false>
+//
+// CM > 1: thread-block clusters of CM CTAs along M share the W_x tile of their common n0: the
+// B operand of every K-block is fetched once per cluster and multicast into all CM CTAs'
+// shared memory (CTA rank r loads B slices r, r + CM, ... of SLICE rows), cutting the L2 -> SM
+// operand traffic that bounds the projection at M = T*B = 1024.  A stage is
+// refilled only when all CM CTAs' MMAs have read it: every MMA commit arrives on the empty
+// barrier of each CTA of the cluster (empty counts CM arrivals).
+template <int BN, bool X3 = false, int CM = 1>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_f16_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                        const float* __restrict__ bias, float* __restrict__ C, int M, int N, int K, int m_off,
-                       const __grid_constant__ CUtensorMap map_a_lo, const __grid_constant__ CUtensorMap map_b_lo) {
+                       const __grid_constant__ CUtensorMap map_a_lo, const __grid_constant__ CUtensorMap map_b_lo,
+                       const __grid_constant__ CUtensorMap map_b32) {
     using Cfg = TcCfg<BN, X3>;
+    static_assert(CM == 1 || !X3, "multicast clusters: fp16 operands only");
+    // B slices: 64-row boxes (map_b); with clusters, CM slices of BN / CM rows (map_b32: 32-row
+    // boxes for BN = 128, CM = 4) or, for BN = 144, three 48-row slices (map_b32 then holds
+    // 48-row boxes; rank 3 loads none)
+    constexpr int SLICE = BN == 144 ? 48 : BN / (CM > BN / 64 ? CM : BN / 64);
+    constexpr int NSL = BN / SLICE;
+    static_assert(BN % SLICE == 0 && (CM == 1 || NSL <= CM || NSL % CM == 0), "B slices");
+    constexpr uint16_t kMask = static_cast<uint16_t>((1u << CM) - 1u);
+    uint32_t crank = 0;
+    if constexpr (CM > 1) asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
     constexpr int STAGES = Cfg::STAGES;
     constexpr uint32_t kIdesc = idesc_f16<BN, X3>();
     constexpr int KB_ELEMS = X3 ? TC_BK / 2 : TC_BK;  // elements of K per 128-byte row
@@ -119,12 +151,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nk = (K + KB_ELEMS - 1) / KB_ELEMS;
     const int tiles_n = (N + BN - 1) / BN;
-    const int n_tiles = tiles_n * ((M + TC_BM - 1) / TC_BM);
+    // (cluster) tiles: CM vertically adjacent 128-row tiles with one n0; CTA rank r takes row
+    // tile group * CM + r (rows past M are zero-filled by TMA and never stored)
+    const int n_tiles = tiles_n * (((M + TC_BM - 1) / TC_BM + CM - 1) / CM);
+    const int t0 = static_cast<int>(blockIdx.x) / CM, t_step = static_cast<int>(gridDim.x) / CM;
+    auto tile_m0 = [&](int t) { return ((t / tiles_n) * CM + static_cast<int>(crank)) * TC_BM; };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], CM);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
@@ -146,14 +182,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if constexpr (CM > 1) cluster_sync_all();  // every CTA's barriers exist before any multicast
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0 && lane == 0) {
         // ---- TMA producer ----
         int it = 0;
-        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-            const int m0 = (t / tiles_n) * TC_BM, n0 = (t % tiles_n) * BN;
+        for (int t = t0; t < n_tiles; t += t_step) {
+            const int m0 = tile_m0(t), n0 = (t % tiles_n) * BN;
             for (int kb = 0; kb < nk; ++kb, ++it) {
                 const int s = it % STAGES;
                 if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
@@ -161,6 +198,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const int a_stride = TC_TILE_BYTES * (X3 ? 2 : 1), b_stride = Cfg::B_BYTES * (X3 ? 2 : 1);
                 tma_load_2d(sA + s * a_stride, &map_a, &full[s], kb * KB_ELEMS, m_off + m0);
                 if (X3) tma_load_2d(sA + s * a_stride + TC_TILE_BYTES, &map_a_lo, &full[s], kb * KB_ELEMS, m_off + m0);
+                if constexpr (CM > 1) {  // this rank's B slices, multicast to the whole cluster
+#pragma unroll
+                    for (int j = 0; j < NSL; ++j)
+                        if (j % CM == static_cast<int>(crank))
+                            tma_load_2d_mc(sB + s * b_stride + j * SLICE * 128, SLICE == 64 ? &map_b : &map_b32,
+                                           &full[s], kb * KB_ELEMS, n0 + SLICE * j, kMask);
+                    continue;
+                }
 #pragma unroll
                 for (int j = 0; j < BN / 64; ++j) {  // rows past N are zero-filled by TMA
                     tma_load_2d(sB + s * b_stride + j * (TC_TILE_BYTES / 2), &map_b, &full[s], kb * KB_ELEMS,
@@ -174,11 +219,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer: D[tmem acc] (+)= A[smem] * B[smem]^T ----
         int it = 0, lt = 0;
-        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+        for (int t = t0; t < n_tiles; t += t_step, ++lt) {
             const int acc = lt & 1;
             if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) - 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t d_tmem = tmem + static_cast<uint32_t>(acc * BN);
+            const uint32_t d_tmem = tmem + static_cast<uint32_t>(acc) * Cfg::ACC_STRIDE;
             for (int kb = 0; kb < nk; ++kb, ++it) {
                 const int s = it % STAGES;
                 mbar_wait(&full[s], (it / STAGES) & 1);
@@ -207,10 +252,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             : "memory");
                     }
                 }
-                // free the smem stage once these MMAs have read it
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 su32(&empty[s]))
-                             : "memory");
+                // free the smem stage once these MMAs have read it (CM > 1: in every CTA of the
+                // cluster, whose producers multicast into this stage)
+                if constexpr (CM > 1)
+                    asm volatile(
+                        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                        "%1;" ::"r"(su32(&empty[s])),
+                        "h"(kMask)
+                        : "memory");
+                else
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                     su32(&empty[s]))
+                                 : "memory");
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                              su32(&tfull[acc]))
@@ -220,9 +273,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // ---- epilogue: TMEM -> registers -> + bias -> global ----
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
         int lt = 0;
-        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+        for (int t = t0; t < n_tiles; t += t_step, ++lt) {
             const int acc = lt & 1;
-            const int m0 = (t / tiles_n) * TC_BM, n0 = (t % tiles_n) * BN;
+            const int m0 = tile_m0(t), n0 = (t % tiles_n) * BN;
             const int row = m0 + quarter * 32 + lane;
             mbar_wait(&tfull[acc], (lt >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -230,7 +283,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int c = 0; c < BN; c += 32) {
                 uint32_t v[32];
                 const uint32_t taddr =
-                    tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * BN + c);
+                    tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc) * Cfg::ACC_STRIDE +
+                    static_cast<uint32_t>(c);
                 asm volatile(
                     "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
                     "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -248,7 +302,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 }
                 if (row < M) {
                     float* crow = C + static_cast<size_t>(m_off + row) * N + n0 + c;
-                    const int nvalid = min(32, N - (n0 + c));
+                    const int nvalid = min(min(32, BN - c), N - (n0 + c));  // BN = 144: a 16-column last chunk
                     if (nvalid == 32 && (N & 3) == 0) {
 #pragma unroll
                         for (int j = 0; j < 32; j += 4) {
@@ -270,6 +324,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    // no CTA leaves while a peer's last MMA commit may still arrive on its barriers
+    if constexpr (CM > 1) cluster_sync_all();
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cfg::TMEM_COLS)
@@ -331,11 +387,16 @@ __global__ void split_tf32_kernel(const float* __restrict__ in, float* __restric
 // Force module loading of the projection kernels (CUDA lazy loading would
 // otherwise load them at first launch, which can stall behind a running
 // persistent kernel that is waiting for their output).
+static int fit_clusters_144x4();
 int preload_projection_kernels() {
     cudaFuncAttributes a;
     cudaError_t e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel<128>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel<192>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel<256>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel<128, false, 2>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel<128, false, 4>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel<144, false, 4>);
+    if (e == cudaSuccess) (void)fit_clusters_144x4();  // occupancy query once, outside any stream capture
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, gemm_tc_f16_kernel<128, true>);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, split_tf32_kernel);
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, f32_to_f16_kernel);
@@ -351,24 +412,49 @@ int launch_f32_to_f16(const float* in, void* out, int64_t n, void* stream) {
     return static_cast<int>(cudaGetLastError());
 }
 
-template <int BN, bool X3 = false>
+template <int BN, bool X3 = false, int CM = 1>
 static int launch_gemm_tc_bn(const void* map_a, const void* map_b, const float* bias, float* C, int M, int N, int K,
                              cudaStream_t stream, int m_off, int sms, const void* map_a_lo = nullptr,
-                             const void* map_b_lo = nullptr) {
+                             const void* map_b_lo = nullptr, const void* map_b32 = nullptr) {
     // The shared-memory opt-in is a per-device function attribute: set it on every launch
     // (cheap, thread-safe; a process may drive plans on several devices).
     const size_t smem = TcCfg<BN, X3>::SMEM;
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_f16_kernel<BN, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    auto fn = gemm_tc_f16_kernel<BN, X3, CM>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return static_cast<int>(e);
-    const int64_t tiles = static_cast<int64_t>((N + BN - 1) / BN) * ((M + TC_BM - 1) / TC_BM);
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
+    const int64_t tiles = static_cast<int64_t>((N + BN - 1) / BN) * (((M + TC_BM - 1) / TC_BM + CM - 1) / CM);
     const CUtensorMap& ma = *static_cast<const CUtensorMap*>(map_a);
     const CUtensorMap& mb = *static_cast<const CUtensorMap*>(map_b);
-    gemm_tc_f16_kernel<BN, X3><<<grid, TC_THREADS, smem, stream>>>(
-        ma, mb, bias, C, M, N, K, m_off, X3 ? *static_cast<const CUtensorMap*>(map_a_lo) : ma,
-        X3 ? *static_cast<const CUtensorMap*>(map_b_lo) : mb);
-    return static_cast<int>(cudaGetLastError());
+    const CUtensorMap& ma_lo = X3 ? *static_cast<const CUtensorMap*>(map_a_lo) : ma;
+    const CUtensorMap& mb_lo = X3 ? *static_cast<const CUtensorMap*>(map_b_lo) : mb;
+    const CUtensorMap& mb32 = map_b32 ? *static_cast<const CUtensorMap*>(map_b32) : mb;
+    if constexpr (CM == 1) {
+        const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
+        fn<<<grid, TC_THREADS, smem, stream>>>(ma, mb, bias, C, M, N, K, m_off, ma_lo, mb_lo, mb32);
+        return static_cast<int>(cudaGetLastError());
+    } else {
+        // clusters of CM CTAs; the persistent grid holds at most as many clusters as fit at once
+        cudaLaunchConfig_t lc = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CM;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.blockDim = dim3(TC_THREADS);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = stream;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        lc.gridDim = dim3(static_cast<unsigned>(CM * std::max(1, sms / CM)));
+        int fit = 0;
+        e = cudaOccupancyMaxActiveClusters(&fit, fn, &lc);
+        if (e != cudaSuccess) return static_cast<int>(e);
+        const int64_t ncl = std::max<int64_t>(1, std::min<int64_t>({tiles, static_cast<int64_t>(sms / CM),
+                                                                    static_cast<int64_t>(std::max(1, fit))}));
+        lc.gridDim = dim3(static_cast<unsigned>(CM * ncl));
+        e = cudaLaunchKernelEx(&lc, fn, ma, mb, bias, C, M, N, K, m_off, ma_lo, mb_lo, mb32);
+        return static_cast<int>(e);
+    }
 }
 
 // fp32 mode: 3xTF32 tcgen05 GEMM on pre-split operands (tf32 hi / lo as fp32 arrays).
@@ -391,11 +477,59 @@ int launch_split_tf32(const float* in, float* hi, float* lo, int64_t rows, int c
 // the busiest CTA: ceil(tiles / sms) x (128 + bn) rows of K -- 128 when the
 // 128-wide grid fits in one wave, wider when the launch has few SMs (the
 // pipelined projections on the SMs the persistent kernel leaves free).
+// Clusters of 4 CTAs of the BN = 144 multicast instance that fit on the device at once (per
+// device, cached; a benign race writes the same value).
+static int fit_clusters_144x4() {
+    static int cache[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
+    if (cache[dev] > 0) return cache[dev];
+    auto fn = gemm_tc_f16_kernel<144, false, 4>;
+    const size_t smem = TcCfg<144>::SMEM;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+        return 0;
+    cudaLaunchConfig_t lc = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 4;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.gridDim = dim3(4);
+    lc.blockDim = dim3(TC_THREADS);
+    lc.dynamicSmemBytes = smem;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    int fit = 0;
+    if (cudaOccupancyMaxActiveClusters(&fit, fn, &lc) != cudaSuccess) return 0;
+    cache[dev] = fit;
+    return fit;
+}
+
 int launch_gemm_tc(const void* map_a, const void* map_b, const float* bias, float* C, int M, int N, int K,
-                   void* stream, int m_off, int bn, int sms) {
+                   void* stream, int m_off, int bn, int sms, const void* map_b32, const void* map_b48) {
     if (M <= 0 || N <= 0) return 0;
     if (const char* e = std::getenv("SRNN_GEMM_SMS")) sms = std::atoi(e);  // experiment: cap the grid
     sms = std::max(1, sms);
+    const char* env_cm = std::getenv("SRNN_GEMM_CM");
+    const char* env_bn = std::getenv("SRNN_GEMM_BN");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // Opt-in (SRNN_GEMM_CM=4): 144-wide tiles in 4-CTA clusters along M that multicast their W_x
+    // tile, when all cluster tiles fit in one wave (C2: 2 x 16 = 32 <= 33 clusters).  Per CTA,
+    // A 128 x K + a quarter of B 144 x K instead of 128 x K + 128 x K.  Measured on B200 (C2,
+    // ncu): 26.4 us vs 21.8 us for the unclustered 128-wide kernel although the L2 sectors fall
+    // 117 -> 82 MB -- L2 already merges the unicast reads of CTAs that fetch the same W_x tile
+    // at the same time (B300_MICROARCH: multicast ~ unicast at cluster size <= 4) and the
+    // cluster-wide stage release couples the four CTAs' pipelines.
+    if (bn == 0 && map_b48 != nullptr && sms >= 128 && !env_bn && env_cm && std::atoi(env_cm) == 4) {
+        const int64_t ctiles = static_cast<int64_t>((M + 4 * TC_BM - 1) / (4 * TC_BM)) * ((N + 143) / 144);
+        const int fit = fit_clusters_144x4();
+        if (ctiles >= 8 && ctiles <= std::min(fit, sms / 4))
+            return launch_gemm_tc_bn<144, false, 4>(map_a, map_b, bias, C, M, N, K, st, m_off, sms, nullptr, nullptr,
+                                                    map_b48);
+    }
+    if (env_bn && std::atoi(env_bn) == 144 && map_b48 != nullptr)  // forced (tests)
+        return launch_gemm_tc_bn<144, false, 4>(map_a, map_b, bias, C, M, N, K, st, m_off, sms, nullptr, nullptr,
+                                                map_b48);
     if (bn == 0) {
         const int64_t tm = (M + TC_BM - 1) / TC_BM;
         int64_t best = -1;
@@ -409,7 +543,12 @@ int launch_gemm_tc(const void* map_a, const void* map_b, const float* bias, floa
         }
         if (const char* e = std::getenv("SRNN_GEMM_BN")) bn = std::atoi(e);
     }
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // 128-wide tiles in clusters of 2 / 4 along M (experiments / tests only: at C2 the 128-wide
+    // cluster tiles do not fit in one wave, measured slower than CM = 1)
+    const int cm = env_cm ? std::atoi(env_cm) : 1;
+    if (bn == 128 && cm == 2) return launch_gemm_tc_bn<128, false, 2>(map_a, map_b, bias, C, M, N, K, st, m_off, sms);
+    if (bn == 128 && cm == 4 && map_b32 != nullptr)
+        return launch_gemm_tc_bn<128, false, 4>(map_a, map_b, bias, C, M, N, K, st, m_off, sms, nullptr, nullptr, map_b32);
     switch (bn) {
         case 192: return launch_gemm_tc_bn<192>(map_a, map_b, bias, C, M, N, K, st, m_off, sms);
         case 256: return launch_gemm_tc_bn<256>(map_a, map_b, bias, C, M, N, K, st, m_off, sms);

@@ -120,7 +120,8 @@ int launch_dense(int nf, int mt, int bt, int g, const RecParams& p, int num_ctas
 int launch_gemm_f32(const GemmParams& p, void* stream);
 // fp16 tensor-core input GEMM (srnn_gemm_tc.cu); maps are CUtensorMap*.
 int launch_gemm_tc(const void* map_a, const void* map_b, const float* bias, float* C, int M, int N, int K,
-                   void* stream, int m_off = 0, int bn = 0, int sms = 148);
+                   void* stream, int m_off = 0, int bn = 0, int sms = 148, const void* map_b32 = nullptr,
+                   const void* map_b48 = nullptr);  // W_x maps in 32 / 48-row boxes (multicast clusters)
 // rows [m_off, m_off + M) of A and C; bn = tile width (0: pick from the grid size vs `sms`, the SMs it may use)
 int launch_f32_to_f16(const float* in, void* out, int64_t n, void* stream);
 // fp32 mode: 3xTF32 tcgen05 GEMM on tf32 hi/lo splits (maps: fp32 K-major, 32-element boxes)
