@@ -194,6 +194,15 @@ struct Poller {
 
     // sel: the chunks j of the (single) batch to complete now (the staged instance completes the
     // early chunks, operates on them, then completes the rest); ~0 = all
+    // The first poll round from hoisted addresses (chunk j at ptr + j * js bytes, valid j in
+    // jmask): nothing but the loads between the post-publish barrier and the round trip.
+    __device__ __forceinline__ void issue_at(const unsigned char* ptr, uint32_t jmask, uint32_t js) {
+        pend = jmask;
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if ((jmask >> j) & 1u) v[j] = ld_relaxed_v2(reinterpret_cast<const ulonglong2*>(ptr + j * js));
+    }
+
     __device__ __forceinline__ bool complete(const ulonglong2* __restrict__ src, unsigned char* hs, int n_chunks,
                                              uint32_t tag, bool spin, int32_t* status, unsigned long long timeout_ns,
                                              uint32_t backoff_ns, int nt, int* rounds, long long* t_first,
@@ -743,6 +752,20 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     const bool bp_tma = G == 1 && p.bp_tma != 0;  // RNN cells only (the gate cells keep cp.async: registers)
 #endif
     const int boxu = p.bp_boxu;
+#ifndef SRNN_GENERIC_SMEM_PTRS
+    // carve-up by byte offsets from the shared array (aligned in the shared window), so every
+    // pointer below stays in the shared state space: LDS / STS, not generic loads, in the
+    // epilogue's b' read and the abort-flag read after the staging barrier
+    const uint32_t sm_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    const uint32_t cs_end = static_cast<uint32_t>(
+        reinterpret_cast<unsigned char*>(cs + (G >= 3 ? p.n_tiles * umax_bt : 0)) - smem);
+    const uint32_t bp_al = bp_tma ? 127u : 0u;  // TMA destination: 128-byte aligned
+    float* bpw = reinterpret_cast<float*>(smem + (((sm_base + cs_end + bp_al) & ~bp_al) - sm_base));
+    uint64_t* bp_mbar = reinterpret_cast<uint64_t*>(bpw + (bp_tma ? 2 * G * kBpWin * BT * boxu : 0));
+    int* s_abort = reinterpret_cast<int*>(bp_mbar + (bp_tma ? 2 : 0));
+    const uint32_t ab_end = static_cast<uint32_t>(reinterpret_cast<unsigned char*>(s_abort + 1) - smem);
+    unsigned char* ws = smem + (((sm_base + ab_end + 15u) & ~15u) - sm_base);  // smem weight tier
+#else
     float* bpw = reinterpret_cast<float*>(  // TMA destination: 128-byte aligned
         (reinterpret_cast<uintptr_t>(cs + (G >= 3 ? p.n_tiles * umax_bt : 0)) + (bp_tma ? 127 : 0)) &
         ~static_cast<uintptr_t>(bp_tma ? 127 : 0));
@@ -750,6 +773,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     int* s_abort = reinterpret_cast<int*>(bp_mbar + (bp_tma ? 2 : 0));
     unsigned char* ws = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(s_abort + 1) + 15) & ~static_cast<uintptr_t>(15));  // smem weight tier
+#endif
 
     const int L = DENSE ? 32 : p.lanes_per_row;
     const int n_w = DENSE ? 0 : p.warp_slots[cta * (p.threads >> 5) + warp];
@@ -988,6 +1012,24 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
 #endif
     const int n_loaders = p.loader_threads > 0 ? min(p.loader_threads, nt) : nt;
     Poller<F16, BT, poll_slots(NP, F16, BT, MT == -1), DENSE> poll;
+    // A/B build option (-DSRNN_HOIST_POLL): the first poll round's addresses, the exchange
+    // store address, the global step and the y pointer hoisted out of the time loop (RNN cells,
+    // instances of <= 512 threads).  Measured on two boxes against the shared-space carve-up
+    // alone: C2 2.225 vs 2.230 us/step, B = 8 2.946 vs 3.035, C4 LSTM 2.061 vs 2.087 (C2 2.28 ->
+    // 2.20 on the first box came from the carve-up, not the hoist): off by default.
+#ifdef SRNN_HOIST_POLL
+    constexpr bool kHoistPoll = G == 1 && MaxThreadsBT<NP, F16, BT>::value <= 512 && MT <= 0;
+#else
+    constexpr bool kHoistPoll = false;
+#endif
+    const unsigned char* poll0 = p.xbuf + (static_cast<size_t>(c_lo) + tid) * 16;
+    const uint32_t poll_par = static_cast<uint32_t>(p.xbuf_tiles) * static_cast<uint32_t>(p.tile_bytes);
+    const uint32_t poll_js = static_cast<uint32_t>(n_loaders) * 16u;
+    unsigned char* const pub0 = p.xbuf + xo_e1;  // this thread's exchange value of tile 0, parity 0 (RNN fast path)
+    uint32_t poll_jmask = 0u;
+#pragma unroll
+    for (int j = 0; j < poll_slots(NP, F16, BT, MT == -1); ++j)
+        if (tid + j * n_loaders < n_ch) poll_jmask |= 1u << j;
     // staged instance (partial progress): this thread's early chunks (chunk
     // tid + j * n_loaders < early_chunks; one poll batch, host-checked) and its warp's
     // early slots [0, n_we)
@@ -1001,6 +1043,15 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
         n_we = p.warp_early[cta * (p.threads >> 5) + warp];
     }
 
+    // RNN fast-path epilogue state in two registers instead of per-step parameter / special
+    // register reloads (the compiler rematerialised them at 128 registers): bit 0 this thread
+    // owns an item, 1 the lost-message test hook, 2 its warp has items or pad values to publish,
+    // 3 y is written; the running global step of h_{s-1}; y of step s for tile 0
+    constexpr uint32_t kEpiItem = 1u, kEpiDrop = 2u, kEpiWarp = 4u, kEpiY = 8u;
+    const uint32_t epi_ctl = (e1_ok ? kEpiItem : 0u) | (drop_cta ? kEpiDrop : 0u) |
+                             ((warp * 32 < max(n_items, n_pad)) ? kEpiWarp : 0u) | (y_e1 != nullptr ? kEpiY : 0u);
+    uint32_t g_run = p.epoch;
+    float* y_run = y_e1;
     for (int s = 1; s <= p.T; ++s) {
         for (int k = 0; k < p.n_tiles; ++k) {
 #ifdef SRNN_PROFILE
@@ -1012,7 +1063,8 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
 #endif
             SRNN_STAMP(0, clock64());
             // ---- load: h_{s-1} tile k -> hs; the first poll round goes out first ----
-            const uint32_t g_prev = p.epoch + static_cast<uint32_t>(s - 1);  // global step of h_{s-1}
+            // global step of h_{s-1}
+            const uint32_t g_prev = kHoistPoll ? g_run : p.epoch + static_cast<uint32_t>(s - 1);
             // column split: only the chunks of this CTA's column half [c_lo, c_lo + n_ch)
             const ulonglong2* src = reinterpret_cast<const ulonglong2*>(
                 p.xbuf + static_cast<size_t>((g_prev & 1u) * p.xbuf_tiles + k) * p.tile_bytes) + c_lo;
@@ -1021,7 +1073,13 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
             // per thread, whose registers would stay live across it (measured: slower), so they
             // poll after it
             constexpr bool kEarlyPoll = F16 && BT <= 4;
-            if (kEarlyPoll && tid < n_loaders) poll.issue(src, tid, n_ch, n_loaders);
+            if (kEarlyPoll && tid < n_loaders) {
+                if constexpr (kHoistPoll)
+                    poll.issue_at(poll0 + ((g_prev & 1u) ? poll_par : 0u) + static_cast<uint32_t>(k) * p.tile_bytes,
+                                  poll_jmask, poll_js);
+                else
+                    poll.issue(src, tid, n_ch, n_loaders);
+            }
             // b' of the NEXT tile -> shared memory (cp.async, double-buffered) while the
             // poll loads are in flight; it lands during this whole tile (this tile's b'
             // was issued one tile earlier)
@@ -1033,7 +1091,13 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                 cp_async_commit();
             }
 
-            if (!kEarlyPoll && tid < n_loaders) poll.issue(src, tid, n_ch, n_loaders);
+            if (!kEarlyPoll && tid < n_loaders) {
+                if constexpr (kHoistPoll)
+                    poll.issue_at(poll0 + ((g_prev & 1u) ? poll_par : 0u) + static_cast<uint32_t>(k) * p.tile_bytes,
+                                  poll_jmask, poll_js);
+                else
+                    poll.issue(src, tid, n_ch, n_loaders);
+            }
             bool failed = bp_failed;
             float acc_early[BT];  // staged instance: the early slots' partial sums
 #pragma unroll
@@ -1211,6 +1275,23 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
             if (G == 1 && item_rounds == 1) {
                 // fast path (one item per thread, RNN): hoisted offsets; the exchange store goes
                 // out first (it is the step's critical path), y / h_T after it
+              if constexpr (kHoistPoll) {
+              if (epi_ctl & kEpiWarp) {  // warps without items go straight to the barrier
+                float h = 0.0f;
+                const uint32_t g = g_prev + 1u;  // parity g & 1, tag (g >> 1) & 1
+                if (epi_ctl & kEpiItem) h = activation<F16>(act, (pc == nullptr && !CS ? zs_e1[0] : zval(e1 / BT, e1_b)) + bpv(e1, 0));
+                if ((epi_ctl & kEpiItem) && !((epi_ctl & kEpiDrop) && s == 2))
+                    store_tagged(pub0 + ((g & 1u) ? poll_par : 0u) + static_cast<uint32_t>(k) * p.tile_bytes, 0, h,
+                                 (g >> 1) & 1u);
+                publish(s, k, e1, false, 0.0f);  // only the pad values of the last chunk (last CTA)
+                if ((epi_ctl & kEpiItem) && k * BT + e1_b < p.B) {
+#ifndef SRNN_ABL_NO_Y
+                    if (epi_ctl & kEpiY) y_run[k * BT * p.y_bstride] = h;
+#endif
+                    if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(k * BT + e1_b) * H + e1_unit] = h;
+                }
+              }
+              } else {
                 float h = 0.0f;
                 const uint32_t g = p.epoch + static_cast<uint32_t>(s);  // parity g & 1, tag (g >> 1) & 1
                 if (e1_ok) h = activation<F16>(act, (pc == nullptr && !CS ? zs_e1[0] : zval(e1 / BT, e1_b)) + bpv(e1, 0));
@@ -1227,6 +1308,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
 #endif
                     if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(k * BT + e1_b) * H + e1_unit] = h;
                 }
+              }
             } else
             for (int j = 0; j < item_rounds; ++j) {
                 const int e = tid + j * nt;
@@ -1274,6 +1356,10 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
             __syncthreads();
 #endif
             SRNN_STAMP(7, clock64());
+            if (kHoistPoll && k == p.n_tiles - 1) {
+                ++g_run;
+                if (y_run != nullptr) y_run += p.y_tstride;
+            }
             buf ^= 1;
             if (p.progress != nullptr && tid == 0 && k == p.n_tiles - 1 &&
                 (s % p.progress_every == 0 || s == p.T)) {
