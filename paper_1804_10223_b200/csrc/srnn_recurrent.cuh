@@ -302,6 +302,36 @@ __device__ __forceinline__ uint32_t xoff_lo16(uint32_t w) { return w & 0xffffu; 
 __device__ __forceinline__ uint32_t xoff_u16(uint32_t w) { return (w >> 12) & 0xffff0u; }
 #endif
 
+// Gathers by 32-bit shared-window addresses (base + offset, one LEA per slot): the generic
+// pointer form made the compiler re-derive the shared window base (S2UR CgaCtaId + ULEA) in
+// every operate group, a serialising dependency at the head of each group (ncu source view).
+// volatile: per-use address (no hoisted NP-register offset arrays), order kept vs the barriers.
+#ifndef SRNN_GENERIC_GATHER
+#define SRNN_SHARED_GATHER 1
+#endif
+__device__ __forceinline__ uint32_t xaddr_hi16(uint32_t w, uint32_t base) {  // base + byte offset (high half)
+    uint32_t a;
+    asm volatile("{\n.reg .b32 t;\nshr.b32 t, %1, 16;\nadd.u32 %0, t, %2;\n}" : "=r"(a) : "r"(w), "r"(base));
+    return a;
+}
+__device__ __forceinline__ uint32_t xaddr_u16(uint32_t w, uint32_t base) {  // base + 16-byte units (high half)
+    uint32_t a;
+    asm volatile("{\n.reg .b32 t;\nshr.b32 t, %1, 12;\nand.b32 t, t, 1048560;\nadd.u32 %0, t, %2;\n}"
+                 : "=r"(a)
+                 : "r"(w), "r"(base));
+    return a;
+}
+__device__ __forceinline__ uint2 lds_v2(uint32_t a) {
+    uint2 r;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(a));
+    return r;
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+    uint4 r;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+    return r;
+}
+
 // The operate loop runs in groups of GS slots: all GS shared-memory loads of
 // a group are issued before its FMAs (memory-level parallelism), and the
 // warp-uniform slot count n_w is checked once per group.  Slots between n_w
@@ -347,7 +377,7 @@ struct Weights<NP, BT, false> {
         }
     }
     __device__ __forceinline__ void operate(float (&acc)[BT], const unsigned char* hs, int n_w,
-                                            const unsigned char* = nullptr) const {
+                                            const unsigned char* = nullptr, uint32_t = 0u) const {
 #pragma unroll
         for (int i0 = 0; i0 < NP; i0 += GS) {
             if (i0 < n_w) {
@@ -406,23 +436,24 @@ struct Weights<NP, BT, true> {
     // hs2: the second sample plane (BT = 16 only).  A warp whose slots are all used (the common
     // case of a balanced layout) runs the groups without the per-group slot-count checks, so the
     // compiler may issue the next group's gathers under the current group's FMAs.
+    // hb: shared-window address of hs (kept in a register for the whole launch)
     __device__ __forceinline__ void operate(float (&acc)[BT], const unsigned char* hs, int n_w,
-                                            const unsigned char* hs2 = nullptr) const {
+                                            const unsigned char* hs2 = nullptr, uint32_t hb = 0u) const {
 #ifdef SRNN_OPERATE_NOGUARD
         if (n_w >= NP)
-            operate_groups<false>(acc, hs, 0, n_w, hs2);
+            operate_groups<false>(acc, hs, 0, n_w, hs2, hb);
         else
 #endif
-            operate_groups<true>(acc, hs, 0, n_w, hs2);
+            operate_groups<true>(acc, hs, 0, n_w, hs2, hb);
     }
     // Slots [lo, hi) only (the staged instance: lo and hi are multiples of GS, warp-uniform).
     __device__ __forceinline__ void operate_span(float (&acc)[BT], const unsigned char* hs, int lo, int hi,
-                                                 const unsigned char* hs2 = nullptr) const {
-        operate_groups<true>(acc, hs, lo, hi, hs2);
+                                                 const unsigned char* hs2 = nullptr, uint32_t hb = 0u) const {
+        operate_groups<true>(acc, hs, lo, hi, hs2, hb);
     }
     template <bool GUARD>
     __device__ __forceinline__ void operate_groups(float (&acc)[BT], const unsigned char* hs, int lo, int n_w,
-                                                   const unsigned char* hs2) const {
+                                                   const unsigned char* hs2, uint32_t hb) const {
 #pragma unroll
         for (int i0 = 0; i0 < NP; i0 += GS) {
             if (!GUARD || (i0 >= lo && i0 < n_w)) {
@@ -450,9 +481,15 @@ struct Weights<NP, BT, true> {
                     }
                 } else if (BT == 8) {
                     uint4 h[GS];
+#ifdef SRNN_SHARED_GATHER
+#pragma unroll
+                    for (int j = 0; j < GS; ++j)
+                        if (i0 + j < NP) h[j] = lds_v4(xaddr_u16(pw[i0 + j], hb));
+#else
 #pragma unroll
                     for (int j = 0; j < GS; ++j)
                         if (i0 + j < NP) h[j] = *reinterpret_cast<const uint4*>(hs + (xoff_u16(pw[i0 + j])));
+#endif
 #pragma unroll
                     for (int j = 0; j < GS; ++j) {
                         if (i0 + j < NP) {
@@ -469,9 +506,15 @@ struct Weights<NP, BT, true> {
                     }
                 } else if (BT == 4) {
                     uint2 h[GS];
+#ifdef SRNN_SHARED_GATHER
+#pragma unroll
+                    for (int j = 0; j < GS; ++j)
+                        if (i0 + j < NP) h[j] = lds_v2(xaddr_hi16(pw[i0 + j], hb));
+#else
 #pragma unroll
                     for (int j = 0; j < GS; ++j)
                         if (i0 + j < NP) h[j] = *reinterpret_cast<const uint2*>(hs + xoff_hi16(pw[i0 + j]));
+#endif
 #pragma unroll
                     for (int j = 0; j < GS; ++j) {
                         if (i0 + j < NP) {
@@ -781,6 +824,10 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     const int c_lo = CS && crank ? (p.hsplit * F::E) >> 4 : 0;             // first chunk this CTA stages
     const int n_ch = CS ? (crank ? n_chunks - c_lo : (p.hsplit * F::E) >> 4) : n_chunks;
     const unsigned char* hs2 = hs + H * 16;     // BT = 16: second hs plane
+    // shared-window address of hs, from an opaque cvta so the compiler keeps it in a register
+    // instead of re-deriving the window base in every operate group
+    uint32_t hs_sb;
+    asm volatile("{\n.reg .u64 t;\ncvta.to.shared.u64 t, %1;\ncvt.u32.u64 %0, t;\n}" : "=r"(hs_sb) : "l"(hs));
     const int GH = G * H;
     // values after the last unit that pad the image to whole chunks (written by the last CTA)
     const int n_pad = (cta == static_cast<int>(gridDim.x) - 1 && !(F16 && BT == 16))
@@ -1112,7 +1159,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                 __syncthreads();
                 SRNN_STAMP(13, clock64());
 #ifndef SRNN_ABL_NO_OP
-                W.operate_span(acc_early, hs, 0, n_we);
+                W.operate_span(acc_early, hs, 0, n_we, nullptr, hs_sb);
 #endif
                 SRNN_STAMP(14, clock64());
             }
@@ -1167,9 +1214,9 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                 for (int b = 0; b < BT; ++b) acc[b] = acc_early[b];
 #ifndef SRNN_ABL_NO_OP  // A/B ablation builds only (scripts/abl.sh): phase costs
                 if constexpr (STAGED) {
-                    W.operate_span(acc, hs, n_we, n_w);  // the late slots (no smem tier: host-checked)
+                    W.operate_span(acc, hs, n_we, n_w, nullptr, hs_sb);  // the late slots (no smem tier: host-checked)
                 } else {
-                    W.operate(acc, hs, n_w, hs2);
+                    W.operate(acc, hs, n_w, hs2, hs_sb);
                     if (n_w > NP) operate_smem_tier<BT, F16>(acc, hs, ws, NP, n_w, nt, hs2);
                 }
 #endif
