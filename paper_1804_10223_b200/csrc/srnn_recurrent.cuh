@@ -1078,15 +1078,15 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
 #endif
     const int n_loaders = p.loader_threads > 0 ? min(p.loader_threads, nt) : nt;
     Poller<F16, BT, poll_slots(NP, F16, BT, MT == -1), DENSE> poll;
-    // A/B build option (-DSRNN_HOIST_POLL): the first poll round's addresses, the exchange
-    // store address, the global step and the y pointer hoisted out of the time loop (RNN cells,
-    // instances of <= 512 threads).  Measured on two boxes against the shared-space carve-up
-    // alone: C2 2.225 vs 2.230 us/step, B = 8 2.946 vs 3.035, C4 LSTM 2.061 vs 2.087 (C2 2.28 ->
-    // 2.20 on the first box came from the carve-up, not the hoist): off by default.
-#ifdef SRNN_HOIST_POLL
-    constexpr bool kHoistPoll = G == 1 && MaxThreadsBT<NP, F16, BT>::value <= 512 && MT <= 0;
+    // The first poll round's addresses, the exchange store address, the global step and the y
+    // pointer hoisted out of the time loop: fp16 RNN tiles of 4 (instances of <= 512 threads).
+    // Same-box A/B with the shared-window gathers: C2 2.204 -> 2.164 us/step, 1152 @ 10% and
+    // 2304 @ 10% within noise; tiles of 8 slower (2.85 -> 3.10) and the gate cells slower
+    // (C4 LSTM 2.06 -> 2.09), so they keep the per-step form.  -DSRNN_HOIST_POLL=0 / 1 forces.
+#ifndef SRNN_HOIST_POLL
+    constexpr bool kHoistPoll = F16 && BT == 4 && G == 1 && MaxThreadsBT<NP, F16, BT>::value <= 512 && MT <= 0;
 #else
-    constexpr bool kHoistPoll = false;
+    constexpr bool kHoistPoll = SRNN_HOIST_POLL != 0 && G == 1 && MaxThreadsBT<NP, F16, BT>::value <= 512 && MT <= 0;
 #endif
     const unsigned char* poll0 = p.xbuf + (static_cast<size_t>(c_lo) + tid) * 16;
     const uint32_t poll_par = static_cast<uint32_t>(p.xbuf_tiles) * static_cast<uint32_t>(p.tile_bytes);
