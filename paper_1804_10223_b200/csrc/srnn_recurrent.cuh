@@ -1020,6 +1020,22 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     }
     const bool grid_sync = (p.flags & kFlagGridSync) != 0u;
     if (grid_sync) cg::this_grid().sync();
+    // launch-constant switches of the time loop in one register (as single flags the compiler
+    // re-loaded them from the parameter bank every step, on the step's critical path)
+    constexpr uint32_t kCtlJitter = 1u, kCtlBpTma = 2u;
+    uint32_t kctl = (jitter0 ? kCtlJitter : 0u) | (bp_tma ? kCtlBpTma : 0u);
+    // opaque: kept in a register -- RNN tiles <= 4 with a 128-register budget only (same-box
+    // A/B: C2 2.165 -> 2.115 us/step, B = 8 2.86 -> 2.83; the 96-register instances lost: 1152 @
+    // 10% 1.71 -> 1.87)
+    constexpr bool kPinCtl = G == 1 && BT <= 4 && MaxThreadsBT<NP, F16, BT>::value <= 512;
+    if constexpr (kPinCtl) asm volatile("" : "+r"(kctl));
+    // shared-window address of this lane's zs slot (fast path: L >= BT, one writer per sample)
+    int sbase0 = 0;
+    for (int lvl = 0, half = BT / 2; half >= 1; ++lvl, half /= 2)
+        if (lane & (1 << lvl)) sbase0 += half;
+    uint32_t zs_wa = static_cast<uint32_t>(__cvta_generic_to_shared(zs)) +
+                     static_cast<uint32_t>(krow * BT + sbase0) * 4u;
+    if constexpr (kPinCtl) asm volatile("" : "+r"(zs_wa));
     __syncthreads();
 
     // pipelined host forward: b' arrives in chunks of steps and the ready counter only
@@ -1029,7 +1045,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     const bool bp_pipelined = p.bp_ready != nullptr;
     // one item per thread (the common case): b' source of item e1 = tid hoisted out of the time loop
     auto issue_bprime = [&](int s, int k, int b) {
-        if (bp_tma) {  // one thread loads window w + 1 during the first step of window w (s = that step + 1)
+        if (kPinCtl ? (kctl & kCtlBpTma) != 0u : bp_tma) {  // one thread loads window w + 1 during the first step of window w (s = that step + 1)
             if (tid == 0 && (s - 2) % kBpWin == 0 && (s - 2 + kBpWin) < p.T) bp_issue((s - 2) / kBpWin + 1);
             return;
         }
@@ -1282,14 +1298,18 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                 }
                 SRNN_STAMP(5, clock64());
                 if (L >= BT) {
-                    if (zs_writer) zsp[krow * BT + sbase] = acc[0];
+                    if (CS || !kPinCtl) {
+                        if (zs_writer) zsp[krow * BT + sbase] = acc[0];
+                    } else if (zs_writer) {  // (sbase == sbase0: the same lane bits)
+                        asm volatile("st.shared.f32 [%0], %1;" ::"r"(zs_wa), "f"(acc[0]) : "memory");
+                    }
                 } else if (row_leader) {
 #pragma unroll
                     for (int b = 0; b < BT; ++b) zsp[krow * BT + b] = acc[b];
                 }
             }
             if (!CS && aborted) goto done;
-            if (bp_tma && (s - 1) % kBpWin == 0) {  // first step of a b' window: wait for its TMA load
+            if ((kPinCtl ? (kctl & kCtlBpTma) != 0u : bp_tma) && (s - 1) % kBpWin == 0) {  // first step of a b' window: wait for its TMA load
                 const int w = (s - 1) / kBpWin;
                 const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(bp_mbar + (w & 1)));
                 Watchdog wdb{0ull, 0u};
@@ -1304,7 +1324,8 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
                     if (watchdog_tick(wdb, p.status, p.timeout_ns)) break;  // the next poll aborts the launch
                 }
             }
-            asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's b' (the newest group may pend)
+            if (!kPinCtl || !(kctl & kCtlBpTma))  // (b' by TMA: no cp.async in flight)
+                asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's b' (the newest group may pend)
             SRNN_STAMP(6, clock64());
             if (CS) {
                 // both CTAs' partial sums are complete (release / acquire across the cluster); the
@@ -1334,7 +1355,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
             auto bpv = [&](int e, int q) -> float {
                 return bp_tma ? bpt[q * kBpWin * BT * boxu + (e % BT) * boxu + (u0 & 3) + e / BT] : bps[e * G + q];
             };
-            if (jitter0) {
+            if (kPinCtl ? (kctl & kCtlJitter) != 0u : jitter0) {
                 const uint32_t r = (static_cast<uint32_t>(cta) * 2654435761u) ^ (static_cast<uint32_t>(s * 40503 + k));
                 __nanosleep((r >> 7) & 2047u);
             }
@@ -1356,6 +1377,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
 #endif
                     if (s == p.T && p.hT != nullptr) p.hT[static_cast<size_t>(k * BT + e1_b) * H + e1_unit] = h;
                 }
+                if ((epi_ctl & kEpiY) && k == p.n_tiles - 1) y_run += p.y_tstride;  // (only this block uses y_run)
               }
               } else {
                 float h = 0.0f;
@@ -1422,10 +1444,7 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
             __syncthreads();
 #endif
             SRNN_STAMP(7, clock64());
-            if (kHoistPoll && k == p.n_tiles - 1) {
-                ++g_run;
-                if (y_run != nullptr) y_run += p.y_tstride;
-            }
+            if (kHoistPoll && k == p.n_tiles - 1) ++g_run;
             buf ^= 1;
             if (p.progress != nullptr && tid == 0 && k == p.n_tiles - 1 &&
                 (s % p.progress_every == 0 || s == p.T)) {
