@@ -1327,6 +1327,15 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
             if (!kPinCtl || !(kctl & kCtlBpTma))  // (b' by TMA: no cp.async in flight)
                 asm volatile("cp.async.wait_group 1;" ::: "memory");  // this tile's b' (the newest group may pend)
             SRNN_STAMP(6, clock64());
+            // fast path with b' by TMA: this item's b' is in shared memory once the window's
+            // mbarrier wait above has passed, so the epilogue warps read it before the barrier
+            // (off the chain zs -> g -> publish that follows it)
+            float bp_pre = 0.0f;
+            if constexpr (kHoistPoll) {
+                if ((kctl & kCtlBpTma) && item_rounds == 1 && (epi_ctl & kEpiItem))
+                    bp_pre = bpw[static_cast<size_t>(((s - 1) & (2 * kBpWin - 1)) * BT * boxu) + (e1 % BT) * boxu +
+                                 (u0 & 3) + e1 / BT];
+            }
             if (CS) {
                 // both CTAs' partial sums are complete (release / acquire across the cluster); the
                 // pair takes the same abort decision (own flag or the peer's) so neither waits alone
@@ -1366,7 +1375,9 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
               if (epi_ctl & kEpiWarp) {  // warps without items go straight to the barrier
                 float h = 0.0f;
                 const uint32_t g = g_prev + 1u;  // parity g & 1, tag (g >> 1) & 1
-                if (epi_ctl & kEpiItem) h = activation<F16>(act, (pc == nullptr && !CS ? zs_e1[0] : zval(e1 / BT, e1_b)) + bpv(e1, 0));
+                if (epi_ctl & kEpiItem)
+                    h = activation<F16>(act, (pc == nullptr && !CS ? zs_e1[0] : zval(e1 / BT, e1_b)) +
+                                                 ((kctl & kCtlBpTma) ? bp_pre : bpv(e1, 0)));
                 if ((epi_ctl & kEpiItem) && !((epi_ctl & kEpiDrop) && s == 2))
                     store_tagged(pub0 + ((g & 1u) ? poll_par : 0u) + static_cast<uint32_t>(k) * p.tile_bytes, 0, h,
                                  (g >> 1) & 1u);
