@@ -1105,9 +1105,9 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     constexpr bool kHoistPoll = SRNN_HOIST_POLL != 0 && G == 1 && MaxThreadsBT<NP, F16, BT>::value <= 512 && MT <= 0;
 #endif
     const unsigned char* poll0 = p.xbuf + (static_cast<size_t>(c_lo) + tid) * 16;
-    const uint32_t poll_par = static_cast<uint32_t>(p.xbuf_tiles) * static_cast<uint32_t>(p.tile_bytes);
+    uint32_t poll_par = static_cast<uint32_t>(p.xbuf_tiles) * static_cast<uint32_t>(p.tile_bytes);
     const uint32_t poll_js = static_cast<uint32_t>(n_loaders) * 16u;
-    unsigned char* const pub0 = p.xbuf + xo_e1;  // this thread's exchange value of tile 0, parity 0 (RNN fast path)
+    unsigned char* pub0 = p.xbuf + xo_e1;  // this thread's exchange value of tile 0, parity 0 (RNN fast path)
     uint32_t poll_jmask = 0u;
 #pragma unroll
     for (int j = 0; j < poll_slots(NP, F16, BT, MT == -1); ++j)
@@ -1130,8 +1130,15 @@ __global__ void __launch_bounds__(MT > 0 ? kDenseThreads : MaxThreadsBT<NP, F16,
     // owns an item, 1 the lost-message test hook, 2 its warp has items or pad values to publish,
     // 3 y is written; the running global step of h_{s-1}; y of step s for tile 0
     constexpr uint32_t kEpiItem = 1u, kEpiDrop = 2u, kEpiWarp = 4u, kEpiY = 8u;
-    const uint32_t epi_ctl = (e1_ok ? kEpiItem : 0u) | (drop_cta ? kEpiDrop : 0u) |
-                             ((warp * 32 < max(n_items, n_pad)) ? kEpiWarp : 0u) | (y_e1 != nullptr ? kEpiY : 0u);
+    uint32_t epi_ctl = (e1_ok ? kEpiItem : 0u) | (drop_cta ? kEpiDrop : 0u) |
+                       ((warp * 32 < max(n_items, n_pad)) ? kEpiWarp : 0u) | (y_e1 != nullptr ? kEpiY : 0u);
+#ifndef SRNN_NO_PIN_EPI
+    if constexpr (kHoistPoll) {  // pinned (else rematerialised from CTAID / parameter reloads every step)
+        asm volatile("" : "+r"(epi_ctl));
+        asm volatile("" : "+r"(poll_par));
+        asm volatile("" : "+l"(pub0));
+    }
+#endif
     uint32_t g_run = p.epoch;
     float* y_run = y_e1;
     for (int s = 1; s <= p.T; ++s) {
